@@ -1,0 +1,239 @@
+"""Host-side number representation shared with the reference multiply API.
+
+The reference passes operands as Python ints or as ``Natural`` (little-endian
+w-bit word lists, w thread-local, default 64; ``bigmul/words.py:17-41``,
+``bigmul/words.py:56-117``).  This module restates exactly the parts of that
+contract the DKSS entry points touch:
+
+* ``Natural`` construction / ``to_int`` / ``len`` / equality semantics
+  (``bigmul/words.py:56-109``) -- needed because ``dmul`` returns a Natural of
+  exactly ``len(a) + len(b)`` words (``bigmul/dkss.py:529,548``);
+* ``as_natural`` type checks (``bigmul/words.py:112-117``);
+* thread-local word size (``bigmul/words.py:17-41``) -- the DKSS plan depends
+  on it (d is rounded to a multiple of w, ``bigmul/dkss.py:327-328``);
+* ``ScratchArena`` accounting (``bigmul/words.py:234-304``) -- accepted by the
+  API; the GPU path records its device workspace in it;
+* ``bit_slices`` / ``join_bits`` (``bigmul/words.py:307-349``) -- the encode /
+  decode semantics, used here only by host-side helpers and tests.
+
+Conversion between ints and the u32 limb arrays that cross the C ABI is done
+with ``int.to_bytes`` / ``numpy.frombuffer`` (no per-word Python loops).
+"""
+
+from __future__ import annotations
+
+import threading
+from contextlib import contextmanager
+
+import numpy as np
+
+_WORD_SIZES = (8, 16, 32, 64)
+_tls = threading.local()
+
+
+def word_bits() -> int:
+    return getattr(_tls, "w", 64)
+
+
+def word_base() -> int:
+    return 1 << word_bits()
+
+
+def set_word_bits(w: int) -> None:
+    if w not in _WORD_SIZES:
+        raise ValueError(f"unsupported word size {w}, pick one of {_WORD_SIZES}")
+    _tls.w = w
+
+
+@contextmanager
+def using_word_bits(w: int):
+    prev = word_bits()
+    set_word_bits(w)
+    try:
+        yield
+    finally:
+        set_word_bits(prev)
+
+
+def _words_needed(value: int, w: int) -> int:
+    return max(1, -(-value.bit_length() // w))
+
+
+def int_to_words(value: int, length: int, w: int) -> list:
+    if length == 0:
+        return []
+    dt = {8: np.uint8, 16: np.uint16, 32: np.uint32, 64: np.uint64}[w]
+    raw = value.to_bytes(length * (w // 8), "little")
+    return np.frombuffer(raw, dtype=dt).tolist()
+
+
+def words_to_int(words, w: int) -> int:
+    if len(words) == 0:
+        return 0
+    dt = {8: np.uint8, 16: np.uint16, 32: np.uint32, 64: np.uint64}[w]
+    return int.from_bytes(np.asarray(words, dtype=dt).tobytes(), "little")
+
+
+class Natural:
+    """Nonnegative integer as little-endian words of the current word size.
+
+    Mirrors ``bigmul.words.Natural``: leading zero words are allowed, the
+    object is treated as immutable, equality compares values (also against
+    plain ints).
+    """
+
+    __slots__ = ("words",)
+
+    def __init__(self, words):
+        self.words = list(words)
+
+    @classmethod
+    def from_int(cls, value: int, length: int | None = None, w: int | None = None) -> "Natural":
+        if value < 0:
+            raise ValueError("Natural is nonnegative")
+        w = word_bits() if w is None else w
+        need = _words_needed(value, w)
+        if length is None:
+            length = need
+        elif length < need:
+            raise ValueError(f"value needs {need} words, got length={length}")
+        return cls(int_to_words(value, length, w))
+
+    def to_int(self, w: int | None = None) -> int:
+        return words_to_int(self.words, word_bits() if w is None else w)
+
+    def normalized(self) -> "Natural":
+        n = len(self.words)
+        while n > 1 and self.words[n - 1] == 0:
+            n -= 1
+        return Natural(self.words[:n])
+
+    def bit_length(self, w: int | None = None) -> int:
+        return self.to_int(w).bit_length()
+
+    def __len__(self) -> int:
+        return len(self.words)
+
+    def __eq__(self, other) -> bool:
+        if isinstance(other, Natural):
+            return self.to_int() == other.to_int()
+        if isinstance(other, int):
+            return self.to_int() == other
+        return NotImplemented
+
+    __hash__ = None
+
+    def __repr__(self) -> str:
+        return f"Natural({self.words!r})"
+
+
+def as_natural(x) -> Natural:
+    if isinstance(x, Natural):
+        return x
+    if isinstance(x, int) and not isinstance(x, bool):
+        return Natural.from_int(x)
+    if isinstance(x, bool):
+        return Natural.from_int(int(x))
+    raise TypeError(f"expected int or Natural, got {type(x).__name__}")
+
+
+class ScratchArena:
+    """LIFO scratch accounting in machine words (``bigmul/words.py:234-286``).
+
+    The GPU path allocates its workspace once per plan; it still reports the
+    words it keeps live per multiply through ``alloc_words`` so the arena's
+    ``peak_words`` remains a meaningful memory instrument.
+    """
+
+    __slots__ = ("pos", "peak_words", "reserved_words")
+
+    def __init__(self):
+        self.pos = 0
+        self.peak_words = 0
+        self.reserved_words = 0
+
+    def acquire(self) -> int:
+        return self.pos
+
+    def release(self, mark: int) -> None:
+        if not 0 <= mark <= self.pos:
+            raise ValueError("release does not match an acquire mark")
+        self.pos = mark
+        self.reserved_words = max(self.reserved_words, self.peak_words)
+
+    @contextmanager
+    def frame(self):
+        mark = self.acquire()
+        try:
+            yield self
+        finally:
+            self.release(mark)
+
+    def alloc_words(self, nwords: int) -> None:
+        if nwords < 0:
+            raise ValueError("negative allocation")
+        self.pos += nwords
+        self.peak_words = max(self.peak_words, self.pos)
+
+    def alloc_list(self, count: int, words_per_item: int, fill=0) -> list:
+        self.alloc_words(count * words_per_item)
+        return [fill] * count
+
+    def reset_stats(self) -> None:
+        self.peak_words = 0
+
+    def peak_bytes(self, w: int | None = None) -> int:
+        return self.peak_words * ((word_bits() if w is None else w) // 8)
+
+
+def current_arena() -> ScratchArena:
+    arena = getattr(_tls, "arena", None)
+    if arena is None:
+        arena = _tls.arena = ScratchArena()
+    return arena
+
+
+@contextmanager
+def use_arena(arena: ScratchArena):
+    prev = getattr(_tls, "arena", None)
+    _tls.arena = arena
+    try:
+        yield arena
+    finally:
+        _tls.arena = prev
+
+
+def bit_slices(value: int, width: int, count: int) -> list:
+    """``count`` little-endian fields of ``width`` bits (``bigmul/words.py:307-329``)."""
+    if width <= 0:
+        raise ValueError("field width must be positive")
+    mask = (1 << width) - 1
+    return [(value >> (i * width)) & mask for i in range(count)]
+
+
+def join_bits(parts, width: int) -> int:
+    """sum(parts[i] << width*i); parts may exceed ``width`` (``bigmul/words.py:332-349``)."""
+    # pairwise tree combination keeps this O(n log n) for long part lists
+    vals = [int(p) for p in parts]
+    shift = width
+    while len(vals) > 1:
+        nxt = [vals[i] + (vals[i + 1] << shift) for i in range(0, len(vals) - 1, 2)]
+        if len(vals) & 1:
+            nxt.append(vals[-1])
+        vals = nxt
+        shift *= 2
+    return vals[0] if vals else 0
+
+
+# ---------------------------------------------------------------------------
+# int <-> u32 limb arrays for the C ABI
+
+def int_to_u32(value: int, nlimbs: int) -> np.ndarray:
+    """Little-endian uint32 limbs, zero-padded to ``nlimbs``."""
+    if value < 0:
+        raise ValueError("negative operand")
+    return np.frombuffer(value.to_bytes(4 * nlimbs, "little"), dtype=np.uint32).copy()
+
+
+def u32_to_int(limbs) -> int:
+    return int.from_bytes(np.ascontiguousarray(limbs, dtype=np.uint32).tobytes(), "little")
