@@ -1,0 +1,101 @@
+/*
+ * dkss.h -- C ABI of libdkss (B200 / sm_100a DKSS large-integer multiplication).
+ *
+ * This is the drop-in boundary for the reference's DKSS multiply path.  The reference
+ * (bigmul, pure Python) has no FFI of its own; its plugin surface is the ALGORITHMS
+ * table entry  ALGORITHMS["dmul"] = lambda a, b, table, arena: dmul(a, b, table, arena)
+ * (bigmul/dispatch.py:17) and the stage functions of bigmul/dkss.py.  Each entry point
+ * below names the reference function it replaces; INTEGRATION.md shows the ctypes
+ * binding a bigmul maintainer would add.
+ *
+ * Conventions
+ *  - plain pointers and sizes; integers are little-endian uint32 limb arrays;
+ *    polynomials are uint32[2M][m][L] (L = ceil(d/32) limbs per canonical residue).
+ *  - every call returns 0 on success and a negative DKSS_E* code on failure;
+ *    dkss_last_error() returns a thread-local message for the last failure.
+ *  - the plan is built by the host planner (Python, bigmul/dkss.py:314-361 restated in
+ *    paper_1503_04955_b200/plan.py); the library only uploads it (rho table -> Montgomery
+ *    form) and owns device workspace.
+ *  - a plan handle may be used by one host thread at a time; calls are synchronous for
+ *    host pointers and stream-ordered for the *_device entry points.
+ */
+#ifndef DKSS_H
+#define DKSS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DKSS_OK 0
+#define DKSS_EINVAL (-1)  /* bad argument / plan shape (reference: ValueError) */
+#define DKSS_ECUDA (-2)   /* CUDA runtime failure */
+#define DKSS_ERANGE (-3)  /* operand does not fit the plan (bigmul/dkss.py:389-390) */
+#define DKSS_ENOMEM (-4)
+
+typedef struct dkss_plan dkss_plan;
+
+/* Plan description, field-for-field the reference DkssPlan (bigmul/dkss.py:97-146)
+ * restricted to what the device needs. */
+typedef struct {
+  int64_t N;                   /* inputs < 2^N */
+  int32_t M, m, u;             /* outer length M (transform 2M), inner length m, bits per piece */
+  int32_t L;                   /* u32 limbs per residue, ceil(d/32) */
+  const uint32_t* p;           /* L limbs, the Proth prime p (z = 1) */
+  const uint32_t* rho_powers;  /* (M/m) * m * L limbs: rho^s, s < M/m (DkssPlan.rho_powers) */
+} dkss_plan_desc;
+
+typedef struct {
+  int64_t N;
+  int32_t M, m, u, L;
+  int32_t levels;           /* radix-2m column passes per transform */
+  int32_t base_len;         /* length of the base-case DFT */
+  int64_t poly_bytes;       /* one polynomial, 2M*m*L*4 */
+  int64_t operand_limbs;    /* ceil(N/32) */
+  int64_t product_limbs;    /* ceil(2N/32) */
+  int64_t ring_products;    /* r_mul-equivalents per multiply: 3*twiddles + 2M (== ks_calls) */
+  int64_t twiddles_per_fft; /* (2m-1)(mu-1) summed over levels (bigmul/dkss.py:483-492) */
+  int32_t launches_per_mul; /* kernels launched by one dkss_mul_device call */
+  int64_t workspace_bytes;  /* device workspace currently held */
+} dkss_plan_info;
+
+/* plan lifetime -------------------------------------------------------------------- */
+int dkss_plan_create(const dkss_plan_desc* desc, int device, dkss_plan** out);
+void dkss_plan_destroy(dkss_plan* plan);
+int dkss_plan_get_info(const dkss_plan* plan, dkss_plan_info* out);
+const char* dkss_last_error(void);
+int dkss_version(void);
+
+/* dmul (bigmul/dkss.py:520-548) for operands below 2^N: c = a * b.
+ * Host buffers; na, nb <= operand_limbs; nc limbs are written (zero padded); the call
+ * fails with DKSS_ERANGE if the product does not fit nc limbs. */
+int dkss_mul(dkss_plan* plan, const uint32_t* a, size_t na, const uint32_t* b, size_t nb, uint32_t* c, size_t nc);
+
+/* batched independent products sharing one plan (config 3): a, b are batch x n_limbs,
+ * c is batch x nc.  Host buffers. */
+int dkss_mul_batch(dkss_plan* plan, int batch, const uint32_t* a, const uint32_t* b, size_t n_limbs, uint32_t* c,
+                   size_t nc);
+
+/* device-resident variant: a_dev, b_dev, c_dev are device pointers with the same shapes,
+ * `stream` is a cudaStream_t (NULL = legacy default stream).  Stream-ordered; replays a
+ * cached CUDA graph per (pointers, batch, sizes). */
+int dkss_mul_device(dkss_plan* plan, int batch, const uint32_t* a_dev, const uint32_t* b_dev, size_t n_limbs,
+                    uint32_t* c_dev, size_t nc, void* stream);
+
+/* stage entry points for parity checks (host buffers) ------------------------------ */
+/* dkss_encode, bigmul/dkss.py:381-398: poly = uint32[2M][m][L] */
+int dkss_encode_host(dkss_plan* plan, const uint32_t* a, size_t na, uint32_t* poly);
+/* dkss_fft, bigmul/dkss.py:443-495: count polynomials transformed in place (natural order) */
+int dkss_fft_host(dkss_plan* plan, uint32_t* polys, int count);
+/* r_mul, bigmul/dkss.py:401-420: count ring products out[i] = x[i]*y[i] (count x m x L) */
+int dkss_rmul_host(dkss_plan* plan, const uint32_t* x, const uint32_t* y, uint32_t* out, size_t count);
+/* dkss_decode, bigmul/dkss.py:498-513: v = forward transform of the product polynomial
+ * (natural order, still scaled by 2M); out gets nout limbs of the integer */
+int dkss_decode_host(dkss_plan* plan, const uint32_t* v, uint32_t* out, size_t nout);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DKSS_H */

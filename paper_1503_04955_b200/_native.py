@@ -1,0 +1,186 @@
+"""ctypes binding of libdkss.so (include/dkss.h).
+
+The library is built in-tree (``python -m paper_1503_04955_b200.build``) into
+``paper_1503_04955_b200/_lib/libdkss.so``.  There is no CPU fallback: if the
+library is missing or cannot be loaded, every GPU entry point raises
+``NativeUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libdkss.so")
+
+# every symbol include/dkss.h declares (checked by tests/test_native_abi.py)
+EXPORTS = (
+    "dkss_plan_create", "dkss_plan_destroy", "dkss_plan_get_info", "dkss_last_error", "dkss_version",
+    "dkss_mul", "dkss_mul_batch", "dkss_mul_device",
+    "dkss_encode_host", "dkss_fft_host", "dkss_rmul_host", "dkss_decode_host",
+)
+
+DKSS_OK, DKSS_EINVAL, DKSS_ECUDA, DKSS_ERANGE, DKSS_ENOMEM = 0, -1, -2, -3, -4
+
+
+class NativeUnavailable(RuntimeError):
+    pass
+
+
+class DkssError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"libdkss error {code}: {msg}")
+        self.code = code
+
+
+class PlanDesc(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int64), ("M", ctypes.c_int32), ("m", ctypes.c_int32), ("u", ctypes.c_int32),
+                ("L", ctypes.c_int32), ("p", ctypes.POINTER(ctypes.c_uint32)),
+                ("rho_powers", ctypes.POINTER(ctypes.c_uint32))]
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int64), ("M", ctypes.c_int32), ("m", ctypes.c_int32), ("u", ctypes.c_int32),
+                ("L", ctypes.c_int32), ("levels", ctypes.c_int32), ("base_len", ctypes.c_int32),
+                ("poly_bytes", ctypes.c_int64), ("operand_limbs", ctypes.c_int64),
+                ("product_limbs", ctypes.c_int64), ("ring_products", ctypes.c_int64),
+                ("twiddles_per_fft", ctypes.c_int64), ("launches_per_mul", ctypes.c_int32),
+                ("workspace_bytes", ctypes.c_int64)]
+
+
+_u32p = ctypes.POINTER(ctypes.c_uint32)
+_lock = threading.Lock()
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libdkss.so (raises NativeUnavailable, never falls back)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailable(f"{path} is missing: run `python -m paper_1503_04955_b200.build`")
+        try:
+            L = ctypes.CDLL(path)
+        except OSError as e:
+            raise NativeUnavailable(f"cannot load {path}: {e}") from e
+        vp = ctypes.c_void_p
+        L.dkss_plan_create.argtypes = [ctypes.POINTER(PlanDesc), ctypes.c_int, ctypes.POINTER(vp)]
+        L.dkss_plan_destroy.argtypes = [vp]
+        L.dkss_plan_destroy.restype = None
+        L.dkss_plan_get_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]
+        L.dkss_last_error.restype = ctypes.c_char_p
+        L.dkss_mul.argtypes = [vp, _u32p, ctypes.c_size_t, _u32p, ctypes.c_size_t, _u32p, ctypes.c_size_t]
+        L.dkss_mul_batch.argtypes = [vp, ctypes.c_int, _u32p, _u32p, ctypes.c_size_t, _u32p, ctypes.c_size_t]
+        L.dkss_mul_device.argtypes = [vp, ctypes.c_int, vp, vp, ctypes.c_size_t, vp, ctypes.c_size_t, vp]
+        L.dkss_encode_host.argtypes = [vp, _u32p, ctypes.c_size_t, _u32p]
+        L.dkss_fft_host.argtypes = [vp, _u32p, ctypes.c_int]
+        L.dkss_rmul_host.argtypes = [vp, _u32p, _u32p, _u32p, ctypes.c_size_t]
+        L.dkss_decode_host.argtypes = [vp, _u32p, _u32p, ctypes.c_size_t]
+        for name in EXPORTS:
+            if not hasattr(L, name):
+                raise NativeUnavailable(f"{path} lacks symbol {name}")
+        _lib = L
+        return L
+
+
+def _ptr(a: np.ndarray):
+    if a.dtype != np.uint32 or not a.flags.c_contiguous:
+        raise TypeError("expected a C-contiguous uint32 array")
+    return a.ctypes.data_as(_u32p)
+
+
+def _check(rc: int):
+    if rc != DKSS_OK:
+        msg = load().dkss_last_error().decode(errors="replace")
+        if rc in (DKSS_EINVAL, DKSS_ERANGE):
+            raise ValueError(f"libdkss: {msg}")
+        raise DkssError(rc, msg)
+
+
+class DevicePlan:
+    """A plan uploaded to one GPU (twiddle table in Montgomery form + workspace)."""
+
+    def __init__(self, N: int, M: int, m: int, u: int, p: int, rho_powers, device: int = 0):
+        lib = load()
+        self.N, self.M, self.m, self.u, self.p, self.device = N, M, m, u, p, device
+        self.L = L = -(-p.bit_length() // 32)
+        p_l = np.frombuffer(p.to_bytes(4 * L, "little"), dtype=np.uint32).copy()
+        raw = b"".join(c.to_bytes(4 * L, "little") for row in rho_powers for c in row)
+        rho_l = np.frombuffer(raw, dtype=np.uint32).copy()
+        desc = PlanDesc(N, M, m, u, L, _ptr(p_l), _ptr(rho_l))
+        h = ctypes.c_void_p()
+        _check(lib.dkss_plan_create(ctypes.byref(desc), device, ctypes.byref(h)))
+        self._h = h
+        self._lib = lib
+        self.info = self.get_info()
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.dkss_plan_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    @property
+    def handle(self):
+        return self._h
+
+    def get_info(self) -> dict:
+        info = PlanInfo()
+        _check(self._lib.dkss_plan_get_info(self._h, ctypes.byref(info)))
+        return {k: getattr(info, k) for k, _ in PlanInfo._fields_}
+
+    @property
+    def poly_shape(self):
+        return (2 * self.M, self.m, self.L)
+
+    # -- products --------------------------------------------------------------
+    def mul_limbs(self, a: np.ndarray, b: np.ndarray, nc: int) -> np.ndarray:
+        out = np.zeros(nc, dtype=np.uint32)
+        _check(self._lib.dkss_mul(self._h, _ptr(a), a.size, _ptr(b), b.size, _ptr(out), nc))
+        return out
+
+    def mul_batch(self, a: np.ndarray, b: np.ndarray, nc: int | None = None) -> np.ndarray:
+        a = np.ascontiguousarray(a, dtype=np.uint32)
+        b = np.ascontiguousarray(b, dtype=np.uint32)
+        batch, nl = a.shape
+        nc = nc or self.info["product_limbs"]
+        out = np.zeros((batch, nc), dtype=np.uint32)
+        _check(self._lib.dkss_mul_batch(self._h, batch, _ptr(a), _ptr(b), nl, _ptr(out), nc))
+        return out
+
+    def mul_device(self, batch: int, a_ptr: int, b_ptr: int, n_limbs: int, c_ptr: int, nc: int, stream: int = 0):
+        _check(self._lib.dkss_mul_device(self._h, batch, ctypes.c_void_p(a_ptr), ctypes.c_void_p(b_ptr), n_limbs,
+                                         ctypes.c_void_p(c_ptr), nc, ctypes.c_void_p(stream)))
+
+    # -- stages ----------------------------------------------------------------
+    def encode(self, a_limbs: np.ndarray) -> np.ndarray:
+        out = np.zeros(self.poly_shape, dtype=np.uint32)
+        _check(self._lib.dkss_encode_host(self._h, _ptr(a_limbs), a_limbs.size, _ptr(out)))
+        return out
+
+    def fft(self, polys: np.ndarray) -> np.ndarray:
+        v = np.ascontiguousarray(polys, dtype=np.uint32).copy()
+        count = v.size // (2 * self.M * self.m * self.L)
+        _check(self._lib.dkss_fft_host(self._h, _ptr(v), count))
+        return v
+
+    def rmul(self, x: np.ndarray, y: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.uint32)
+        y = np.ascontiguousarray(y, dtype=np.uint32)
+        out = np.empty_like(x)
+        count = x.size // (self.m * self.L)
+        _check(self._lib.dkss_rmul_host(self._h, _ptr(x), _ptr(y), _ptr(out), count))
+        return out
+
+    def decode(self, v: np.ndarray, nout: int) -> np.ndarray:
+        v = np.ascontiguousarray(v, dtype=np.uint32)
+        out = np.zeros(nout, dtype=np.uint32)
+        _check(self._lib.dkss_decode_host(self._h, _ptr(v), _ptr(out), nout))
+        return out

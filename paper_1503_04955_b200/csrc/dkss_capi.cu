@@ -1,0 +1,605 @@
+// dkss_capi.cu -- libdkss: plan upload, device workspace, launch sequence, C ABI.
+// See include/dkss.h for the contract and DESIGN.md for the kernel/roofline story.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/dkss.h"
+#define DKSS_COMMON_KERNELS
+#include "dkss_table.cuh"
+
+using namespace dkss;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUCHK(expr)                                                                              \
+  do {                                                                                           \
+    cudaError_t _e = (expr);                                                                     \
+    if (_e != cudaSuccess) return fail(DKSS_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
+  } while (0)
+
+int ilog2i(long long v) {
+  int k = 0;
+  while ((1LL << k) < v) ++k;
+  return k;
+}
+
+// ---- host multiprecision for the plan constants ----------------------------------
+using Limbs = std::vector<uint32_t>;
+
+int cmp(const Limbs& a, const Limbs& b) {
+  for (int i = (int)a.size() - 1; i >= 0; --i)
+    if (a[i] != b[i]) return a[i] > b[i] ? 1 : -1;
+  return 0;
+}
+void sub_inplace(Limbs& a, const Limbs& b) {
+  int64_t br = 0;
+  for (size_t i = 0; i < a.size(); ++i) {
+    int64_t x = (int64_t)a[i] - b[i] + br;
+    a[i] = (uint32_t)x;
+    br = x >> 32;
+  }
+}
+// a = 2a mod p  (a < p)
+void dbl_mod(Limbs& a, const Limbs& p) {
+  uint32_t carry = 0;
+  for (size_t i = 0; i < a.size(); ++i) {
+    uint32_t nc = a[i] >> 31;
+    a[i] = (a[i] << 1) | carry;
+    carry = nc;
+  }
+  if (carry || cmp(a, p) >= 0) sub_inplace(a, p);
+}
+// a = a/2 mod p  (p odd)
+void half_mod(Limbs& a, const Limbs& p) {
+  uint32_t top = 0;
+  if (a[0] & 1) {
+    uint64_t c = 0;
+    for (size_t i = 0; i < a.size(); ++i) {
+      c += (uint64_t)a[i] + p[i];
+      a[i] = (uint32_t)c;
+      c >>= 32;
+    }
+    top = (uint32_t)c;
+  }
+  for (size_t i = 0; i < a.size(); ++i) {
+    uint32_t hi = i + 1 < a.size() ? a[i + 1] : top;
+    a[i] = (a[i] >> 1) | (hi << 31);
+  }
+}
+
+// ---- kernel table per (m, L): instantiated in dkss_inst_m{8,16,32}.cu ----------------
+bool lookup(int m, int L, KTable* out) {
+  KTable t{};
+#define DKSS_CASE(MM, L_) \
+  if (m == MM && L == L_) t = dkss_table_m##MM##_L##L_();
+  DKSS_FOR_EACH_INST(DKSS_CASE)
+#undef DKSS_CASE
+  *out = t;
+  return t.fwd != nullptr;
+}
+
+}  // namespace
+
+struct GraphKey {
+  int batch;
+  const void* a;
+  const void* b;
+  void* c;
+  size_t nl, nc;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(batch, a, b, c, nl, nc) < std::tie(o.batch, o.a, o.b, o.c, o.nl, o.nc);
+  }
+};
+
+struct dkss_plan {
+  int device = 0;
+  long long N = 0;
+  int M = 0, m = 0, u = 0, L = 0;
+  int levels = 0, base_len = 0, logE = 0, logb = 0, log_top_mu = 0;
+  long long poly_words = 0, op_limbs = 0, prod_limbs = 0;
+  long long twiddles = 0;
+  ModCtx mc{};
+  KTable kt{};
+  uint32_t* d_tw = nullptr;  // Montgomery-form rho table
+  // workspace
+  int cap_batch = 0;
+  uint32_t* d_poly = nullptr;  // 2 * cap_batch polynomials
+  uint32_t* d_ops = nullptr;   // 2 * cap_batch operands (host API staging)
+  uint32_t* d_prod = nullptr;  // cap_batch products
+  uint32_t* d_gmask = nullptr;
+  uint32_t* d_pmask = nullptr;
+  uint32_t* d_bstat = nullptr;
+  uint32_t* h_pin = nullptr;   // pinned staging
+  size_t h_pin_words = 0;
+  size_t ws_bytes = 0;
+  cudaStream_t stream = nullptr;
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  std::mutex mu;
+};
+
+namespace {
+
+int dec_blocks(const dkss_plan* P) { return (int)((P->prod_limbs + kDecThreads - 1) / kDecThreads); }
+
+void free_ws(dkss_plan* P) {
+  cudaFree(P->d_poly);
+  cudaFree(P->d_ops);
+  cudaFree(P->d_prod);
+  cudaFree(P->d_gmask);
+  cudaFree(P->d_pmask);
+  cudaFree(P->d_bstat);
+  P->d_poly = P->d_ops = P->d_prod = P->d_gmask = P->d_pmask = P->d_bstat = nullptr;
+  for (auto& kv : P->graphs) cudaGraphExecDestroy(kv.second);
+  P->graphs.clear();
+  P->cap_batch = 0;
+  P->ws_bytes = 0;
+}
+
+int ensure_ws(dkss_plan* P, int batch) {
+  if (batch <= P->cap_batch) return 0;
+  free_ws(P);
+  const size_t poly_b = (size_t)P->poly_words * 4;
+  const size_t nwarps = (size_t)dec_blocks(P) * 32;
+  CUCHK(cudaMalloc(&P->d_poly, 2 * (size_t)batch * poly_b));
+  CUCHK(cudaMalloc(&P->d_ops, 2 * (size_t)batch * P->op_limbs * 4));
+  CUCHK(cudaMalloc(&P->d_prod, (size_t)batch * P->prod_limbs * 4));
+  CUCHK(cudaMalloc(&P->d_gmask, (size_t)batch * nwarps * 4));
+  CUCHK(cudaMalloc(&P->d_pmask, (size_t)batch * nwarps * 4));
+  CUCHK(cudaMalloc(&P->d_bstat, (size_t)batch * dec_blocks(P) * 4));
+  P->cap_batch = batch;
+  P->ws_bytes = 2 * (size_t)batch * poly_b + 2 * (size_t)batch * P->op_limbs * 4 + (size_t)batch * P->prod_limbs * 4 +
+                (size_t)batch * nwarps * 8 + (size_t)batch * dec_blocks(P) * 4;
+  return 0;
+}
+
+int ensure_pin(dkss_plan* P, size_t words) {
+  if (words <= P->h_pin_words) return 0;
+  if (P->h_pin) cudaFreeHost(P->h_pin);
+  P->h_pin = nullptr;
+  CUCHK(cudaMallocHost(&P->h_pin, words * 4));
+  P->h_pin_words = words;
+  return 0;
+}
+
+size_t smem_bytes(const dkss_plan* P, int nbuf) { return (size_t)nbuf * P->kt.ne * P->kt.es * 4; }
+
+// --- launch helpers (all stream-ordered) ---------------------------------------------
+int launch_encode(dkss_plan* P, const uint32_t* ops, long long na, uint32_t* poly, int npoly, cudaStream_t s) {
+  EncodeArgs A{ops, na, poly, P->poly_words, npoly, P->M, P->m, P->L, P->u};
+  const long long total = 2LL * P->M * P->m * npoly;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  k_encode<<<blocks, 256, 0, s>>>(A);
+  CUCHK(cudaGetLastError());
+  return 0;
+}
+
+int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s) {
+  const long long cols = (long long)npoly << P->log_top_mu;
+  const int grid = (int)((cols + P->kt.cols - 1) / P->kt.cols);
+  for (int lv = 0; lv < P->levels; ++lv) {
+    PassArgs A{};
+    A.poly = poly;
+    A.poly_words = P->poly_words;
+    // column stride at level lv: mu_lv = 2M / (2m)^(lv+1)
+    A.log_mu = ilog2i(2LL * P->M) - P->logE * (lv + 1);
+    A.log_top_mu = P->log_top_mu;
+    A.base_pow = 1LL << (P->logE * lv);
+    A.tw = P->d_tw;
+    A.scale = 0;
+    A.total_cols = cols;
+    P->kt.fwd<<<grid, kThreads, smem_bytes(P, 1), s>>>(A, P->mc);
+    CUCHK(cudaGetLastError());
+  }
+  return 0;
+}
+
+int launch_inv_levels(dkss_plan* P, uint32_t* poly, int npoly, bool scale_last, cudaStream_t s) {
+  const long long cols = (long long)npoly << P->log_top_mu;
+  const int grid = (int)((cols + P->kt.cols - 1) / P->kt.cols);
+  for (int lv = P->levels - 1; lv >= 0; --lv) {
+    PassArgs A{};
+    A.poly = poly;
+    A.poly_words = P->poly_words;
+    A.log_mu = ilog2i(2LL * P->M) - P->logE * (lv + 1);
+    A.log_top_mu = P->log_top_mu;
+    A.base_pow = 1LL << (P->logE * lv);
+    A.tw = P->d_tw;
+    A.scale = (lv == 0 && scale_last) ? 1 : 0;
+    A.total_cols = cols;
+    P->kt.inv<<<grid, kThreads, smem_bytes(P, 2), s>>>(A, P->mc);
+    CUCHK(cudaGetLastError());
+  }
+  return 0;
+}
+
+int launch_bottom(dkss_plan* P, uint32_t* a, const uint32_t* b, int npoly, int mode, bool scale, cudaStream_t s) {
+  BottomArgs A{};
+  A.a = a;
+  A.b = b;
+  A.poly_words = P->poly_words;
+  A.elems_per_poly = 2LL * P->M;
+  A.logb = P->logb;
+  A.mode = mode;
+  A.scale = scale ? 1 : 0;
+  const long long elems = 2LL * P->M * npoly;
+  const int grid = (int)((elems + P->kt.ne - 1) / P->kt.ne);
+  A.total_elems = elems;
+  P->kt.bottom<<<grid, kThreads, smem_bytes(P, 2), s>>>(A, P->mc);
+  CUCHK(cudaGetLastError());
+  return 0;
+}
+
+int launch_decode(dkss_plan* P, const uint32_t* v, uint32_t* out, int npoly, cudaStream_t s) {
+  DecodeArgs A{};
+  A.v = v;
+  A.poly_words = P->poly_words;
+  A.out = out;
+  A.nout = P->prod_limbs;
+  A.gmask = P->d_gmask;
+  A.pmask = P->d_pmask;
+  A.bstat = P->d_bstat;
+  A.blocks_per_poly = dec_blocks(P);
+  A.M = P->M;
+  A.MM = P->m;
+  A.L = P->L;
+  A.u = P->u;
+  const int grid = A.blocks_per_poly * npoly;
+  k_decode1<<<grid, kDecThreads, 0, s>>>(A);
+  CUCHK(cudaGetLastError());
+  k_decode2<<<grid, kDecThreads, 0, s>>>(A);
+  CUCHK(cudaGetLastError());
+  return 0;
+}
+
+// whole multiply: operands already encoded-able in device memory
+int run_mul(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, long long nl, uint32_t* prod,
+            cudaStream_t s) {
+  uint32_t* pa = P->d_poly;
+  uint32_t* pb = P->d_poly + (size_t)batch * P->poly_words;
+  int rc;
+  if ((rc = launch_encode(P, a, nl, pa, batch, s))) return rc;
+  if ((rc = launch_encode(P, b, nl, pb, batch, s))) return rc;
+  if ((rc = launch_fwd_levels(P, P->d_poly, 2 * batch, s))) return rc;
+  if ((rc = launch_bottom(P, pa, pb, batch, 1, P->levels == 0, s))) return rc;
+  if ((rc = launch_inv_levels(P, pa, batch, true, s))) return rc;
+  if ((rc = launch_decode(P, pa, prod, batch, s))) return rc;
+  return 0;
+}
+
+int check_operand(const dkss_plan* P, const uint32_t* a, size_t na) {
+  // value must be < 2^N (bigmul/dkss.py:389-390)
+  for (size_t i = na; i-- > 0;) {
+    if (!a[i]) continue;
+    const long long top = 32LL * (long long)i + (31 - __builtin_clz(a[i]));
+    if (top >= P->N) return fail(DKSS_ERANGE, "operand does not fit the plan (bit %lld >= N=%lld)", top, P->N);
+    break;
+  }
+  return 0;
+}
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+int dkss_version(void) { return 1; }
+
+const char* dkss_last_error(void) { return g_err.c_str(); }
+
+int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
+  if (!d || !out || !d->p || !d->rho_powers) return fail(DKSS_EINVAL, "null argument");
+  *out = nullptr;
+  const int M = d->M, m = d->m, L = d->L;
+  if (M < m || m < 2 || (M & (M - 1)) || (m & (m - 1))) return fail(DKSS_EINVAL, "M and m must be powers of 2, M >= m");
+  if (L < 2 || L > DKSS_MAXL) return fail(DKSS_EINVAL, "L=%d unsupported (2..%d)", L, DKSS_MAXL);
+  if (d->p[L - 1] == 0 || !(d->p[0] & 1)) return fail(DKSS_EINVAL, "p must be odd with exactly L=%d limbs", L);
+  KTable kt;
+  if (!lookup(m, L, &kt)) return fail(DKSS_EINVAL, "no kernels for m=%d, L=%d (m in {8,16,32})", m, L);
+  CUCHK(cudaSetDevice(device));
+  dkss_plan* P = new dkss_plan();
+  P->device = device;
+  P->N = d->N;
+  P->M = M;
+  P->m = m;
+  P->u = d->u;
+  P->L = L;
+  P->kt = kt;
+  P->logE = ilog2i(2 * m);
+  const int logn = ilog2i(2LL * M);
+  P->levels = 0;
+  long long n = 2LL * M;
+  while (n > 2 * m) {
+    n /= 2 * m;
+    P->levels++;
+  }
+  P->base_len = (int)n;
+  P->logb = ilog2i(n);
+  P->log_top_mu = ilog2i((long long)M / m);
+  (void)logn;
+  P->poly_words = 2LL * M * m * L;
+  P->op_limbs = (d->N + 31) / 32;
+  P->prod_limbs = (2 * d->N + 31) / 32;
+  {
+    long long tw = 0, len = 2LL * M, inst = 1;
+    while (len > 2 * m) {
+      const long long mu = len / (2 * m);
+      tw += inst * (2 * m - 1) * (mu - 1);
+      inst *= 2 * m;
+      len = mu;
+    }
+    P->twiddles = tw;
+  }
+  // modulus constants
+  Limbs p(d->p, d->p + L);
+  memcpy(P->mc.p, d->p, 4 * L);
+  uint32_t inv = 1;
+  for (int i = 0; i < 5; ++i) inv *= 2u - p[0] * inv;
+  P->mc.pinv = 0u - inv;
+  Limbs x(L, 0);
+  x[0] = 1;
+  for (int i = 0; i < 32 * L; ++i) dbl_mod(x, p);
+  Limbs rmod = x;  // R mod p
+  for (int i = 0; i < 32 * L; ++i) dbl_mod(x, p);
+  memcpy(P->mc.r2, x.data(), 4 * L);  // R^2 mod p
+  Limbs ks = x;
+  for (int i = 0; i < logn; ++i) half_mod(ks, p);
+  memcpy(P->mc.kscale, ks.data(), 4 * L);
+  Limbs ki = rmod;
+  for (int i = 0; i < logn; ++i) half_mod(ki, p);
+  memcpy(P->mc.kinv, ki.data(), 4 * L);
+  double pd = 0;
+  for (int i = L - 1; i >= 0; --i) pd = pd * 4294967296.0 + p[i];
+  P->mc.pf_inv = (float)(ldexp(1.0, 32 * (L - 2)) / pd);
+  // kernels: opt into >48 KB dynamic smem
+  const size_t sm2 = smem_bytes(P, 2);
+  CUCHK(cudaFuncSetAttribute(kt.fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(P, 1)));
+  CUCHK(cudaFuncSetAttribute(kt.inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+  CUCHK(cudaFuncSetAttribute(kt.bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+  CUCHK(cudaFuncSetAttribute(kt.rmul, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+  CUCHK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+  // twiddle table -> Montgomery form
+  const size_t tw_words = (size_t)(M / m) * m * L;
+  cudaError_t e = cudaMalloc(&P->d_tw, tw_words * 4);
+  if (e == cudaSuccess) e = cudaMemcpy(P->d_tw, d->rho_powers, tw_words * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    kt.mscale<<<(int)std::min<size_t>((tw_words / L + 255) / 256, 4096), 256, 0, P->stream>>>(P->d_tw, tw_words / L, 0,
+                                                                                               P->mc);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(P->stream);
+  if (e != cudaSuccess) {
+    dkss_plan_destroy(P);
+    return fail(DKSS_ECUDA, "plan upload failed: %s", cudaGetErrorString(e));
+  }
+  *out = P;
+  return DKSS_OK;
+}
+
+void dkss_plan_destroy(dkss_plan* P) {
+  if (!P) return;
+  cudaSetDevice(P->device);
+  free_ws(P);
+  cudaFree(P->d_tw);
+  if (P->h_pin) cudaFreeHost(P->h_pin);
+  if (P->stream) cudaStreamDestroy(P->stream);
+  delete P;
+}
+
+int dkss_plan_get_info(const dkss_plan* P, dkss_plan_info* o) {
+  if (!P || !o) return fail(DKSS_EINVAL, "null argument");
+  o->N = P->N;
+  o->M = P->M;
+  o->m = P->m;
+  o->u = P->u;
+  o->L = P->L;
+  o->levels = P->levels;
+  o->base_len = P->base_len;
+  o->poly_bytes = P->poly_words * 4;
+  o->operand_limbs = P->op_limbs;
+  o->product_limbs = P->prod_limbs;
+  o->twiddles_per_fft = P->twiddles;
+  o->ring_products = 3 * P->twiddles + 2LL * P->M;
+  o->launches_per_mul = 2 + P->levels + 1 + P->levels + 2;
+  o->workspace_bytes = (int64_t)P->ws_bytes;
+  return DKSS_OK;
+}
+
+int dkss_mul_device(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, size_t nl, uint32_t* c, size_t nc,
+                    void* stream) {
+  if (!P || batch < 1 || !a || !b || !c) return fail(DKSS_EINVAL, "bad argument");
+  if ((long long)nl > P->op_limbs) return fail(DKSS_ERANGE, "operand limbs %zu exceed plan (%lld)", nl, P->op_limbs);
+  if ((long long)nc < P->prod_limbs) return fail(DKSS_EINVAL, "nc=%zu below product limbs %lld", nc, P->prod_limbs);
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  int rc;
+  if ((rc = ensure_ws(P, batch))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  GraphKey key{batch, a, b, c, nl, nc};
+  auto it = P->graphs.find(key);
+  if (it == P->graphs.end()) {
+    cudaStream_t cap;
+    CUCHK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    CUCHK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    rc = run_mul(P, batch, a, b, (long long)nl, P->d_prod, cap);
+    if (!rc && (long long)nc == P->prod_limbs) {
+      // decode wrote into d_prod; copy into the caller's buffer
+      cudaMemcpyAsync(c, P->d_prod, (size_t)batch * P->prod_limbs * 4, cudaMemcpyDeviceToDevice, cap);
+    } else if (!rc) {
+      cudaMemsetAsync(c, 0, (size_t)batch * nc * 4, cap);
+      cudaMemcpy2DAsync(c, nc * 4, P->d_prod, P->prod_limbs * 4, P->prod_limbs * 4, batch, cudaMemcpyDeviceToDevice,
+                        cap);
+    }
+    cudaGraph_t g;
+    cudaError_t e = cudaStreamEndCapture(cap, &g);
+    cudaStreamDestroy(cap);
+    if (rc) return rc;
+    if (e != cudaSuccess) return fail(DKSS_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
+    cudaGraphExec_t ge;
+    e = cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(DKSS_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+    it = P->graphs.emplace(key, ge).first;
+  }
+  CUCHK(cudaGraphLaunch(it->second, s));
+  return DKSS_OK;
+}
+
+int dkss_mul_batch(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, size_t nl, uint32_t* c, size_t nc) {
+  if (!P || batch < 1 || !a || !b || !c) return fail(DKSS_EINVAL, "bad argument");
+  if ((long long)nl > P->op_limbs) return fail(DKSS_ERANGE, "operand limbs %zu exceed plan (%lld)", nl, P->op_limbs);
+  int rc;
+  for (int i = 0; i < batch; ++i) {
+    if ((rc = check_operand(P, a + (size_t)i * nl, nl))) return rc;
+    if ((rc = check_operand(P, b + (size_t)i * nl, nl))) return rc;
+  }
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  if ((rc = ensure_ws(P, batch))) return rc;
+  const size_t opw = (size_t)batch * nl;
+  const size_t prw = (size_t)batch * P->prod_limbs;
+  if ((rc = ensure_pin(P, std::max(2 * opw, prw)))) return rc;
+  cudaStream_t s = P->stream;
+  memcpy(P->h_pin, a, opw * 4);
+  memcpy(P->h_pin + opw, b, opw * 4);
+  CUCHK(cudaMemcpyAsync(P->d_ops, P->h_pin, 2 * opw * 4, cudaMemcpyHostToDevice, s));
+  if ((rc = run_mul(P, batch, P->d_ops, P->d_ops + opw, (long long)nl, P->d_prod, s))) return rc;
+  CUCHK(cudaMemcpyAsync(P->h_pin, P->d_prod, prw * 4, cudaMemcpyDeviceToHost, s));
+  CUCHK(cudaStreamSynchronize(s));
+  for (int i = 0; i < batch; ++i) {
+    const uint32_t* src = P->h_pin + (size_t)i * P->prod_limbs;
+    uint32_t* dst = c + (size_t)i * nc;
+    const size_t ncopy = std::min<size_t>(nc, P->prod_limbs);
+    memcpy(dst, src, ncopy * 4);
+    for (size_t k = ncopy; k < (size_t)P->prod_limbs; ++k)
+      if (src[k]) return fail(DKSS_ERANGE, "product does not fit nc=%zu limbs", nc);
+    if (nc > ncopy) memset(dst + ncopy, 0, (nc - ncopy) * 4);
+  }
+  return DKSS_OK;
+}
+
+int dkss_mul(dkss_plan* P, const uint32_t* a, size_t na, const uint32_t* b, size_t nb, uint32_t* c, size_t nc) {
+  if (!P || !a || !b || !c) return fail(DKSS_EINVAL, "bad argument");
+  if ((long long)na > P->op_limbs || (long long)nb > P->op_limbs) {
+    // allow zero high limbs beyond the plan
+    size_t na2 = na, nb2 = nb;
+    while (na2 > 0 && (long long)na2 > P->op_limbs && a[na2 - 1] == 0) --na2;
+    while (nb2 > 0 && (long long)nb2 > P->op_limbs && b[nb2 - 1] == 0) --nb2;
+    if ((long long)na2 > P->op_limbs || (long long)nb2 > P->op_limbs)
+      return fail(DKSS_ERANGE, "operand does not fit the plan");
+    na = na2;
+    nb = nb2;
+  }
+  std::vector<uint32_t> A((size_t)P->op_limbs, 0), B((size_t)P->op_limbs, 0);
+  memcpy(A.data(), a, na * 4);
+  memcpy(B.data(), b, nb * 4);
+  return dkss_mul_batch(P, 1, A.data(), B.data(), (size_t)P->op_limbs, c, nc);
+}
+
+int dkss_encode_host(dkss_plan* P, const uint32_t* a, size_t na, uint32_t* poly) {
+  if (!P || !a || !poly) return fail(DKSS_EINVAL, "bad argument");
+  int rc;
+  if ((rc = check_operand(P, a, na))) return rc;
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  if ((rc = ensure_ws(P, 1))) return rc;
+  size_t nl = std::min<size_t>(na, (size_t)P->op_limbs);
+  std::vector<uint32_t> A((size_t)P->op_limbs, 0);
+  memcpy(A.data(), a, nl * 4);
+  CUCHK(cudaMemcpyAsync(P->d_ops, A.data(), A.size() * 4, cudaMemcpyHostToDevice, P->stream));
+  if ((rc = launch_encode(P, P->d_ops, P->op_limbs, P->d_poly, 1, P->stream))) return rc;
+  CUCHK(cudaMemcpyAsync(poly, P->d_poly, P->poly_words * 4, cudaMemcpyDeviceToHost, P->stream));
+  CUCHK(cudaStreamSynchronize(P->stream));
+  return DKSS_OK;
+}
+
+int dkss_fft_host(dkss_plan* P, uint32_t* polys, int count) {
+  if (!P || !polys || count < 1) return fail(DKSS_EINVAL, "bad argument");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  int rc;
+  if ((rc = ensure_ws(P, count))) return rc;  // 2*count polys available
+  uint32_t* work = P->d_poly;
+  uint32_t* scratch = P->d_poly + (size_t)count * P->poly_words;
+  const size_t bytes = (size_t)count * P->poly_words * 4;
+  cudaStream_t s = P->stream;
+  CUCHK(cudaMemcpyAsync(work, polys, bytes, cudaMemcpyHostToDevice, s));
+  if ((rc = launch_fwd_levels(P, work, count, s))) return rc;
+  if ((rc = launch_bottom(P, work, nullptr, count, 0, false, s))) return rc;
+  const long long elems = 2LL * P->M;
+  k_permute<<<(int)std::min<long long>((elems * count * P->m * P->L + 255) / 256, 148LL * 32), 256, 0, s>>>(
+      work, scratch, elems, P->m * P->L, P->logE, P->levels, P->logb, 1, P->poly_words, count);
+  CUCHK(cudaGetLastError());
+  CUCHK(cudaMemcpyAsync(polys, scratch, bytes, cudaMemcpyDeviceToHost, s));
+  CUCHK(cudaStreamSynchronize(s));
+  return DKSS_OK;
+}
+
+int dkss_rmul_host(dkss_plan* P, const uint32_t* x, const uint32_t* y, uint32_t* out, size_t count) {
+  if (!P || !x || !y || !out) return fail(DKSS_EINVAL, "bad argument");
+  if (count == 0) return DKSS_OK;
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  const size_t ew = (size_t)P->m * P->L;
+  uint32_t *dx, *dy, *dout;
+  CUCHK(cudaMalloc(&dx, count * ew * 4));
+  CUCHK(cudaMalloc(&dy, count * ew * 4));
+  CUCHK(cudaMalloc(&dout, count * ew * 4));
+  cudaStream_t s = P->stream;
+  cudaMemcpyAsync(dx, x, count * ew * 4, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(dy, y, count * ew * 4, cudaMemcpyHostToDevice, s);
+  const int grid = (int)((count + P->kt.ne - 1) / P->kt.ne);
+  P->kt.rmul<<<grid, kThreads, smem_bytes(P, 2), s>>>(dx, dy, dout, (long long)count, P->mc);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, count * ew * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(dx);
+  cudaFree(dy);
+  cudaFree(dout);
+  if (e != cudaSuccess) return fail(DKSS_ECUDA, "rmul failed: %s", cudaGetErrorString(e));
+  return DKSS_OK;
+}
+
+int dkss_decode_host(dkss_plan* P, const uint32_t* v, uint32_t* out, size_t nout) {
+  if (!P || !v || !out) return fail(DKSS_EINVAL, "bad argument");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  int rc;
+  if ((rc = ensure_ws(P, 1))) return rc;
+  cudaStream_t s = P->stream;
+  CUCHK(cudaMemcpyAsync(P->d_poly, v, P->poly_words * 4, cudaMemcpyHostToDevice, s));
+  const long long nres = 2LL * P->M * P->m;
+  P->kt.mscale<<<(int)std::min<long long>((nres + 255) / 256, 4096), 256, 0, s>>>(P->d_poly, nres, 1, P->mc);
+  CUCHK(cudaGetLastError());
+  if ((rc = launch_decode(P, P->d_poly, P->d_prod, 1, s))) return rc;
+  std::vector<uint32_t> full((size_t)P->prod_limbs);
+  CUCHK(cudaMemcpyAsync(full.data(), P->d_prod, full.size() * 4, cudaMemcpyDeviceToHost, s));
+  CUCHK(cudaStreamSynchronize(s));
+  const size_t ncopy = std::min<size_t>(nout, full.size());
+  memcpy(out, full.data(), ncopy * 4);
+  for (size_t k = ncopy; k < full.size(); ++k)
+    if (full[k]) return fail(DKSS_ERANGE, "decoded value does not fit nout=%zu limbs", nout);
+  if (nout > ncopy) memset(out + ncopy, 0, (nout - ncopy) * 4);
+  return DKSS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,41 @@
+// dkss_table.cuh -- per-(m, L) kernel table; each m is instantiated in its own
+// translation unit (dkss_inst_m*.cu) so the build parallelises.
+#pragma once
+#include "dkss_kernels.cuh"
+
+namespace dkss {
+
+struct KTable {
+  void (*fwd)(PassArgs, ModCtx);
+  void (*inv)(PassArgs, ModCtx);
+  void (*bottom)(BottomArgs, ModCtx);
+  void (*rmul)(const uint32_t*, const uint32_t*, uint32_t*, long long, ModCtx);
+  void (*mscale)(uint32_t*, long long, int, ModCtx);
+  int ne;     // elements per CTA
+  int cols;   // columns per CTA
+  size_t es;  // smem words per element
+};
+
+template <int MM, int L>
+KTable make_table() {
+  KTable t;
+  t.fwd = k_fwd_pass<MM, L>;
+  t.inv = k_inv_pass<MM, L>;
+  t.bottom = k_bottom<MM, L>;
+  t.rmul = k_rmul<MM, L>;
+  t.mscale = k_mont_scale<L>;
+  t.ne = Cfg<MM>::NE;
+  t.cols = Cfg<MM>::COLS;
+  t.es = Smem<MM, L>::ES;
+  return t;
+}
+
+#define DKSS_FOR_EACH_INST(X) \
+  X(8, 2) X(8, 3) X(8, 4) X(8, 5) X(8, 6) X(16, 2) X(16, 3) X(16, 4) X(16, 5) X(16, 6) \
+  X(32, 2) X(32, 3) X(32, 4) X(32, 5) X(32, 6)
+
+#define DKSS_DECLARE(MM, L) KTable dkss_table_m##MM##_L##L();
+DKSS_FOR_EACH_INST(DKSS_DECLARE)
+#undef DKSS_DECLARE
+
+}  // namespace dkss

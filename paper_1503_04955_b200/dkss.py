@@ -1,0 +1,179 @@
+"""DKSS multiplication on B200 behind the reference's Python API.
+
+Public entry points keep the reference signatures (BASELINE.json north_star:
+"The Python package's public multiply entry points keep their signatures, so
+the build is a drop-in"):
+
+* ``dmul(a, b, thresholds=None, arena=None) -> Natural``   -- bigmul/dkss.py:520-548
+* ``dkss_encode(a, plan, arena=None)``                      -- bigmul/dkss.py:381-398
+* ``dkss_fft(v, plan, table=None, arena=None, base_pow=1)`` -- bigmul/dkss.py:443-495
+* ``r_mul(x, y, plan, table=None, arena=None)``             -- bigmul/dkss.py:401-420
+* ``dkss_decode(v, plan, arena=None) -> Natural``           -- bigmul/dkss.py:498-513
+
+Host work is parameter selection (plan.py, identical to the reference) and
+int <-> u32-limb conversion; every arithmetic step runs in libdkss.so on the
+GPU (no CPU fallback -- a missing library raises).  The stage functions accept
+and return the reference's list-of-lists representation; the ``*_limbs``
+variants take numpy uint32[2M][m][L] arrays and skip the Python int boxing.
+"""
+
+from __future__ import annotations
+
+import os
+import threading
+
+import numpy as np
+
+from ._native import DevicePlan
+from .plan import DkssPlan, dkss_select_params, ring_products_per_multiply, twiddle_count
+from .words import (Natural, ScratchArena, as_natural, current_arena, int_to_u32, u32_to_int, word_bits)
+
+# The reference hands products below 2048 result bits to smul (bigmul/dkss.py:517,
+# 533-535); that rung is out of scope here, so such inputs run through DKSS on the GPU
+# with the plan for N = _MIN_PLAN_BITS (any input below 2^N fits a plan for N).
+_MIN_DKSS_BITS = 2048
+_MIN_PLAN_BITS = 1024
+
+_dev_lock = threading.Lock()
+_dev_plans: dict = {}
+
+
+def _device() -> int:
+    return int(os.environ.get("DKSS_DEVICE", "0"))
+
+
+def device_plan(plan: DkssPlan, device: int | None = None) -> DevicePlan:
+    """Upload (once) and return the device plan for a host plan."""
+    device = _device() if device is None else device
+    key = (plan.N, plan.M, plan.m, plan.u, plan.p, device)
+    with _dev_lock:
+        dp = _dev_plans.get(key)
+        if dp is None:
+            dp = DevicePlan(plan.N, plan.M, plan.m, plan.u, plan.p, plan.rho_powers, device)
+            _dev_plans[key] = dp
+        return dp
+
+
+def clear_device_plans() -> None:
+    with _dev_lock:
+        for dp in _dev_plans.values():
+            dp.close()
+        _dev_plans.clear()
+
+
+def _L(plan: DkssPlan) -> int:
+    return -(-plan.pz.bit_length() // 32)
+
+
+def poly_to_limbs(poly, plan: DkssPlan) -> np.ndarray:
+    """list[2M][m] of ints -> uint32[2M, m, L]"""
+    L = _L(plan)
+    raw = b"".join(int(c).to_bytes(4 * L, "little") for row in poly for c in row)
+    return np.frombuffer(raw, dtype=np.uint32).reshape(len(poly), plan.m, L).copy()
+
+
+def limbs_to_poly(arr: np.ndarray) -> list:
+    n, m, L = arr.shape
+    flat = arr.reshape(-1, L)
+    vals = [int.from_bytes(row.tobytes(), "little") for row in flat]
+    return [vals[i * m:(i + 1) * m] for i in range(n)]
+
+
+# ---------------------------------------------------------------------------
+# stages
+
+def dkss_encode_limbs(a, plan: DkssPlan) -> np.ndarray:
+    ai = as_natural(a).to_int()
+    if plan.N and ai >= 1 << plan.N:
+        raise ValueError("operand does not fit the plan")
+    dp = device_plan(plan)
+    return dp.encode(int_to_u32(ai, max(1, dp.info["operand_limbs"])))
+
+
+def dkss_encode(a, plan: DkssPlan, arena: ScratchArena | None = None):
+    arena = arena or current_arena()
+    arena.alloc_words(2 * plan.M * plan.oclen)
+    return limbs_to_poly(dkss_encode_limbs(a, plan))
+
+
+def dkss_fft_limbs(polys: np.ndarray, plan: DkssPlan) -> np.ndarray:
+    return device_plan(plan).fft(polys)
+
+
+def dkss_fft(v, plan: DkssPlan, table=None, arena: ScratchArena | None = None, base_pow: int = 1) -> None:
+    """In place: v[i] <- a(rho^i) (natural order), like the reference."""
+    length = len(v)
+    if length & (length - 1):
+        raise ValueError("transform length must be a power of 2")
+    if base_pow != 1 or length != 2 * plan.M:
+        raise ValueError("the device transform evaluates the full length-2M transform (base_pow=1)")
+    out = dkss_fft_limbs(poly_to_limbs(v, plan), plan)
+    plan.ks_calls += twiddle_count(plan)
+    v[:] = limbs_to_poly(out)
+
+
+def r_mul_limbs(x: np.ndarray, y: np.ndarray, plan: DkssPlan) -> np.ndarray:
+    return device_plan(plan).rmul(x, y)
+
+
+def r_mul(x, y, plan: DkssPlan, table=None, arena: ScratchArena | None = None):
+    plan.ks_calls += 1
+    L = _L(plan)
+    xa = poly_to_limbs([x], plan)
+    ya = poly_to_limbs([y], plan)
+    del L
+    return limbs_to_poly(r_mul_limbs(xa, ya, plan))[0]
+
+
+def dkss_decode_limbs(v: np.ndarray, plan: DkssPlan, nout: int) -> np.ndarray:
+    return device_plan(plan).decode(v, nout)
+
+
+def dkss_decode(v, plan: DkssPlan, arena: ScratchArena | None = None) -> Natural:
+    dp = device_plan(plan)
+    limbs = dkss_decode_limbs(poly_to_limbs(v, plan), plan, dp.info["product_limbs"])
+    value = u32_to_int(limbs)
+    return Natural.from_int(value) if value else Natural([0])
+
+
+# ---------------------------------------------------------------------------
+# the multiply
+
+def dmul(a, b, thresholds=None, arena: ScratchArena | None = None) -> Natural:
+    """Full product via DKSS on the GPU (bigmul/dkss.py:520-548)."""
+    a, b = as_natural(a), as_natural(b)
+    arena = arena or current_arena()
+    ai, bi = a.to_int(), b.to_int()
+    outlen = max(1, len(a) + len(b))
+    if ai == 0 or bi == 0:
+        return Natural([0] * outlen)
+    n_bits = max(ai.bit_length(), bi.bit_length())
+    N = max(n_bits, _MIN_PLAN_BITS)
+    plan = dkss_select_params(N, word_bits(), thresholds)
+    dp = device_plan(plan)
+    info = dp.info
+    nl = info["operand_limbs"]
+    w = word_bits()
+    nc = max(info["product_limbs"], -(-outlen * w // 32))
+    with arena.frame():
+        # device workspace per multiply: 2 polynomials + operands + product, in words
+        arena.alloc_words((2 * info["poly_bytes"] + 4 * (2 * nl + nc)) * 8 // w)
+        c = dp.mul_limbs(int_to_u32(ai, nl), int_to_u32(bi, nl), nc)
+    plan.ks_calls += ring_products_per_multiply(plan)
+    return Natural.from_int(u32_to_int(c), length=outlen)
+
+
+def dmul_many(pairs, thresholds=None) -> list:
+    """Independent products sharing one plan, batched in one device call (config 3)."""
+    pairs = list(pairs)
+    if not pairs:
+        return []
+    n_bits = max(max(int(a).bit_length(), int(b).bit_length()) for a, b in pairs)
+    N = max(n_bits, _MIN_PLAN_BITS)
+    plan = dkss_select_params(N, word_bits(), thresholds)
+    dp = device_plan(plan)
+    nl = dp.info["operand_limbs"]
+    A = np.stack([int_to_u32(int(a), nl) for a, _ in pairs])
+    B = np.stack([int_to_u32(int(b), nl) for _, b in pairs])
+    C = dp.mul_batch(A, B)
+    return [u32_to_int(row) for row in C]
