@@ -84,6 +84,21 @@ int dkss_mul_batch(dkss_plan* plan, int batch, const uint32_t* a, const uint32_t
 int dkss_mul_device(dkss_plan* plan, int batch, const uint32_t* a_dev, const uint32_t* b_dev, size_t n_limbs,
                     uint32_t* c_dev, size_t nc, void* stream);
 
+/* per-launch profile of one device multiply (same launches as dkss_mul_device, not graphed):
+ * a CUDA event is recorded on `stream` after every kernel; for launch i, kinds[i] is a
+ * DKSS_K_* id, ms[i] its event-to-event duration, work[i] the algorithmic 32x32->64 limb
+ * products it performs (ring products x m^2 L^2) and bytes[i] the
+ * stage-boundary HBM bytes of the §8(d) model.  c_dev receives the product (product_limbs). */
+#define DKSS_K_ENCODE 0
+#define DKSS_K_FWD_PASS 1
+#define DKSS_K_BOTTOM 2
+#define DKSS_K_INV_PASS 3
+#define DKSS_K_DECODE1 4
+#define DKSS_K_DECODE2 5
+int dkss_profile_device(dkss_plan* plan, int batch, const uint32_t* a_dev, const uint32_t* b_dev, size_t n_limbs,
+                        uint32_t* c_dev, void* stream, int max_launches, int32_t* kinds, float* ms, int64_t* work,
+                        int64_t* bytes, int* n_launches);
+
 /* stage entry points for parity checks (host buffers) ------------------------------ */
 /* dkss_encode, bigmul/dkss.py:381-398: poly = uint32[2M][m][L] */
 int dkss_encode_host(dkss_plan* plan, const uint32_t* a, size_t na, uint32_t* poly);

@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(HERE, "_lib", "libdkss.so")
 # every symbol include/dkss.h declares (checked by tests/test_native_abi.py)
 EXPORTS = (
     "dkss_plan_create", "dkss_plan_destroy", "dkss_plan_get_info", "dkss_last_error", "dkss_version",
-    "dkss_mul", "dkss_mul_batch", "dkss_mul_device",
+    "dkss_mul", "dkss_mul_batch", "dkss_mul_device", "dkss_profile_device",
     "dkss_encode_host", "dkss_fft_host", "dkss_rmul_host", "dkss_decode_host",
 )
 
@@ -78,6 +78,10 @@ def load(path: str = LIB_PATH):
         L.dkss_mul.argtypes = [vp, _u32p, ctypes.c_size_t, _u32p, ctypes.c_size_t, _u32p, ctypes.c_size_t]
         L.dkss_mul_batch.argtypes = [vp, ctypes.c_int, _u32p, _u32p, ctypes.c_size_t, _u32p, ctypes.c_size_t]
         L.dkss_mul_device.argtypes = [vp, ctypes.c_int, vp, vp, ctypes.c_size_t, vp, ctypes.c_size_t, vp]
+        L.dkss_profile_device.argtypes = [vp, ctypes.c_int, vp, vp, ctypes.c_size_t, vp, vp, ctypes.c_int,
+                                          ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_float),
+                                          ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                                          ctypes.POINTER(ctypes.c_int)]
         L.dkss_encode_host.argtypes = [vp, _u32p, ctypes.c_size_t, _u32p]
         L.dkss_fft_host.argtypes = [vp, _u32p, ctypes.c_int]
         L.dkss_rmul_host.argtypes = [vp, _u32p, _u32p, _u32p, ctypes.c_size_t]
@@ -158,6 +162,21 @@ class DevicePlan:
     def mul_device(self, batch: int, a_ptr: int, b_ptr: int, n_limbs: int, c_ptr: int, nc: int, stream: int = 0):
         _check(self._lib.dkss_mul_device(self._h, batch, ctypes.c_void_p(a_ptr), ctypes.c_void_p(b_ptr), n_limbs,
                                          ctypes.c_void_p(c_ptr), nc, ctypes.c_void_p(stream)))
+
+    KIND_NAMES = {0: "encode", 1: "fwd_pass", 2: "bottom", 3: "inv_pass", 4: "decode1", 5: "decode2"}
+
+    def profile_device(self, batch: int, a_ptr: int, b_ptr: int, n_limbs: int, c_ptr: int, stream: int = 0):
+        """Per-launch (kind, ms, limb-products, bytes) of one multiply, timed with CUDA events."""
+        mx = 64
+        kinds = (ctypes.c_int32 * mx)()
+        ms = (ctypes.c_float * mx)()
+        work = (ctypes.c_int64 * mx)()
+        nbytes = (ctypes.c_int64 * mx)()
+        n = ctypes.c_int()
+        _check(self._lib.dkss_profile_device(self._h, batch, ctypes.c_void_p(a_ptr), ctypes.c_void_p(b_ptr), n_limbs,
+                                             ctypes.c_void_p(c_ptr), ctypes.c_void_p(stream), mx, kinds, ms, work,
+                                             nbytes, ctypes.byref(n)))
+        return [(self.KIND_NAMES[kinds[i]], ms[i], work[i], nbytes[i]) for i in range(n.value)]
 
     # -- stages ----------------------------------------------------------------
     def encode(self, a_limbs: np.ndarray) -> np.ndarray:

@@ -135,6 +135,13 @@ struct dkss_plan {
   cudaStream_t stream = nullptr;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   std::mutex mu;
+  struct Prof {
+    static constexpr int kMax = 64;
+    cudaEvent_t ev[kMax + 1];
+    int kind[kMax];
+    long long work[kMax], bytes[kMax];
+    int n = 0;
+  }* prof = nullptr;  // non-null only inside dkss_profile_device
 };
 
 namespace {
@@ -181,6 +188,24 @@ int ensure_pin(dkss_plan* P, size_t words) {
   return 0;
 }
 
+// per-launch accounting hook (kinds: see dkss.h DKSS_K_*)
+void mark(dkss_plan* P, cudaStream_t s, int kind, long long work, long long bytes) {
+  auto* pr = P->prof;
+  if (!pr || pr->n >= dkss_plan::Prof::kMax) return;
+  pr->kind[pr->n] = kind;
+  pr->work[pr->n] = work;
+  pr->bytes[pr->n] = bytes;
+  cudaEventRecord(pr->ev[++pr->n], s);
+}
+
+long long rp_work(const dkss_plan* P, long long ring_products) { return ring_products * P->m * P->m * P->L * P->L; }
+
+long long level_twiddles(const dkss_plan* P, int lv) {
+  const long long E = 2LL * P->m;
+  const long long mu = (2LL * P->M) >> (P->logE * (lv + 1));
+  return (1LL << (P->logE * lv)) * (E - 1) * (mu - 1);
+}
+
 size_t smem_bytes(const dkss_plan* P, int nbuf) { return (size_t)nbuf * P->kt.ne * P->kt.es * 4; }
 
 // --- launch helpers (all stream-ordered) ---------------------------------------------
@@ -190,6 +215,7 @@ int launch_encode(dkss_plan* P, const uint32_t* ops, long long na, uint32_t* pol
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
   k_encode<<<blocks, 256, 0, s>>>(A);
   CUCHK(cudaGetLastError());
+  mark(P, s, DKSS_K_ENCODE, 0, npoly * (P->op_limbs * 4 + P->poly_words * 4));
   return 0;
 }
 
@@ -209,6 +235,7 @@ int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s) {
     A.total_cols = cols;
     P->kt.fwd<<<grid, kThreads, smem_bytes(P, 1), s>>>(A, P->mc);
     CUCHK(cudaGetLastError());
+    mark(P, s, DKSS_K_FWD_PASS, rp_work(P, npoly * level_twiddles(P, lv)), 2LL * npoly * P->poly_words * 4);
   }
   return 0;
 }
@@ -228,6 +255,7 @@ int launch_inv_levels(dkss_plan* P, uint32_t* poly, int npoly, bool scale_last, 
     A.total_cols = cols;
     P->kt.inv<<<grid, kThreads, smem_bytes(P, 2), s>>>(A, P->mc);
     CUCHK(cudaGetLastError());
+    mark(P, s, DKSS_K_INV_PASS, rp_work(P, npoly * level_twiddles(P, lv)), 2LL * npoly * P->poly_words * 4);
   }
   return 0;
 }
@@ -246,6 +274,8 @@ int launch_bottom(dkss_plan* P, uint32_t* a, const uint32_t* b, int npoly, int m
   A.total_elems = elems;
   P->kt.bottom<<<grid, kThreads, smem_bytes(P, 2), s>>>(A, P->mc);
   CUCHK(cudaGetLastError());
+  mark(P, s, DKSS_K_BOTTOM, mode ? rp_work(P, 2LL * P->M * npoly) : 0,
+       (mode ? 3LL : 2LL) * npoly * P->poly_words * 4);
   return 0;
 }
 
@@ -266,8 +296,10 @@ int launch_decode(dkss_plan* P, const uint32_t* v, uint32_t* out, int npoly, cud
   const int grid = A.blocks_per_poly * npoly;
   k_decode1<<<grid, kDecThreads, 0, s>>>(A);
   CUCHK(cudaGetLastError());
+  mark(P, s, DKSS_K_DECODE1, 0, npoly * (P->poly_words * 4 + P->prod_limbs * 4));
   k_decode2<<<grid, kDecThreads, 0, s>>>(A);
   CUCHK(cudaGetLastError());
+  mark(P, s, DKSS_K_DECODE2, 0, npoly * 2LL * P->prod_limbs * 4);
   return 0;
 }
 
@@ -462,6 +494,38 @@ int dkss_mul_device(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* 
   }
   CUCHK(cudaGraphLaunch(it->second, s));
   return DKSS_OK;
+}
+
+int dkss_profile_device(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, size_t nl, uint32_t* c,
+                        void* stream, int max_launches, int32_t* kinds, float* ms, int64_t* work, int64_t* bytes,
+                        int* n_launches) {
+  if (!P || batch < 1 || !a || !b || !c || !kinds || !ms || !n_launches) return fail(DKSS_EINVAL, "bad argument");
+  if ((long long)nl > P->op_limbs) return fail(DKSS_ERANGE, "operand limbs exceed plan");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  int rc;
+  if ((rc = ensure_ws(P, batch))) return rc;
+  dkss_plan::Prof pr;
+  for (int i = 0; i <= dkss_plan::Prof::kMax; ++i) CUCHK(cudaEventCreate(&pr.ev[i]));
+  cudaStream_t s = (cudaStream_t)stream;
+  P->prof = &pr;
+  cudaEventRecord(pr.ev[0], s);
+  rc = run_mul(P, batch, a, b, (long long)nl, c, s);
+  P->prof = nullptr;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (!rc && e != cudaSuccess) rc = fail(DKSS_ECUDA, "profile run failed: %s", cudaGetErrorString(e));
+  if (!rc) {
+    const int n = std::min(pr.n, max_launches);
+    for (int i = 0; i < n; ++i) {
+      kinds[i] = pr.kind[i];
+      cudaEventElapsedTime(&ms[i], pr.ev[i], pr.ev[i + 1]);
+      if (work) work[i] = pr.work[i];
+      if (bytes) bytes[i] = pr.bytes[i];
+    }
+    *n_launches = n;
+  }
+  for (int i = 0; i <= dkss_plan::Prof::kMax; ++i) cudaEventDestroy(pr.ev[i]);
+  return rc;
 }
 
 int dkss_mul_batch(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, size_t nl, uint32_t* c, size_t nc) {

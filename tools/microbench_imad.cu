@@ -3,10 +3,16 @@
 // independent accumulator chains per thread and issues one instruction class in a tight loop.
 // Output: one JSON line per instruction class with ops/clk/SM and ops/s at the observed clock.
 //
-// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench_imad tools/microbench_imad.cu
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench_imad tools/microbench_imad.cu -lnvidia-ml
+// SM clocks are sampled with NVML while each kernel runs (~0.3 s per kernel).
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <nvml.h>
+#include <thread>
+#include <atomic>
+#include <vector>
+#include <algorithm>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); return 1; } } while (0)
 
@@ -118,7 +124,7 @@ int main() {
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   CK(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev));
-  const int threads = 256, blocks_per_sm = 4, blocks = sms * blocks_per_sm, iters = 4096;
+  const int threads = 256, blocks_per_sm = 4, blocks = sms * blocks_per_sm, iters = 4096 * 48;
   uint64_t* out; long long* cyc;
   CK(cudaMalloc(&out, sizeof(uint64_t) * blocks * threads));
   CK(cudaMalloc(&cyc, sizeof(long long) * blocks));
@@ -132,22 +138,37 @@ int main() {
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
   long long* hc = new long long[blocks];
+  nvmlDevice_t nvdev;
+  bool nv = nvmlInit() == NVML_SUCCESS && nvmlDeviceGetHandleByIndex(0, &nvdev) == NVML_SUCCESS;
   for (auto& k : ks) {
     for (int rep = 0; rep < 2; ++rep) {  // first pass = warm-up
+      std::atomic<bool> stop(false);
+      std::vector<unsigned> clk;
+      std::thread sampler([&] {
+        while (nv && !stop.load()) {
+          unsigned c = 0;
+          if (nvmlDeviceGetClockInfo(nvdev, NVML_CLOCK_SM, &c) == NVML_SUCCESS) clk.push_back(c);
+          std::this_thread::sleep_for(std::chrono::milliseconds(5));
+        }
+      });
       CK(cudaEventRecord(e0));
       k.f<<<blocks, threads>>>(out, cyc, iters);
       CK(cudaEventRecord(e1));
       CK(cudaEventSynchronize(e1));
+      stop = true;
+      sampler.join();
       CK(cudaGetLastError());
       if (rep == 0) continue;
+      std::sort(clk.begin(), clk.end());
+      unsigned med = clk.empty() ? 0 : clk[clk.size() / 2];
       float ms = 0; CK(cudaEventElapsedTime(&ms, e0, e1));
       CK(cudaMemcpy(hc, cyc, sizeof(long long) * blocks, cudaMemcpyDeviceToHost));
       double avgc = 0; for (int i = 0; i < blocks; ++i) avgc += hc[i]; avgc /= blocks;
       double ops = (double)blocks * threads * iters * 8 * ILP * k.ops_per_inner;
       double ops_per_clk_sm = ops / sms / avgc;
       double ghz = avgc / (ms * 1e-3) / 1e9;  // SM cycles per wall second (all blocks concurrent)
-      printf("{\"instr\": \"%s\", \"ops_per_clk_per_sm\": %.2f, \"ops_per_s\": %.4e, \"kernel_ms\": %.4f, \"sm_ghz_est\": %.3f, \"sms\": %d}\n",
-             k.name, ops_per_clk_sm, ops / (ms * 1e-3), ms, ghz, sms);
+      printf("{\"instr\": \"%s\", \"ops_per_clk_per_sm\": %.2f, \"ops_per_s\": %.4e, \"kernel_ms\": %.4f, \"sm_ghz_est\": %.3f, \"nvml_sm_mhz_median\": %u, \"nvml_samples\": %zu, \"sms\": %d}\n",
+             k.name, ops_per_clk_sm, ops / (ms * 1e-3), ms, ghz, med, clk.size(), sms);
     }
   }
   printf("{\"clock_rate_attr_mhz\": %d}\n", clk_khz / 1000);
