@@ -1,19 +1,11 @@
 // dkss_arith.cuh -- multi-limb arithmetic mod p for the DKSS ring R = (Z/pZ)[alpha]/(alpha^m+1).
 //
 // Residues are canonical in [0, p), stored as L little-endian u32 limbs (L = ceil(d/32)).
-// The ring product (reference r_mul, bigmul/dkss.py:401-420) is computed here as a
-// negacyclic convolution
-//     c_k = sum_i x_i * z_{k-i},   z_j = y_j (j >= 0),  z_j = p - y_{j+m} (j < 0)
-// so every term is a plain non-negative product (the wrap alpha^m = -1 is folded into
-// z).  Products are accumulated exactly in radix-2^28 column sums held in 64-bit
-// registers: each 28x28-bit digit product is ONE IMAD.WIDE.U32 (a*b + c64) with no
-// carry handling at all (measured ~100 IMAD.WIDE/clk/SM on B200, vs ~50 limb products
-// per clk/SM for the radix-2^32 mad.lo.cc/madc.hi.cc chain; tools/microbench_imad.cu).
-// Column capacity: m * ndig products of < 2^56 each <= 32*7*2^56 < 2^64.
-//
-// One Montgomery reduction (R = 2^(32L)) per output coefficient brings the
-// <= 2d+log2(m)-bit sum back to a canonical residue; twiddle tables are stored in
-// Montgomery form (rho^s * R mod p) so twiddle products come out exact.
+// Modular reduction is Montgomery's (R = 2^(32L)) with a single-precision quotient
+// estimate for the final canonicalisation, so every prime the planner can select works
+// (d from 56 to 192 bits).  The ring product itself lives in dkss_kernels.cuh (ring_mul);
+// twiddle tables are stored in Montgomery form (rho^s * R mod p) so twiddle products come
+// out exact, and the pointwise product's R^-1 is undone by the final (2M)^-1 scaling.
 #pragma once
 #include <cstdint>
 
@@ -32,39 +24,8 @@ struct ModCtx {
   uint32_t kinv[DKSS_MAXL];    // (2M)^-1 * R mod p    (plain (2M)^-1 scaling)
   uint32_t pinv;               // -p^-1 mod 2^32
   float pf_inv;                // 2^(32(L-2)) / p  (quotient estimate)
+  uint32_t cbias[DKSS_MAXL];   // -(2^(32L) - 1) * R mod p  (ring_mul bias correction)
 };
-
-template <int L>
-struct NDig {
-  static constexpr int v = (32 * L + 27) / 28;  // radix-2^28 digits covering 32L bits
-};
-
-__device__ __forceinline__ uint32_t fshr(uint32_t lo, uint32_t hi, uint32_t sh) {
-  return __funnelshift_r(lo, hi, sh);
-}
-
-// radix-2^32 limbs -> radix-2^28 digits
-template <int L>
-__device__ __forceinline__ void to_r28(const uint32_t (&w)[L], uint32_t (&d)[NDig<L>::v]) {
-  constexpr int ND = NDig<L>::v;
-#pragma unroll
-  for (int j = 0; j < ND; ++j) {
-    const int bit = 28 * j, q = bit >> 5, s = bit & 31;
-    const uint32_t lo = q < L ? w[q] : 0u;
-    const uint32_t hi = q + 1 < L ? w[q + 1] : 0u;
-    d[j] = (s == 0 ? lo : fshr(lo, hi, s)) & 0x0FFFFFFFu;
-  }
-}
-
-// acc[t] += x (x) z over digit columns: NDxND IMAD.WIDE.U32, no carries
-template <int ND>
-__device__ __forceinline__ void mac_cols(uint64_t (&acc)[2 * ND - 1], const uint32_t (&x)[ND],
-                                         const uint32_t (&z)[ND]) {
-#pragma unroll
-  for (int a = 0; a < ND; ++a)
-#pragma unroll
-    for (int b = 0; b < ND; ++b) acc[a + b] += (uint64_t)x[a] * z[b];
-}
 
 // r (L limbs) = (a + b) mod p
 template <int L>
@@ -138,8 +99,11 @@ __device__ __forceinline__ void neg_mod_canon(uint32_t (&r)[L], const uint32_t (
   for (int i = 0; i < L; ++i) r[i] = nz ? t[i] : 0u;
 }
 
-// Montgomery reduction of a (2L+1)-limb value T < 2^(32(2L+1)) with T/R < 2^32 * p
-// (true for every caller: T < m*p^2 + small).  Returns the canonical residue T*R^-1 mod p.
+// Montgomery reduction of a (2L+1)-limb value T < 2^(32(2L+1)).  After the L REDC steps
+// v = (T + q p)/R < T/R + p; the quotient floor(v/p) is estimated in single precision from
+// the top three limbs, which is exact to +-1 while v/p < 2^20 (callers: ring products give
+// T < m * 2^(32L) * p + p, i.e. v/p <= m + 1; mont_mul gives T < p^2).
+// Returns the canonical residue T*R^-1 mod p.
 template <int L>
 __device__ __forceinline__ void redc(uint32_t (&r)[L], uint32_t (&t)[2 * L + 1], const ModCtx& M) {
 #pragma unroll
@@ -202,32 +166,6 @@ __device__ __forceinline__ void redc(uint32_t (&r)[L], uint32_t (&t)[2 * L + 1],
     const bool ge = (b2 == 0);
 #pragma unroll
     for (int j = 0; j < L; ++j) r[j] = ge ? w[j] : v[j];
-  }
-}
-
-// radix-2^28 column sums -> (2L+1) radix-2^32 limbs (value < 2^(32(2L+1)) by the bound)
-template <int L>
-__device__ __forceinline__ void cols_to_limbs(const uint64_t (&col)[2 * NDig<L>::v - 1], uint32_t (&t)[2 * L + 1]) {
-  constexpr int ND = NDig<L>::v;
-  constexpr int NC = 2 * ND - 1;
-  constexpr int NT = 2 * L + 1;
-  uint32_t dg[NC + 2];
-  uint64_t c = 0;
-#pragma unroll
-  for (int k = 0; k < NC; ++k) {
-    c += col[k];
-    dg[k] = (uint32_t)c & 0x0FFFFFFFu;
-    c >>= 28;
-  }
-  dg[NC] = (uint32_t)c & 0x0FFFFFFFu;
-  dg[NC + 1] = (uint32_t)(c >> 28);
-#pragma unroll
-  for (int i = 0; i < NT; ++i) t[i] = 0;
-#pragma unroll
-  for (int k = 0; k < NC + 2; ++k) {
-    const int bit = 28 * k, q = bit >> 5, s = bit & 31;
-    if (q < NT) t[q] |= dg[k] << s;
-    if (s > 4 && q + 1 < NT) t[q + 1] |= dg[k] >> (32 - s);
   }
 }
 

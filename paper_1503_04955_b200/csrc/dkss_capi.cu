@@ -120,7 +120,9 @@ struct dkss_plan {
   long long twiddles = 0;
   ModCtx mc{};
   KTable kt{};
-  uint32_t* d_tw = nullptr;  // Montgomery-form rho table
+  uint32_t* d_tw = nullptr;   // Montgomery-form rho table [M/m][m][L]
+  uint32_t* d_twr = nullptr;  // twiddle rows [M/m][2m][L]: Montgomery-form rho^s, then W_s
+  int grid_pass = 0, grid_bot = 0;  // persistent grid sizes (SMs x resident CTAs)
   // workspace
   int cap_batch = 0;
   uint32_t* d_poly = nullptr;  // 2 * cap_batch polynomials
@@ -206,7 +208,8 @@ long long level_twiddles(const dkss_plan* P, int lv) {
   return (1LL << (P->logE * lv)) * (E - 1) * (mu - 1);
 }
 
-size_t smem_bytes(const dkss_plan* P, int nbuf) { return (size_t)nbuf * P->kt.ne * P->kt.es * 4; }
+size_t smem_pass(const dkss_plan* P) { return P->kt.smem_pass; }
+size_t smem_two(const dkss_plan* P) { return P->kt.smem_bot; }
 
 // --- launch helpers (all stream-ordered) ---------------------------------------------
 int launch_encode(dkss_plan* P, const uint32_t* ops, long long na, uint32_t* poly, int npoly, cudaStream_t s) {
@@ -221,7 +224,7 @@ int launch_encode(dkss_plan* P, const uint32_t* ops, long long na, uint32_t* pol
 
 int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s) {
   const long long cols = (long long)npoly << P->log_top_mu;
-  const int grid = (int)((cols + P->kt.cols - 1) / P->kt.cols);
+  const int grid = (int)std::min<long long>((cols + P->kt.cols - 1) / P->kt.cols, P->grid_pass);
   for (int lv = 0; lv < P->levels; ++lv) {
     PassArgs A{};
     A.poly = poly;
@@ -230,10 +233,10 @@ int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s) {
     A.log_mu = ilog2i(2LL * P->M) - P->logE * (lv + 1);
     A.log_top_mu = P->log_top_mu;
     A.base_pow = 1LL << (P->logE * lv);
-    A.tw = P->d_tw;
+    A.twr = P->d_twr;
     A.scale = 0;
     A.total_cols = cols;
-    P->kt.fwd<<<grid, kThreads, smem_bytes(P, 1), s>>>(A, P->mc);
+    P->kt.fwd<<<grid, P->kt.nt, smem_pass(P), s>>>(A, P->mc);
     CUCHK(cudaGetLastError());
     mark(P, s, DKSS_K_FWD_PASS, rp_work(P, npoly * level_twiddles(P, lv)), 2LL * npoly * P->poly_words * 4);
   }
@@ -242,7 +245,7 @@ int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s) {
 
 int launch_inv_levels(dkss_plan* P, uint32_t* poly, int npoly, bool scale_last, cudaStream_t s) {
   const long long cols = (long long)npoly << P->log_top_mu;
-  const int grid = (int)((cols + P->kt.cols - 1) / P->kt.cols);
+  const int grid = (int)std::min<long long>((cols + P->kt.cols - 1) / P->kt.cols, P->grid_pass);
   for (int lv = P->levels - 1; lv >= 0; --lv) {
     PassArgs A{};
     A.poly = poly;
@@ -250,10 +253,10 @@ int launch_inv_levels(dkss_plan* P, uint32_t* poly, int npoly, bool scale_last, 
     A.log_mu = ilog2i(2LL * P->M) - P->logE * (lv + 1);
     A.log_top_mu = P->log_top_mu;
     A.base_pow = 1LL << (P->logE * lv);
-    A.tw = P->d_tw;
+    A.twr = P->d_twr;
     A.scale = (lv == 0 && scale_last) ? 1 : 0;
     A.total_cols = cols;
-    P->kt.inv<<<grid, kThreads, smem_bytes(P, 2), s>>>(A, P->mc);
+    P->kt.inv<<<grid, P->kt.nt, smem_pass(P), s>>>(A, P->mc);
     CUCHK(cudaGetLastError());
     mark(P, s, DKSS_K_INV_PASS, rp_work(P, npoly * level_twiddles(P, lv)), 2LL * npoly * P->poly_words * 4);
   }
@@ -270,9 +273,9 @@ int launch_bottom(dkss_plan* P, uint32_t* a, const uint32_t* b, int npoly, int m
   A.mode = mode;
   A.scale = scale ? 1 : 0;
   const long long elems = 2LL * P->M * npoly;
-  const int grid = (int)((elems + P->kt.ne - 1) / P->kt.ne);
+  const int grid = (int)std::min<long long>((elems + P->kt.ne - 1) / P->kt.ne, P->grid_bot);
   A.total_elems = elems;
-  P->kt.bottom<<<grid, kThreads, smem_bytes(P, 2), s>>>(A, P->mc);
+  P->kt.bottom<<<grid, P->kt.nt, smem_two(P), s>>>(A, P->mc);
   CUCHK(cudaGetLastError());
   mark(P, s, DKSS_K_BOTTOM, mode ? rp_work(P, 2LL * P->M * npoly) : 0,
        (mode ? 3LL : 2LL) * npoly * P->poly_words * 4);
@@ -403,11 +406,43 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
   for (int i = L - 1; i >= 0; --i) pd = pd * 4294967296.0 + p[i];
   P->mc.pf_inv = (float)(ldexp(1.0, 32 * (L - 2)) / pd);
   // kernels: opt into >48 KB dynamic smem
-  const size_t sm2 = smem_bytes(P, 2);
-  CUCHK(cudaFuncSetAttribute(kt.fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(P, 1)));
-  CUCHK(cudaFuncSetAttribute(kt.inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-  CUCHK(cudaFuncSetAttribute(kt.bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-  CUCHK(cudaFuncSetAttribute(kt.rmul, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+  // kernels: opt into >48 KB dynamic smem and the max-shared carveout; persistent grids
+  {
+    const void* fns[4] = {(const void*)kt.fwd, (const void*)kt.inv, (const void*)kt.bottom, (const void*)kt.rmul};
+    const size_t need[4] = {kt.smem_pass, kt.smem_pass, kt.smem_bot, kt.smem_rmul};
+    for (int i = 0; i < 4; ++i) {
+      CUCHK(cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need[i]));
+      CUCHK(cudaFuncSetAttribute(fns[i], cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    }
+    int sms = 0, occ_f = 0, occ_i = 0, occ_b = 0;
+    CUCHK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    CUCHK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, kt.fwd, kt.nt, kt.smem_pass));
+    CUCHK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_i, kt.inv, kt.nt, kt.smem_pass));
+    CUCHK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, kt.bottom, kt.nt, kt.smem_bot));
+    if (occ_f < 1 || occ_i < 1 || occ_b < 1) {
+      delete P;
+      return fail(DKSS_EINVAL, "kernels for m=%d L=%d do not fit an SM", m, L);
+    }
+    P->grid_pass = sms * std::min(occ_f, occ_i);
+    P->grid_bot = sms * occ_b;
+  }
+  // cbias = -(2^(32L) - 1) * R mod p = (p - ((R mod p) - 1)) * R mod p  (ring_mul bias correction)
+  {
+    Limbs b = rmod;  // R mod p
+    // b = (R mod p) - 1  (R mod p != 0 since p is odd and > 1)
+    for (int i = 0; i < L; ++i) {
+      if (b[i]--) break;
+    }
+    Limbs nb(L, 0);  // p - b  (b in [0, p))
+    bool bz = true;
+    for (int i = 0; i < L; ++i) bz = bz && b[i] == 0;
+    if (!bz) {
+      nb = p;
+      sub_inplace(nb, b);
+    }
+    for (int i = 0; i < 32 * L; ++i) dbl_mod(nb, p);  // * R
+    memcpy(P->mc.cbias, nb.data(), 4 * L);
+  }
   CUCHK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
   // twiddle table -> Montgomery form
   const size_t tw_words = (size_t)(M / m) * m * L;
@@ -416,6 +451,12 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
   if (e == cudaSuccess) {
     kt.mscale<<<(int)std::min<size_t>((tw_words / L + 255) / 256, 4096), 256, 0, P->stream>>>(P->d_tw, tw_words / L, 0,
                                                                                                P->mc);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_twr, (size_t)(M / m) * 2 * m * L * 4);
+  if (e == cudaSuccess) {
+    kt.build_twr<<<(int)std::min<size_t>(((size_t)(M / m) * m + 255) / 256, 4096), 256, 0, P->stream>>>(
+        P->d_tw, P->d_twr, (long long)(M / m), m, P->mc);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(P->stream);
@@ -432,6 +473,7 @@ void dkss_plan_destroy(dkss_plan* P) {
   cudaSetDevice(P->device);
   free_ws(P);
   cudaFree(P->d_tw);
+  cudaFree(P->d_twr);
   if (P->h_pin) cudaFreeHost(P->h_pin);
   if (P->stream) cudaStreamDestroy(P->stream);
   delete P;
@@ -632,7 +674,7 @@ int dkss_rmul_host(dkss_plan* P, const uint32_t* x, const uint32_t* y, uint32_t*
   cudaMemcpyAsync(dx, x, count * ew * 4, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(dy, y, count * ew * 4, cudaMemcpyHostToDevice, s);
   const int grid = (int)((count + P->kt.ne - 1) / P->kt.ne);
-  P->kt.rmul<<<grid, kThreads, smem_bytes(P, 2), s>>>(dx, dy, dout, (long long)count, P->mc);
+  P->kt.rmul<<<grid, P->kt.nt, P->kt.smem_rmul, s>>>(dx, dy, dout, (long long)count, P->mc);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, count * ew * 4, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);

@@ -15,30 +15,99 @@
 // the TRANSPOSE of our forward pass sequence, F P^-1 = (P F)^T: the same passes in
 // reverse order with "twiddle, then column DFT" (the DFT and twiddle matrices are
 // symmetric).  Only stage-level parity checks permute back to natural order.
+//
+// Kernel shape.  Every pass kernel is persistent: a CTA walks tiles (NE elements = COLS
+// columns, or NE contiguous elements for the bottom kernel) with a 2-stage pipeline --
+// TMA bulk copies (cp.async.bulk, mbarrier completion) bring tile k+1's elements and
+// twiddle rows into shared memory while tile k is transformed and multiplied.
 #pragma once
 #include <cstdint>
 #include "dkss_arith.cuh"
 
 namespace dkss {
 
-constexpr int kThreads = 256;
-constexpr int kT = 4;  // output coefficients per thread in a ring product
 
-// words per element in shared memory: padded so that 8 elements read by one warp
-// (4 threads each) land on distinct banks
+__host__ __device__ constexpr int pad_4mod8(int w) { return ((w + 3) / 8) * 8 + 4; }
+
+// shared-memory strides (words).  Elements are L-limb residues x MM coefficients, padded
+// so the elements touched by one warp start on different banks.  A twiddle row holds
+// [rho~_s (MM residues) | W_s (MM residues)]; a W row holds MM residues.
 template <int MM, int L>
 struct Smem {
   static constexpr int ES = ((MM * L + 31) / 32) * 32 + 4;
+  static constexpr int EST = pad_4mod8(2 * MM * L);
+  static constexpr int ESW = pad_4mod8(MM * L);
 };
 
+// CTA shape per inner length m: NT threads, NE elements (COLS columns of 2m) per tile; a
+// ring-product work item is T consecutive output coefficients of one element.  Registers
+// are capped by MINB CTAs per SM.  TWS: twiddle rows staged in shared memory by TMA
+// (m = 32 reads them through L1 instead -- the shared-memory budget of a 64-element column).
 template <int MM>
-struct Cfg {
-  // elements per CTA: enough ring-product work items (elements * MM/kT) for kThreads
-  static constexpr int NE = (kThreads * kT / MM) >= 2 * MM ? (kThreads * kT / MM) : 2 * MM;
-  static constexpr int COLS = NE / (2 * MM);
+struct Cfg;
+template <>
+struct Cfg<8> {
+  static constexpr int NT = 256, COLS = 4, NE = 64, MINB = 3, T = 2;
+  static constexpr bool TWS = true;
+};
+template <>
+struct Cfg<16> {
+  static constexpr int NT = 256, COLS = 1, NE = 32, MINB = 3, T = 2;
+  static constexpr bool TWS = true;
+};
+template <>
+struct Cfg<32> {
+  static constexpr int NT = 256, COLS = 1, NE = 64, MINB = 2, T = 2;
+  static constexpr bool TWS = false;
+};
+
+// shared-memory words per CTA, by kernel kind (host uses the same formulas)
+template <int MM, int L>
+struct SmemPlan {
+  using S = Smem<MM, L>;
+  using C = Cfg<MM>;
+  static constexpr int STAGE_PASS = C::NE * S::ES + (C::TWS ? C::NE * S::EST : 0);
+  static constexpr int PASS = 2 * STAGE_PASS;
+  static constexpr int BOT_STAGES = (MM == 32) ? 1 : 2;
+  static constexpr int STAGE_BOT = 2 * C::NE * S::ES;
+  static constexpr int BOT = BOT_STAGES * STAGE_BOT + C::NE * S::ESW;
+  static constexpr int RMUL = 2 * C::NE * S::ES + C::NE * S::ESW;
 };
 
 __device__ __forceinline__ int bitrev_n(int x, int bits) { return bits ? (int)(__brev((unsigned)x) >> (32 - bits)) : 0; }
+
+// ---------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk global -> shared, completion on an mbarrier)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// generic-proxy accesses of this thread are ordered before later async-proxy (TMA) writes
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 template <int L>
 __device__ __forceinline__ void ld_res(uint32_t (&r)[L], const uint32_t* p) {
@@ -80,58 +149,95 @@ __device__ __forceinline__ void st_res(uint32_t* p, const uint32_t (&r)[L]) {
   }
 }
 
+// residue loaders used as ring-product operands
+template <int L>
+struct ResS {  // shared memory, L words per coefficient
+  const uint32_t* p;
+  __device__ __forceinline__ void operator()(int i, uint32_t (&d)[L]) const { ld_res<L>(d, p + i * L); }
+};
+template <int L>
+struct ResG {  // global memory through the read-only path
+  const uint32_t* p;
+  __device__ __forceinline__ void operator()(int i, uint32_t (&d)[L]) const { ld_res_g<L>(d, p + i * L); }
+};
+
 // ---------------------------------------------------------------------------
-// ring product core: out[t] = (x * y)_{k0+t} for t < kT, canonical, times R^-1
-// (Montgomery).  x: element in shared memory (stride L per coefficient).
-// y: loader functor giving the plain coefficient y_j, j in [0, MM).
-template <int MM, int L, class YL>
-__device__ __forceinline__ void ring_mul_rows(const uint32_t* xs, YL yl, int k0, const ModCtx& mc,
-                                              uint32_t (&out)[kT][L]) {
-  constexpr int ND = NDig<L>::v;
-  constexpr int NC = 2 * ND - 1;
-  uint64_t acc[kT][NC];
+// Ring product core (reference r_mul, bigmul/dkss.py:401-420):
+//   out[t] = ((y * x) mod (alpha^MM + 1))_{k0+t} * R^-1 mod p,  t < kT,
+//   c_k = sum_i y_i X_{k-i},  X_j = x_j (j >= 0),  X_j = -x_{j+MM} (j < 0)   (alpha^MM = -1).
+// y (yl(i, r), the outer operand -- the twiddle in the transforms) is read once per step; x
+// (xl(j, r), j in [0, MM)) forms a sliding window of kT residues.  A wrapped window entry is
+// complemented, x' = ~x = B - x with B = 2^(32L) - 1, so every product is non-negative and
+// the accumulated value is c_k + B * sum_{i>k} y_i; wl(k, r) supplies the residue
+// W_k = -B * sum_{i>k} y_i mod p that cancels the bias.  Each 32x32 limb product is
+// accumulated into a column (64-bit sum, 32-bit carry counter) with mad.lo.cc / madc.hi.cc /
+// addc, which ptxas maps to one IMAD.WIDE.U32 with carry-out plus a shared IADD3.X:
+// L^2 wide products per residue pair (the IMAD.WIDE pipe sustains ~30/clk/SM on B200,
+// tools/microbench_imad.cu).
+__device__ __forceinline__ void mac_limb(uint32_t& lo, uint32_t& hi, uint32_t& cy, uint32_t a, uint32_t b) {
+  asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\tmadc.hi.cc.u32 %1, %3, %4, %1;\n\taddc.u32 %2, %2, 0;"
+      : "+r"(lo), "+r"(hi), "+r"(cy)
+      : "r"(a), "r"(b));
+}
+
+#ifndef DKSS_R32_UNROLL
+#define DKSS_R32_UNROLL 4
+#endif
+template <int MM, int L, class YL, class XL, class WL, int kT = Cfg<MM>::T>
+__device__ __forceinline__ void ring_mul(YL yl, XL xl, WL wl, int k0, const ModCtx& mc, uint32_t (&out)[kT][L]) {
+  constexpr int NCOL = 2 * L - 1;
+  constexpr int UNR = DKSS_R32_UNROLL;
+  uint32_t lo[kT][NCOL], hi[kT][NCOL], cy[kT][NCOL];
 #pragma unroll
   for (int t = 0; t < kT; ++t)
 #pragma unroll
-    for (int c = 0; c < NC; ++c) acc[t][c] = 0;
-  uint32_t win[kT][ND];
+    for (int c = 0; c < NCOL; ++c) lo[t][c] = hi[t][c] = cy[t][c] = 0;
+  uint32_t win[kT][L];
 #pragma unroll
-  for (int t = 1; t < kT; ++t) {
-    uint32_t zw[L];
-    yl(k0 + t, zw);
-    to_r28<L>(zw, win[t]);
-  }
-#pragma unroll(MM <= 16 ? MM / kT : 1)
+  for (int t = 1; t < kT; ++t) xl(k0 + t, win[t]);
+#pragma unroll(UNR)
   for (int i0 = 0; i0 < MM; i0 += kT) {
 #pragma unroll
     for (int s = 0; s < kT; ++s) {
       const int i = i0 + s;
-      uint32_t xw[L], xd[ND];
-      ld_res<L>(xw, xs + i * L);
-      to_r28<L>(xw, xd);
-      // new window entry: z_{k0 - i}; negative index wraps with a sign (alpha^m = -1)
+      uint32_t yg[L], xg[L];
+      yl(i, yg);
       const int j = k0 - i;
-      uint32_t yw[L], nw[L];
-      yl(j & (MM - 1), yw);
-      p_minus<L>(nw, yw, mc);
-      const bool wrap = j < 0;
+      xl(j & (MM - 1), xg);
+      const uint32_t msk = (uint32_t)(j >> 31);
 #pragma unroll
-      for (int q = 0; q < L; ++q) yw[q] = wrap ? nw[q] : yw[q];
-      to_r28<L>(yw, win[(kT - s) % kT]);
+      for (int q = 0; q < L; ++q) win[(kT - s) % kT][q] = xg[q] ^ msk;
 #pragma unroll
-      for (int t = 0; t < kT; ++t) mac_cols<ND>(acc[t], xd, win[(t - s + kT) % kT]);
+      for (int t = 0; t < kT; ++t)
+#pragma unroll
+        for (int a = 0; a < L; ++a)
+#pragma unroll
+          for (int b = 0; b < L; ++b)
+            mac_limb(lo[t][a + b], hi[t][a + b], cy[t][a + b], yg[a], win[(t - s + kT) % kT][b]);
     }
   }
 #pragma unroll
   for (int t = 0; t < kT; ++t) {
+    // value = sum_c (lo_c + hi_c 2^32 + cy_c 2^64) 2^(32c) + W_k  ->  2L+1 limbs
+    uint32_t wv[L];
+    wl(k0 + t, wv);
     uint32_t tl[2 * L + 1];
-    cols_to_limbs<L>(acc[t], tl);
+    uint64_t acc = 0;
+#pragma unroll
+    for (int q = 0; q < 2 * L + 1; ++q) {
+      if (q < NCOL) acc += lo[t][q];
+      if (q >= 1 && q - 1 < NCOL) acc += hi[t][q - 1];
+      if (q >= 2 && q - 2 < NCOL) acc += cy[t][q - 2];
+      if (q < L) acc += wv[q];
+      tl[q] = (uint32_t)acc;
+      acc >>= 32;
+    }
     redc<L>(out[t], tl, mc);
   }
 }
 
-// store T consecutive output coefficients k0.. of (alpha^r * w) into element dst
-template <int MM, int L>
+// store kT consecutive output coefficients k0.. of (alpha^r * w) into element dst
+template <int MM, int L, int kT>
 __device__ __forceinline__ void store_rot(uint32_t* dst, const uint32_t (&w)[kT][L], int k0, int r,
                                           const ModCtx& mc) {
 #pragma unroll
@@ -149,6 +255,36 @@ __device__ __forceinline__ void store_rot(uint32_t* dst, const uint32_t (&w)[kT]
   }
 }
 
+// W rows of NE elements y (stride ES) -> dst (stride ESW):
+//   W_k = -(2^(32L) - 1) * sum_{i>k} y_i  mod p   (mc.cbias = -(2^(32L)-1) * R mod p)
+// One thread per element runs the suffix sum (MM-1 modular adds), then all threads scale.
+template <int MM, int L, int NE>
+__device__ __forceinline__ void cta_w_rows(const uint32_t* src, uint32_t* dst, const ModCtx& mc) {
+  constexpr int ES = Smem<MM, L>::ES, ESW = Smem<MM, L>::ESW, NT = Cfg<MM>::NT;
+  for (int el = threadIdx.x; el < NE; el += NT) {
+    uint32_t s[L];
+#pragma unroll
+    for (int q = 0; q < L; ++q) s[q] = 0;
+    st_res<L>(dst + el * ESW + (MM - 1) * L, s);
+    for (int k = MM - 2; k >= 0; --k) {
+      uint32_t y[L];
+      ld_res<L>(y, src + el * ES + (k + 1) * L);
+      add_mod<L>(s, s, y, mc);
+      st_res<L>(dst + el * ESW + k * L, s);
+    }
+  }
+  __syncthreads();
+  for (int it = threadIdx.x; it < NE * MM; it += NT) {
+    const int el = it / MM, k = it % MM;
+    uint32_t s[L], c[L];
+    ld_res<L>(s, dst + el * ESW + k * L);
+#pragma unroll
+    for (int q = 0; q < L; ++q) c[q] = mc.cbias[q];
+    mont_mul<L>(s, s, c, mc);
+    st_res<L>(dst + el * ESW + k * L, s);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // in-place radix-2 DIT over NE elements in shared memory, split into groups of n
 // (power of two <= 2MM) already in bit-reversed order.  Butterfly root for block size
@@ -158,9 +294,9 @@ __device__ __forceinline__ void store_rot(uint32_t* dst, const uint32_t (&w)[kT]
 // (poly_mul_xpow, bigmul/dkss.py:46-61), folded into the add/sub choice.
 template <int MM, int L, int NE>
 __device__ __forceinline__ void dft_inplace(uint32_t* buf, int logn, const ModCtx& mc) {
-  constexpr int ES = Smem<MM, L>::ES;
+  constexpr int ES = Smem<MM, L>::ES, NT = Cfg<MM>::NT;
   constexpr int ITEMS = (NE / 2) * MM;
-  constexpr int PER = (ITEMS + kThreads - 1) / kThreads;
+  constexpr int PER = (ITEMS + NT - 1) / NT;
   for (int ls = 1; ls <= logn; ++ls) {
     const int half = 1 << (ls - 1);
     const int rootstep = (2 * MM) >> ls;  // 2MM / size
@@ -168,17 +304,16 @@ __device__ __forceinline__ void dft_inplace(uint32_t* buf, int logn, const ModCt
     int ia[PER], ib[PER];
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
-      const int it = threadIdx.x + q * kThreads;
+      const int it = threadIdx.x + q * NT;
       ia[q] = -1;
       if (it < ITEMS) {
         const int bf = it / MM, k = it % MM;
         const int blk = bf >> (ls - 1), kk = bf & (half - 1);
         const int a = (blk << ls) + kk, b = a + half;
-        const int e = kk * rootstep;  // < 2MM
+        const int e = kk * rootstep;  // < MM
         int src = k - e;
-        bool neg = false;
-        if (src < 0) { src += MM; neg = true; }
-        if (src < 0) { src += MM; neg = false; }
+        const bool neg = src < 0;
+        if (neg) src += MM;
         uint32_t u[L], x[L];
         ld_res<L>(u, buf + a * ES + k * L);
         ld_res<L>(x, buf + b * ES + src * L);
@@ -212,138 +347,217 @@ struct PassArgs {
   int log_mu;            // column stride mu = 2^log_mu (elements)
   int log_top_mu;        // log2(M/m)
   long long base_pow;    // (2m)^level
-  const uint32_t* tw;    // [M/m][MM][L] Montgomery-form rho^s
+  const uint32_t* twr;   // [M/m][2MM][L]: rho~_s = rho^s R mod p, then W_s (see ring_mul)
   int scale;             // inverse pass: multiply outputs by mc.kscale
   long long total_cols;  // columns in the launch (npoly * M/m)
 };
 
-// forward column pass (one level of dkss_fft): column DFT, then twiddle ring product
-template <int MM, int L>
-__global__ void __launch_bounds__(kThreads) k_fwd_pass(PassArgs A, ModCtx mc) {
-  constexpr int ES = Smem<MM, L>::ES;
-  constexpr int NE = Cfg<MM>::NE, COLS = Cfg<MM>::COLS, E = 2 * MM;
-  constexpr int LOGE = (E == 16) ? 4 : (E == 32) ? 5 : (E == 64) ? 6 : (E == 8) ? 3 : 7;
-  extern __shared__ __align__(16) uint32_t smem[];
-  const long long cols_per_poly = 1LL << A.log_top_mu;  // M/m columns
-  const long long col0 = (long long)blockIdx.x * COLS;
-  const int mu_mask = (1 << A.log_mu) - 1;
-  // load: element j of column c -> smem slot c*E + bitrev(j)
-  constexpr int V4 = MM * L / 4;
-  for (int it = threadIdx.x; it < NE * V4; it += kThreads) {
-    const int el = it / V4, w4 = it % V4;
-    const int c = el / E, j = el % E;
-    const long long cg = col0 + c;
+template <int MM>
+struct Geo {
+  static constexpr int E = 2 * MM;
+  static constexpr int LOGE = (E == 16) ? 4 : (E == 32) ? 5 : (E == 64) ? 6 : (E == 8) ? 3 : 7;
+};
+
+// element j of launch column cg: global word offset, and the column index l in its row
+__device__ __forceinline__ long long col_elem(const PassArgs& A, long long cg, int j, int loge, int elem_words,
+                                              long long* l_out) {
+  const long long poly = cg >> A.log_top_mu, cc = cg & ((1LL << A.log_top_mu) - 1);
+  const long long inst = cc >> A.log_mu, l = cc & ((1LL << A.log_mu) - 1);
+  *l_out = l;
+  return poly * A.poly_words + ((inst << (A.log_mu + loge)) + ((long long)j << A.log_mu) + l) * elem_words;
+}
+
+// twiddle row of element (j, l): s = (j*l*base_pow) mod (M/m), r = its alpha shift
+__device__ __forceinline__ long long tw_exp(const PassArgs& A, int j, long long l, int* r) {
+  const long long e = (long long)j * l * A.base_pow;
+  *r = (int)(e >> A.log_top_mu);
+  return e & ((1LL << A.log_top_mu) - 1);
+}
+
+// warp 0: TMA-load the NE column elements of tile `tile` (FWD: bit-reversed slots) and, when
+// staged, the twiddle row of every element needing a ring product
+template <int MM, int L, bool FWD>
+__device__ __forceinline__ void issue_pass_tile(const PassArgs& A, long long tile, uint64_t* bar, uint32_t* buf,
+                                                uint32_t* tws) {
+  constexpr int ES = Smem<MM, L>::ES, EST = Smem<MM, L>::EST;
+  constexpr int NE = Cfg<MM>::NE, COLS = Cfg<MM>::COLS, E = 2 * MM, LOGE = Geo<MM>::LOGE;
+  constexpr uint32_t EB = MM * L * 4, TB = 2 * MM * L * 4;
+  const int lane = threadIdx.x & 31;
+  uint32_t bytes = 0;
+  for (int e = lane; e < NE; e += 32) {
+    const long long cg = tile * COLS + e / E;
     if (cg >= A.total_cols) continue;
-    const long long poly = cg / cols_per_poly, cc = cg % cols_per_poly;
-    const long long inst = cc >> A.log_mu, l = cc & mu_mask;
-    const long long pos = (inst << (A.log_mu + LOGE)) + ((long long)j << A.log_mu) + l;
-    const uint4 v = *reinterpret_cast<const uint4*>(A.poly + poly * A.poly_words + pos * (MM * L) + w4 * 4);
-    *reinterpret_cast<uint4*>(smem + (c * E + bitrev_n(j, LOGE)) * ES + w4 * 4) = v;
+    bytes += EB;
+    if constexpr (Cfg<MM>::TWS) {
+      long long l;
+      col_elem(A, cg, 0, LOGE, 0, &l);
+      int r;
+      if (tw_exp(A, e % E, l, &r)) bytes += TB;
+    }
+  }
+  bytes = __reduce_add_sync(0xFFFFFFFFu, bytes);
+  if (lane == 0) mbar_expect_tx(bar, bytes);
+  __syncwarp();
+  for (int e = lane; e < NE; e += 32) {
+    const int c = e / E, j = e % E;
+    const long long cg = tile * COLS + c;
+    if (cg >= A.total_cols) continue;
+    long long l;
+    const long long off = col_elem(A, cg, j, LOGE, MM * L, &l);
+    const int slot = FWD ? c * E + bitrev_n(j, LOGE) : e;
+    bulk_g2s(buf + slot * ES, A.poly + off, EB, bar);
+    if constexpr (Cfg<MM>::TWS) {
+      int r;
+      const long long s = tw_exp(A, j, l, &r);
+      if (s) bulk_g2s(tws + e * EST, A.twr + s * (2 * MM * L), TB, bar);
+    }
+  }
+}
+
+// twiddle product of element `el` (x in `xs`) with row s: rho~ from tws (staged) or global
+template <int MM, int L, int kT>
+__device__ __forceinline__ void twiddle_mul(const PassArgs& A, const uint32_t* xs, const uint32_t* tws_el, long long s,
+                                            int k0, const ModCtx& mc, uint32_t (&w)[kT][L]) {
+  if constexpr (Cfg<MM>::TWS) {
+    ring_mul<MM, L>(ResS<L>{tws_el}, ResS<L>{xs}, ResS<L>{tws_el + MM * L}, k0, mc, w);
+  } else {
+    const uint32_t* row = A.twr + s * (2 * MM * L);
+    ring_mul<MM, L>(ResG<L>{row}, ResS<L>{xs}, ResG<L>{row + MM * L}, k0, mc, w);
+  }
+}
+
+// forward column pass (one level of dkss_fft): column DFT, then twiddle ring product
+// rho^(vv*l*base_pow) = alpha^r * rho_table[s] (bigmul/dkss.py:480-492)
+template <int MM, int L>
+__global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArgs A, ModCtx mc) {
+  constexpr int kT = Cfg<MM>::T;
+  constexpr int ES = Smem<MM, L>::ES, EST = Smem<MM, L>::EST;
+  constexpr int NT = Cfg<MM>::NT, NE = Cfg<MM>::NE, COLS = Cfg<MM>::COLS, E = 2 * MM, LOGE = Geo<MM>::LOGE;
+  constexpr int STAGE = SmemPlan<MM, L>::STAGE_PASS;
+  constexpr int TPE = MM / kT;
+  extern __shared__ __align__(16) uint32_t smem[];
+  __shared__ __align__(8) uint64_t bar[2];
+  const long long ntiles = (A.total_cols + COLS - 1) / COLS;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
   }
   __syncthreads();
-  dft_inplace<MM, L, NE>(smem, LOGE, mc);
-  // twiddles rho^(vv*l*base_pow) = alpha^r * rho_table[s] (bigmul/dkss.py:480-492)
-  constexpr int TPE = MM / kT;
-  const long long top_mask = cols_per_poly - 1;
-  for (int it = threadIdx.x; it < NE * TPE; it += kThreads) {
-    const int el = it / TPE, tg = it % TPE, k0 = tg * kT;
-    const int c = el / E, vv = el % E;
-    const long long cg = col0 + c;
-    if (cg >= A.total_cols) continue;
-    const long long poly = cg / cols_per_poly, cc = cg % cols_per_poly;
-    const long long inst = cc >> A.log_mu, l = cc & mu_mask;
-    const long long pos = (inst << (A.log_mu + LOGE)) + ((long long)vv << A.log_mu) + l;
-    uint32_t* dst = A.poly + poly * A.poly_words + pos * (MM * L);
-    const uint32_t* xs = smem + el * ES;
-    const long long e = (long long)vv * l * A.base_pow;
-    const long long s = e & top_mask;
-    const int r = (int)(e >> A.log_top_mu);
-    uint32_t w[kT][L];
-    if (s == 0) {
+  long long tile = blockIdx.x;
+  if (tile < ntiles && threadIdx.x < 32) issue_pass_tile<MM, L, true>(A, tile, &bar[0], smem, smem + NE * ES);
+  for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
+    const int st = k & 1;
+    uint32_t* buf = smem + st * STAGE;
+    uint32_t* tws = buf + NE * ES;
+    const long long nxt = tile + gridDim.x;
+    if (nxt < ntiles && threadIdx.x < 32)
+      issue_pass_tile<MM, L, true>(A, nxt, &bar[st ^ 1], smem + (st ^ 1) * STAGE, smem + (st ^ 1) * STAGE + NE * ES);
+    mbar_wait(&bar[st], (k >> 1) & 1);
+    dft_inplace<MM, L, NE>(buf, LOGE, mc);
+    for (int it = threadIdx.x; it < NE * TPE; it += NT) {
+      const int el = it / TPE, k0 = (it % TPE) * kT;
+      const int c = el / E, vv = el % E;
+      const long long cg = tile * COLS + c;
+      if (cg >= A.total_cols) continue;
+      long long l;
+      uint32_t* dst = A.poly + col_elem(A, cg, vv, LOGE, MM * L, &l);
+      int r;
+      const long long s = tw_exp(A, vv, l, &r);
+      uint32_t w[kT][L];
+      if (s == 0) {
 #pragma unroll
-      for (int t = 0; t < kT; ++t) ld_res<L>(w[t], xs + (k0 + t) * L);
-    } else {
-      const uint32_t* tws = A.tw + s * (MM * L);
-      ring_mul_rows<MM, L>(xs, [&](int j, uint32_t(&y)[L]) { ld_res_g<L>(y, tws + j * L); }, k0, mc, w);
+        for (int t = 0; t < kT; ++t) ld_res<L>(w[t], buf + el * ES + (k0 + t) * L);
+      } else {
+        twiddle_mul<MM, L, kT>(A, buf + el * ES, tws + el * EST, s, k0, mc, w);
+      }
+      store_rot<MM, L, kT>(dst, w, k0, r, mc);
     }
-    store_rot<MM, L>(dst, w, k0, r, mc);
+    fence_proxy_async();
+    __syncthreads();
   }
 }
 
 // inverse (transposed) column pass: twiddle ring product, then column DFT
 template <int MM, int L>
-__global__ void __launch_bounds__(kThreads) k_inv_pass(PassArgs A, ModCtx mc) {
-  constexpr int ES = Smem<MM, L>::ES;
-  constexpr int NE = Cfg<MM>::NE, COLS = Cfg<MM>::COLS, E = 2 * MM;
-  constexpr int LOGE = (E == 16) ? 4 : (E == 32) ? 5 : (E == 64) ? 6 : (E == 8) ? 3 : 7;
-  extern __shared__ __align__(16) uint32_t smem[];
-  uint32_t* raw = smem;
-  uint32_t* tw_buf = smem + NE * ES;
-  const long long cols_per_poly = 1LL << A.log_top_mu;
-  const long long col0 = (long long)blockIdx.x * COLS;
-  const int mu_mask = (1 << A.log_mu) - 1;
-  constexpr int V4 = MM * L / 4;
-  for (int it = threadIdx.x; it < NE * V4; it += kThreads) {
-    const int el = it / V4, w4 = it % V4;
-    const int c = el / E, j = el % E;
-    const long long cg = col0 + c;
-    if (cg >= A.total_cols) continue;
-    const long long poly = cg / cols_per_poly, cc = cg % cols_per_poly;
-    const long long inst = cc >> A.log_mu, l = cc & mu_mask;
-    const long long pos = (inst << (A.log_mu + LOGE)) + ((long long)j << A.log_mu) + l;
-    const uint4 v = *reinterpret_cast<const uint4*>(A.poly + poly * A.poly_words + pos * (MM * L) + w4 * 4);
-    *reinterpret_cast<uint4*>(raw + el * ES + w4 * 4) = v;
-  }
-  __syncthreads();
+__global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArgs A, ModCtx mc) {
+  constexpr int kT = Cfg<MM>::T;
+  constexpr int ES = Smem<MM, L>::ES, EST = Smem<MM, L>::EST;
+  constexpr int NT = Cfg<MM>::NT, NE = Cfg<MM>::NE, COLS = Cfg<MM>::COLS, E = 2 * MM, LOGE = Geo<MM>::LOGE;
+  constexpr int STAGE = SmemPlan<MM, L>::STAGE_PASS;
   constexpr int TPE = MM / kT;
-  const long long top_mask = cols_per_poly - 1;
-  for (int it = threadIdx.x; it < NE * TPE; it += kThreads) {
-    const int el = it / TPE, tg = it % TPE, k0 = tg * kT;
-    const int c = el / E, j = el % E;
-    if (col0 + c >= A.total_cols) continue;
-    const long long cc = (col0 + c) % cols_per_poly;
-    const long long l = cc & mu_mask;
-    const uint32_t* xs = raw + el * ES;
-    const long long e = (long long)j * l * A.base_pow;
-    const long long s = e & top_mask;
-    const int r = (int)(e >> A.log_top_mu);
-    uint32_t w[kT][L];
-    if (s == 0) {
-#pragma unroll
-      for (int t = 0; t < kT; ++t) ld_res<L>(w[t], xs + (k0 + t) * L);
-    } else {
-      const uint32_t* tws = A.tw + s * (MM * L);
-      ring_mul_rows<MM, L>(xs, [&](int jj, uint32_t(&y)[L]) { ld_res_g<L>(y, tws + jj * L); }, k0, mc, w);
-    }
-    store_rot<MM, L>(tw_buf + (c * E + bitrev_n(j, LOGE)) * ES, w, k0, r, mc);
+  constexpr int PER = (NE * TPE + NT - 1) / NT;
+  extern __shared__ __align__(16) uint32_t smem[];
+  __shared__ __align__(8) uint64_t bar[2];
+  const long long ntiles = (A.total_cols + COLS - 1) / COLS;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
   }
   __syncthreads();
-  dft_inplace<MM, L, NE>(tw_buf, LOGE, mc);
-  for (int it = threadIdx.x; it < NE * MM; it += kThreads) {
-    const int el = it / MM, k = it % MM;
-    const int c = el / E, vv = el % E;
-    const long long cg = col0 + c;
-    if (cg >= A.total_cols) continue;
-    const long long poly = cg / cols_per_poly, cc = cg % cols_per_poly;
-    const long long inst = cc >> A.log_mu, l = cc & mu_mask;
-    const long long pos = (inst << (A.log_mu + LOGE)) + ((long long)vv << A.log_mu) + l;
-    uint32_t v[L];
-    ld_res<L>(v, tw_buf + el * ES + k * L);
-    if (A.scale) {
-      uint32_t ks[L];
+  long long tile = blockIdx.x;
+  if (tile < ntiles && threadIdx.x < 32) issue_pass_tile<MM, L, false>(A, tile, &bar[0], smem, smem + NE * ES);
+  for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
+    const int st = k & 1;
+    uint32_t* buf = smem + st * STAGE;
+    uint32_t* tws = buf + NE * ES;
+    const long long nxt = tile + gridDim.x;
+    if (nxt < ntiles && threadIdx.x < 32)
+      issue_pass_tile<MM, L, false>(A, nxt, &bar[st ^ 1], smem + (st ^ 1) * STAGE, smem + (st ^ 1) * STAGE + NE * ES);
+    mbar_wait(&bar[st], (k >> 1) & 1);
+    uint32_t res[PER][kT][L];
+    int dsl[PER], rot[PER];
 #pragma unroll
-      for (int q = 0; q < L; ++q) ks[q] = mc.kscale[q];
-      mont_mul<L>(v, v, ks, mc);
+    for (int q = 0; q < PER; ++q) {
+      const int it = threadIdx.x + q * NT;
+      dsl[q] = -1;
+      if (it >= NE * TPE) continue;
+      const int el = it / TPE, k0 = (it % TPE) * kT;
+      const int c = el / E, j = el % E;
+      const long long cg = tile * COLS + c;
+      if (cg >= A.total_cols) continue;
+      long long l;
+      col_elem(A, cg, 0, LOGE, 0, &l);
+      const long long s = tw_exp(A, j, l, &rot[q]);
+      if (s == 0) {
+#pragma unroll
+        for (int t = 0; t < kT; ++t) ld_res<L>(res[q][t], buf + el * ES + (k0 + t) * L);
+      } else {
+        twiddle_mul<MM, L, kT>(A, buf + el * ES, tws + el * EST, s, k0, mc, res[q]);
+      }
+      dsl[q] = (c * E + bitrev_n(j, LOGE)) * ES;
     }
-    st_res<L>(A.poly + poly * A.poly_words + pos * (MM * L) + k * L, v);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < PER; ++q)
+      if (dsl[q] >= 0) store_rot<MM, L, kT>(buf + dsl[q], res[q], ((threadIdx.x + q * NT) % TPE) * kT, rot[q], mc);
+    __syncthreads();
+    dft_inplace<MM, L, NE>(buf, LOGE, mc);
+    for (int it = threadIdx.x; it < NE * MM; it += NT) {
+      const int el = it / MM, kk = it % MM;
+      const int c = el / E, vv = el % E;
+      const long long cg = tile * COLS + c;
+      if (cg >= A.total_cols) continue;
+      long long l;
+      const long long off = col_elem(A, cg, vv, LOGE, MM * L, &l);
+      uint32_t v[L];
+      ld_res<L>(v, buf + el * ES + kk * L);
+      if (A.scale) {
+        uint32_t ks[L];
+#pragma unroll
+        for (int q = 0; q < L; ++q) ks[q] = mc.kscale[q];
+        mont_mul<L>(v, v, ks, mc);
+      }
+      st_res<L>(A.poly + off + kk * L, v);
+    }
+    fence_proxy_async();
+    __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------------------
 // bottom of the transform: groups of b = 2^logb contiguous elements.
 //   mode 0: base DFT of `a` only (stage API)
-//   mode 1: base DFT a, base DFT b, pointwise a*b (Montgomery, *R^-1), base DFT -> a
-//   mode 2: like 1 but the pointwise product is exact (extra * R^2 R^-1) -- stage API
+//   mode 1: base DFT a, base DFT b, pointwise b*a (Montgomery, *R^-1), base DFT -> a
 // `scale` multiplies the final outputs by mc.kscale (used when the whole transform is
 // one base DFT, levels == 0).
 struct BottomArgs {
@@ -358,105 +572,139 @@ struct BottomArgs {
 };
 
 template <int MM, int L>
-__global__ void __launch_bounds__(kThreads) k_bottom(BottomArgs A, ModCtx mc) {
-  constexpr int ES = Smem<MM, L>::ES;
-  constexpr int NE = Cfg<MM>::NE;
-  extern __shared__ __align__(16) uint32_t smem[];
-  uint32_t* sa = smem;
-  uint32_t* sb = smem + NE * ES;
-  const long long e0 = (long long)blockIdx.x * NE;  // global element index over the batch
-  const int bmask = (1 << A.logb) - 1;
-  constexpr int V4 = MM * L / 4;
+__device__ __forceinline__ void issue_bottom_tile(const BottomArgs& A, long long tile, uint64_t* bar, uint32_t* sa,
+                                                  uint32_t* sb) {
+  constexpr int ES = Smem<MM, L>::ES, NE = Cfg<MM>::NE;
+  constexpr uint32_t EB = MM * L * 4;
+  const int lane = threadIdx.x & 31;
   const bool two = A.mode != 0;
-  for (int it = threadIdx.x; it < NE * V4; it += kThreads) {
-    const int el = it / V4, w4 = it % V4;
-    const long long ge = e0 + el;
-    if (ge >= A.total_elems) continue;
-    const int slot = (el & ~bmask) | bitrev_n(el & bmask, A.logb);
-    const long long off = ge * (MM * L) + w4 * 4;
-    *reinterpret_cast<uint4*>(sa + slot * ES + w4 * 4) = *reinterpret_cast<const uint4*>(A.a + off);
-    if (two) *reinterpret_cast<uint4*>(sb + slot * ES + w4 * 4) = *reinterpret_cast<const uint4*>(A.b + off);
-  }
-  __syncthreads();
-  dft_inplace<MM, L, NE>(sa, A.logb, mc);
-  if (two) {
-    dft_inplace<MM, L, NE>(sb, A.logb, mc);
-    constexpr int TPE = MM / kT;
-    constexpr int PER = (NE * TPE + kThreads - 1) / kThreads;
-    uint32_t res[PER][kT][L];
-    int dsts[PER];
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int it = threadIdx.x + q * kThreads;
-      dsts[q] = -1;
-      if (it < NE * TPE) {
-        const int el = it / TPE, tg = it % TPE, k0 = tg * kT;
-        const uint32_t* ys = sb + el * ES;
-        ring_mul_rows<MM, L>(sa + el * ES, [&](int j, uint32_t(&y)[L]) { ld_res<L>(y, ys + j * L); }, k0, mc,
-                             res[q]);
-        if (A.mode == 2) {
-          uint32_t r2[L];
-#pragma unroll
-          for (int w = 0; w < L; ++w) r2[w] = mc.r2[w];
-#pragma unroll
-          for (int t = 0; t < kT; ++t) mont_mul<L>(res[q][t], res[q][t], r2, mc);
-        }
-        const int slot = (el & ~bmask) | bitrev_n(el & bmask, A.logb);
-        dsts[q] = slot * ES + k0 * L;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < PER; ++q)
-      if (dsts[q] >= 0) {
-#pragma unroll
-        for (int t = 0; t < kT; ++t) st_res<L>(sa + dsts[q] + t * L, res[q][t]);
-      }
-    __syncthreads();
-    dft_inplace<MM, L, NE>(sa, A.logb, mc);
-  }
-  for (int it = threadIdx.x; it < NE * MM; it += kThreads) {
-    const int el = it / MM, k = it % MM;
+  const long long e0 = tile * NE;
+  const int bmask = (1 << A.logb) - 1;
+  uint32_t bytes = 0;
+  for (int el = lane; el < NE; el += 32)
+    if (e0 + el < A.total_elems) bytes += two ? 2 * EB : EB;
+  bytes = __reduce_add_sync(0xFFFFFFFFu, bytes);
+  if (lane == 0) mbar_expect_tx(bar, bytes);
+  __syncwarp();
+  for (int el = lane; el < NE; el += 32) {
     if (e0 + el >= A.total_elems) continue;
-    uint32_t v[L];
-    ld_res<L>(v, sa + el * ES + k * L);
-    if (A.scale) {
-      uint32_t ks[L];
-#pragma unroll
-      for (int q = 0; q < L; ++q) ks[q] = mc.kscale[q];
-      mont_mul<L>(v, v, ks, mc);
-    }
-    st_res<L>(A.a + (e0 + el) * (MM * L) + k * L, v);
+    const int slot = (el & ~bmask) | bitrev_n(el & bmask, A.logb);
+    bulk_g2s(sa + slot * ES, A.a + (e0 + el) * (MM * L), EB, bar);
+    if (two) bulk_g2s(sb + slot * ES, A.b + (e0 + el) * (MM * L), EB, bar);
   }
 }
 
-// standalone batched ring product (stage API r_mul / pointwise): out = x*y (exact)
 template <int MM, int L>
-__global__ void __launch_bounds__(kThreads) k_rmul(const uint32_t* __restrict__ x, const uint32_t* __restrict__ y,
-                                                   uint32_t* out, long long count, ModCtx mc) {
-  constexpr int ES = Smem<MM, L>::ES;
-  constexpr int NE = Cfg<MM>::NE;
+__global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_bottom(BottomArgs A, ModCtx mc) {
+  constexpr int kT = Cfg<MM>::T;
+  constexpr int ES = Smem<MM, L>::ES, ESW = Smem<MM, L>::ESW;
+  constexpr int NT = Cfg<MM>::NT, NE = Cfg<MM>::NE;
+  constexpr int NS = SmemPlan<MM, L>::BOT_STAGES, STAGE = SmemPlan<MM, L>::STAGE_BOT;
+  constexpr int TPE = MM / kT;
+  constexpr int PER = (NE * TPE + NT - 1) / NT;
+  extern __shared__ __align__(16) uint32_t smem[];
+  __shared__ __align__(8) uint64_t bar[2];
+  uint32_t* wr = smem + NS * STAGE;
+  const long long ntiles = (A.total_elems + NE - 1) / NE;
+  const int bmask = (1 << A.logb) - 1;
+  const bool two = A.mode != 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+  }
+  __syncthreads();
+  long long tile = blockIdx.x;
+  if (tile < ntiles && threadIdx.x < 32) issue_bottom_tile<MM, L>(A, tile, &bar[0], smem, smem + NE * ES);
+  for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
+    const int st = NS == 2 ? (k & 1) : 0;
+    uint32_t* sa = smem + st * STAGE;
+    uint32_t* sb = sa + NE * ES;
+    const long long nxt = tile + gridDim.x;
+    if (NS == 2 && nxt < ntiles && threadIdx.x < 32)
+      issue_bottom_tile<MM, L>(A, nxt, &bar[st ^ 1], smem + (st ^ 1) * STAGE, smem + (st ^ 1) * STAGE + NE * ES);
+    mbar_wait(&bar[st], NS == 2 ? ((k >> 1) & 1) : (k & 1));
+    const long long e0 = tile * NE;
+    dft_inplace<MM, L, NE>(sa, A.logb, mc);
+    if (two) {
+      dft_inplace<MM, L, NE>(sb, A.logb, mc);
+      cta_w_rows<MM, L, NE>(sb, wr, mc);
+      __syncthreads();
+      uint32_t res[PER][kT][L];
+      int dsts[PER];
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int it = threadIdx.x + q * NT;
+        dsts[q] = -1;
+        if (it < NE * TPE) {
+          const int el = it / TPE, k0 = (it % TPE) * kT;
+          ring_mul<MM, L>(ResS<L>{sb + el * ES}, ResS<L>{sa + el * ES}, ResS<L>{wr + el * ESW}, k0, mc, res[q]);
+          const int slot = (el & ~bmask) | bitrev_n(el & bmask, A.logb);
+          dsts[q] = slot * ES + k0 * L;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < PER; ++q)
+        if (dsts[q] >= 0) {
+#pragma unroll
+          for (int t = 0; t < kT; ++t) st_res<L>(sa + dsts[q] + t * L, res[q][t]);
+        }
+      __syncthreads();
+      dft_inplace<MM, L, NE>(sa, A.logb, mc);
+    }
+    for (int it = threadIdx.x; it < NE * MM; it += NT) {
+      const int el = it / MM, kk = it % MM;
+      if (e0 + el >= A.total_elems) continue;
+      uint32_t v[L];
+      ld_res<L>(v, sa + el * ES + kk * L);
+      if (A.scale) {
+        uint32_t ks[L];
+#pragma unroll
+        for (int q = 0; q < L; ++q) ks[q] = mc.kscale[q];
+        mont_mul<L>(v, v, ks, mc);
+      }
+      st_res<L>(A.a + (e0 + el) * (MM * L) + kk * L, v);
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (NS == 1 && nxt < ntiles && threadIdx.x < 32) issue_bottom_tile<MM, L>(A, nxt, &bar[0], smem, smem + NE * ES);
+  }
+}
+
+// standalone batched ring product (stage API r_mul / pointwise): out = y*x (exact)
+template <int MM, int L>
+__global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_rmul(const uint32_t* __restrict__ x,
+                                                                     const uint32_t* __restrict__ y, uint32_t* out,
+                                                                     long long count, ModCtx mc) {
+  constexpr int kT = Cfg<MM>::T;
+  constexpr int ES = Smem<MM, L>::ES, ESW = Smem<MM, L>::ESW;
+  constexpr int NT = Cfg<MM>::NT, NE = Cfg<MM>::NE;
   constexpr int TPE = MM / kT;
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t* sx = smem;
   uint32_t* sy = smem + NE * ES;
+  uint32_t* wr = smem + 2 * NE * ES;
   const long long e0 = (long long)blockIdx.x * NE;
   constexpr int V4 = MM * L / 4;
-  for (int it = threadIdx.x; it < NE * V4; it += kThreads) {
+  for (int it = threadIdx.x; it < NE * V4; it += NT) {
     const int el = it / V4, w4 = it % V4;
+    uint4 vx = make_uint4(0, 0, 0, 0), vy = vx;
     if (e0 + el < count) {
       const long long off = (e0 + el) * (MM * L) + w4 * 4;
-      *reinterpret_cast<uint4*>(sx + el * ES + w4 * 4) = *reinterpret_cast<const uint4*>(x + off);
-      *reinterpret_cast<uint4*>(sy + el * ES + w4 * 4) = *reinterpret_cast<const uint4*>(y + off);
+      vx = *reinterpret_cast<const uint4*>(x + off);
+      vy = *reinterpret_cast<const uint4*>(y + off);
     }
+    *reinterpret_cast<uint4*>(sx + el * ES + w4 * 4) = vx;
+    *reinterpret_cast<uint4*>(sy + el * ES + w4 * 4) = vy;
   }
   __syncthreads();
-  for (int it = threadIdx.x; it < NE * TPE; it += kThreads) {
-    const int el = it / TPE, tg = it % TPE, k0 = tg * kT;
+  cta_w_rows<MM, L, NE>(sy, wr, mc);
+  __syncthreads();
+  for (int it = threadIdx.x; it < NE * TPE; it += NT) {
+    const int el = it / TPE, k0 = (it % TPE) * kT;
     if (e0 + el >= count) continue;
-    const uint32_t* ys = sy + el * ES;
     uint32_t w[kT][L];
-    ring_mul_rows<MM, L>(sx + el * ES, [&](int j, uint32_t(&yy)[L]) { ld_res<L>(yy, ys + j * L); }, k0, mc, w);
+    ring_mul<MM, L>(ResS<L>{sy + el * ES}, ResS<L>{sx + el * ES}, ResS<L>{wr + el * ESW}, k0, mc, w);
     uint32_t r2[L];
 #pragma unroll
     for (int q = 0; q < L; ++q) r2[q] = mc.r2[q];
@@ -465,6 +713,36 @@ __global__ void __launch_bounds__(kThreads) k_rmul(const uint32_t* __restrict__ 
       mont_mul<L>(w[t], w[t], r2, mc);
       st_res<L>(out + (e0 + el) * (MM * L) + (k0 + t) * L, w[t]);
     }
+  }
+}
+
+// twiddle rows [top_mu][2MM][L] from the Montgomery-form table [top_mu][MM][L]:
+// first MM residues = rho~_s, next MM = W_s[k] = -(2^(32L)-1) sum_{i>k} rho~_s[i] mod p
+template <int L>
+__global__ void k_build_twr(const uint32_t* __restrict__ tw, uint32_t* twr, long long top_mu, int MM, ModCtx mc) {
+  const long long total = top_mu * MM;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long s = i / MM;
+    const int k = (int)(i % MM);
+    const uint32_t* row = tw + s * MM * L;
+    uint32_t* dst = twr + s * 2LL * MM * L;
+    uint32_t y[L], acc[L];
+#pragma unroll
+    for (int q = 0; q < L; ++q) {
+      y[q] = row[k * L + q];
+      acc[q] = 0;
+    }
+    st_res<L>(dst + k * L, y);
+    for (int j = k + 1; j < MM; ++j) {
+#pragma unroll
+      for (int q = 0; q < L; ++q) y[q] = row[j * L + q];
+      add_mod<L>(acc, acc, y, mc);
+    }
+    uint32_t c[L];
+#pragma unroll
+    for (int q = 0; q < L; ++q) c[q] = mc.cbias[q];
+    mont_mul<L>(acc, acc, c, mc);
+    st_res<L>(dst + (MM + k) * L, acc);
   }
 }
 

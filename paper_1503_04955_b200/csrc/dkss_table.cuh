@@ -11,9 +11,13 @@ struct KTable {
   void (*bottom)(BottomArgs, ModCtx);
   void (*rmul)(const uint32_t*, const uint32_t*, uint32_t*, long long, ModCtx);
   void (*mscale)(uint32_t*, long long, int, ModCtx);
+  void (*build_twr)(const uint32_t*, uint32_t*, long long, int, ModCtx);
   int ne;     // elements per CTA
   int cols;   // columns per CTA
-  size_t es;  // smem words per element
+  int nt;             // threads per CTA
+  size_t smem_pass;   // dynamic shared memory bytes: column passes
+  size_t smem_bot;    // bottom kernel
+  size_t smem_rmul;   // standalone ring product
 };
 
 template <int MM, int L>
@@ -24,9 +28,13 @@ KTable make_table() {
   t.bottom = k_bottom<MM, L>;
   t.rmul = k_rmul<MM, L>;
   t.mscale = k_mont_scale<L>;
+  t.build_twr = k_build_twr<L>;
   t.ne = Cfg<MM>::NE;
   t.cols = Cfg<MM>::COLS;
-  t.es = Smem<MM, L>::ES;
+  t.nt = Cfg<MM>::NT;
+  t.smem_pass = SmemPlan<MM, L>::PASS * 4;
+  t.smem_bot = SmemPlan<MM, L>::BOT * 4;
+  t.smem_rmul = SmemPlan<MM, L>::RMUL * 4;
   return t;
 }
 
