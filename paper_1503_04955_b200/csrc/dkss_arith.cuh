@@ -9,6 +9,8 @@
 #pragma once
 #include <cstdint>
 
+#include "dkss_carry.cuh"
+
 #ifndef DKSS_MAXL
 #define DKSS_MAXL 6
 #endif
@@ -27,52 +29,17 @@ struct ModCtx {
   uint32_t cbias[DKSS_MAXL];   // -(2^(32L) - 1) * R mod p  (ring_mul bias correction)
 };
 
-// r (L limbs) = (a + b) mod p
+// r = (a + b) mod p and r = (a - b) mod p for canonical a, b (PTX carry chains, dkss_carry.cuh)
 template <int L>
 __device__ __forceinline__ void add_mod(uint32_t (&r)[L], const uint32_t (&a)[L], const uint32_t (&b)[L],
                                         const ModCtx& M) {
-  uint32_t s[L], t[L];
-  uint64_t c = 0;
-#pragma unroll
-  for (int i = 0; i < L; ++i) {
-    c += (uint64_t)a[i] + b[i];
-    s[i] = (uint32_t)c;
-    c >>= 32;
-  }
-  int64_t br = 0;
-#pragma unroll
-  for (int i = 0; i < L; ++i) {
-    int64_t x = (int64_t)s[i] - M.p[i] + br;
-    t[i] = (uint32_t)x;
-    br = x >> 32;
-  }
-  // s + carry*2^(32L) >= p  <=>  carry || no borrow
-  const bool ge = (c != 0) || (br == 0);
-#pragma unroll
-  for (int i = 0; i < L; ++i) r[i] = ge ? t[i] : s[i];
+  Carry<L>::add_mod(r, a, b, M.p);
 }
 
-// r = (a - b) mod p
 template <int L>
 __device__ __forceinline__ void sub_mod(uint32_t (&r)[L], const uint32_t (&a)[L], const uint32_t (&b)[L],
                                         const ModCtx& M) {
-  uint32_t s[L], t[L];
-  int64_t br = 0;
-#pragma unroll
-  for (int i = 0; i < L; ++i) {
-    int64_t x = (int64_t)a[i] - b[i] + br;
-    s[i] = (uint32_t)x;
-    br = x >> 32;
-  }
-  uint64_t c = 0;
-#pragma unroll
-  for (int i = 0; i < L; ++i) {
-    c += (uint64_t)s[i] + M.p[i];
-    t[i] = (uint32_t)c;
-    c >>= 32;
-  }
-#pragma unroll
-  for (int i = 0; i < L; ++i) r[i] = br ? t[i] : s[i];
+  Carry<L>::sub_mod(r, a, b, M.p);
 }
 
 // r = p - a (a in [0, p]; the result p for a == 0 is never produced by callers that need

@@ -36,7 +36,7 @@ template <int MM, int L>
 struct Smem {
   static constexpr int ES = ((MM * L + 31) / 32) * 32 + 4;
   static constexpr int EST = pad_4mod8(2 * MM * L);
-  static constexpr int ESW = pad_4mod8(MM * L);
+  static constexpr int ESW = ES;  // W rows double as the DFT's ping-pong buffer
 };
 
 // CTA shape per inner length m: NT threads, NE elements (COLS columns of 2m) per tile; a
@@ -47,12 +47,12 @@ template <int MM>
 struct Cfg;
 template <>
 struct Cfg<8> {
-  static constexpr int NT = 256, COLS = 4, NE = 64, MINB = 3, T = 2;
+  static constexpr int NT = 256, COLS = 4, NE = 64, MINB = 2, T = 2;
   static constexpr bool TWS = true;
 };
 template <>
 struct Cfg<16> {
-  static constexpr int NT = 256, COLS = 1, NE = 32, MINB = 3, T = 2;
+  static constexpr int NT = 256, COLS = 1, NE = 32, MINB = 2, T = 2;
   static constexpr bool TWS = true;
 };
 template <>
@@ -67,7 +67,7 @@ struct SmemPlan {
   using S = Smem<MM, L>;
   using C = Cfg<MM>;
   static constexpr int STAGE_PASS = C::NE * S::ES + (C::TWS ? C::NE * S::EST : 0);
-  static constexpr int PASS = 2 * STAGE_PASS;
+  static constexpr int PASS = 2 * STAGE_PASS + C::NE * S::ES;  // + DFT ping-pong buffer
   static constexpr int BOT_STAGES = (MM == 32) ? 1 : 2;
   static constexpr int STAGE_BOT = 2 * C::NE * S::ES;
   static constexpr int BOT = BOT_STAGES * STAGE_BOT + C::NE * S::ESW;
@@ -286,58 +286,44 @@ __device__ __forceinline__ void cta_w_rows(const uint32_t* src, uint32_t* dst, c
 }
 
 // ---------------------------------------------------------------------------
-// in-place radix-2 DIT over NE elements in shared memory, split into groups of n
-// (power of two <= 2MM) already in bit-reversed order.  Butterfly root for block size
+// radix-2 DIT over NE elements in shared memory, split into groups of n = 2^logn
+// (<= 2MM) already in bit-reversed order; ping-pongs between `buf` and `alt` (one barrier
+// per stage) and returns the buffer holding the result.  Butterfly root for block size
 // `size`: alpha^(kk * 2MM/size) -- the reference's fft_eval merge with PolyAlphaRing,
 // bigmul/fft.py:87-94 and bigmul/dkss.py:64-91 (any transform length n uses
 // scale*step = 2m/size).  alpha^e is a rotation with negation of wrapped slots
-// (poly_mul_xpow, bigmul/dkss.py:46-61), folded into the add/sub choice.
+// (poly_mul_xpow, bigmul/dkss.py:46-61): a negated slot just swaps the two outputs.
 template <int MM, int L, int NE>
-__device__ __forceinline__ void dft_inplace(uint32_t* buf, int logn, const ModCtx& mc) {
+__device__ __forceinline__ uint32_t* dft_pingpong(uint32_t* buf, uint32_t* alt, int logn, const ModCtx& mc) {
   constexpr int ES = Smem<MM, L>::ES, NT = Cfg<MM>::NT;
   constexpr int ITEMS = (NE / 2) * MM;
-  constexpr int PER = (ITEMS + NT - 1) / NT;
+  uint32_t* src = buf;
+  uint32_t* dst = alt;
   for (int ls = 1; ls <= logn; ++ls) {
     const int half = 1 << (ls - 1);
     const int rootstep = (2 * MM) >> ls;  // 2MM / size
-    uint32_t oa[PER][L], ob[PER][L];
-    int ia[PER], ib[PER];
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int it = threadIdx.x + q * NT;
-      ia[q] = -1;
-      if (it < ITEMS) {
-        const int bf = it / MM, k = it % MM;
-        const int blk = bf >> (ls - 1), kk = bf & (half - 1);
-        const int a = (blk << ls) + kk, b = a + half;
-        const int e = kk * rootstep;  // < MM
-        int src = k - e;
-        const bool neg = src < 0;
-        if (neg) src += MM;
-        uint32_t u[L], x[L];
-        ld_res<L>(u, buf + a * ES + k * L);
-        ld_res<L>(x, buf + b * ES + src * L);
-        uint32_t s[L], d[L];
-        add_mod<L>(s, u, x, mc);
-        sub_mod<L>(d, u, x, mc);
-#pragma unroll
-        for (int w = 0; w < L; ++w) {
-          oa[q][w] = neg ? d[w] : s[w];
-          ob[q][w] = neg ? s[w] : d[w];
-        }
-        ia[q] = a * ES + k * L;
-        ib[q] = b * ES + k * L;
-      }
+    for (int it = threadIdx.x; it < ITEMS; it += NT) {
+      const int bf = it / MM, k = it % MM;
+      const int blk = bf >> (ls - 1), kk = bf & (half - 1);
+      const int a = (blk << ls) + kk, b = a + half;
+      int sk = k - kk * rootstep;  // source coefficient of alpha^e * x_b
+      const bool neg = sk < 0;
+      if (neg) sk += MM;
+      uint32_t u[L], x[L], s[L], d[L];
+      ld_res<L>(u, src + a * ES + k * L);
+      ld_res<L>(x, src + b * ES + sk * L);
+      add_mod<L>(s, u, x, mc);
+      sub_mod<L>(d, u, x, mc);
+      const int oa = a * ES + k * L, ob = b * ES + k * L;
+      st_res<L>(dst + (neg ? ob : oa), s);
+      st_res<L>(dst + (neg ? oa : ob), d);
     }
     __syncthreads();
-#pragma unroll
-    for (int q = 0; q < PER; ++q)
-      if (ia[q] >= 0) {
-        st_res<L>(buf + ia[q], oa[q]);
-        st_res<L>(buf + ib[q], ob[q]);
-      }
-    __syncthreads();
+    uint32_t* tmp = src;
+    src = dst;
+    dst = tmp;
   }
+  return src;
 }
 
 // ---------------------------------------------------------------------------
@@ -453,7 +439,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArg
     if (nxt < ntiles && threadIdx.x < 32)
       issue_pass_tile<MM, L, true>(A, nxt, &bar[st ^ 1], smem + (st ^ 1) * STAGE, smem + (st ^ 1) * STAGE + NE * ES);
     mbar_wait(&bar[st], (k >> 1) & 1);
-    dft_inplace<MM, L, NE>(buf, LOGE, mc);
+    const uint32_t* xv = dft_pingpong<MM, L, NE>(buf, smem + 2 * STAGE, LOGE, mc);
     for (int it = threadIdx.x; it < NE * TPE; it += NT) {
       const int el = it / TPE, k0 = (it % TPE) * kT;
       const int c = el / E, vv = el % E;
@@ -466,9 +452,9 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArg
       uint32_t w[kT][L];
       if (s == 0) {
 #pragma unroll
-        for (int t = 0; t < kT; ++t) ld_res<L>(w[t], buf + el * ES + (k0 + t) * L);
+        for (int t = 0; t < kT; ++t) ld_res<L>(w[t], xv + el * ES + (k0 + t) * L);
       } else {
-        twiddle_mul<MM, L, kT>(A, buf + el * ES, tws + el * EST, s, k0, mc, w);
+        twiddle_mul<MM, L, kT>(A, xv + el * ES, tws + el * EST, s, k0, mc, w);
       }
       store_rot<MM, L, kT>(dst, w, k0, r, mc);
     }
@@ -531,7 +517,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArg
     for (int q = 0; q < PER; ++q)
       if (dsl[q] >= 0) store_rot<MM, L, kT>(buf + dsl[q], res[q], ((threadIdx.x + q * NT) % TPE) * kT, rot[q], mc);
     __syncthreads();
-    dft_inplace<MM, L, NE>(buf, LOGE, mc);
+    const uint32_t* ov = dft_pingpong<MM, L, NE>(buf, smem + 2 * STAGE, LOGE, mc);
     for (int it = threadIdx.x; it < NE * MM; it += NT) {
       const int el = it / MM, kk = it % MM;
       const int c = el / E, vv = el % E;
@@ -540,7 +526,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArg
       long long l;
       const long long off = col_elem(A, cg, vv, LOGE, MM * L, &l);
       uint32_t v[L];
-      ld_res<L>(v, buf + el * ES + kk * L);
+      ld_res<L>(v, ov + el * ES + kk * L);
       if (A.scale) {
         uint32_t ks[L];
 #pragma unroll
@@ -624,10 +610,13 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_bottom(BottomArg
       issue_bottom_tile<MM, L>(A, nxt, &bar[st ^ 1], smem + (st ^ 1) * STAGE, smem + (st ^ 1) * STAGE + NE * ES);
     mbar_wait(&bar[st], NS == 2 ? ((k >> 1) & 1) : (k & 1));
     const long long e0 = tile * NE;
-    dft_inplace<MM, L, NE>(sa, A.logb, mc);
+    // three NE-element buffers {sa, sb, wr} serve as DFT ping-pong space, W rows and results
+    uint32_t* ra = dft_pingpong<MM, L, NE>(sa, wr, A.logb, mc);
+    uint32_t* out = ra;
     if (two) {
-      dft_inplace<MM, L, NE>(sb, A.logb, mc);
-      cta_w_rows<MM, L, NE>(sb, wr, mc);
+      uint32_t* rb = dft_pingpong<MM, L, NE>(sb, ra == sa ? wr : sa, A.logb, mc);
+      uint32_t* wb = (ra != sa && rb != sa) ? sa : (ra != sb && rb != sb) ? sb : wr;
+      cta_w_rows<MM, L, NE>(rb, wb, mc);
       __syncthreads();
       uint32_t res[PER][kT][L];
       int dsts[PER];
@@ -637,7 +626,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_bottom(BottomArg
         dsts[q] = -1;
         if (it < NE * TPE) {
           const int el = it / TPE, k0 = (it % TPE) * kT;
-          ring_mul<MM, L>(ResS<L>{sb + el * ES}, ResS<L>{sa + el * ES}, ResS<L>{wr + el * ESW}, k0, mc, res[q]);
+          ring_mul<MM, L>(ResS<L>{rb + el * ES}, ResS<L>{ra + el * ES}, ResS<L>{wb + el * ES}, k0, mc, res[q]);
           const int slot = (el & ~bmask) | bitrev_n(el & bmask, A.logb);
           dsts[q] = slot * ES + k0 * L;
         }
@@ -647,16 +636,16 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_bottom(BottomArg
       for (int q = 0; q < PER; ++q)
         if (dsts[q] >= 0) {
 #pragma unroll
-          for (int t = 0; t < kT; ++t) st_res<L>(sa + dsts[q] + t * L, res[q][t]);
+          for (int t = 0; t < kT; ++t) st_res<L>(ra + dsts[q] + t * L, res[q][t]);
         }
       __syncthreads();
-      dft_inplace<MM, L, NE>(sa, A.logb, mc);
+      out = dft_pingpong<MM, L, NE>(ra, rb, A.logb, mc);
     }
     for (int it = threadIdx.x; it < NE * MM; it += NT) {
       const int el = it / MM, kk = it % MM;
       if (e0 + el >= A.total_elems) continue;
       uint32_t v[L];
-      ld_res<L>(v, sa + el * ES + kk * L);
+      ld_res<L>(v, out + el * ES + kk * L);
       if (A.scale) {
         uint32_t ks[L];
 #pragma unroll
