@@ -1,0 +1,213 @@
+"""GPU parity: every stage and every product of the CUDA path (called through the C ABI)
+against the reference's golden vectors, the CPU oracle, and Python's int product.
+Bit-exact (integer path)."""
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+from oracle.oracle import OraclePlan
+from paper_1503_04955_b200 import Natural, dmul, dmul_many, mul
+from paper_1503_04955_b200 import plan as P
+from paper_1503_04955_b200.dkss import (device_plan, dkss_decode, dkss_encode, dkss_fft, r_mul, dkss_fft_limbs,
+                                        r_mul_limbs)
+from paper_1503_04955_b200.words import int_to_u32, u32_to_int, using_word_bits
+
+pytestmark = pytest.mark.gpu
+
+
+def _stages(golden_dir):
+    with open(os.path.join(golden_dir, "stages_index.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("idx", range(7))
+def test_stages_equal_reference(cuda_ok, golden_dir, idx):
+    r = _stages(golden_dir)[idx]
+    g = np.load(os.path.join(golden_dir, f"stages_{r['tag']}.npz"))
+    with using_word_bits(r["w"]):
+        pl = P.dkss_select_params(r["N"], r["w"])
+    dp = device_plan(pl)
+    a, b = u32_to_int(g["a"]), u32_to_int(g["b"])
+    assert np.array_equal(dp.encode(int_to_u32(a, dp.info["operand_limbs"])), g["enc_a"])
+    assert np.array_equal(dp.fft(g["enc_a"]), g["fft_a"])
+    assert np.array_equal(dp.fft(np.stack([g["enc_a"], g["enc_b"]])), np.stack([g["fft_a"], g["fft_b"]]))
+    assert np.array_equal(dp.rmul(g["fft_a"], g["fft_b"]), g["pointwise"])
+    assert np.array_equal(dp.fft(g["pointwise"]), g["fft_c"])
+    assert np.array_equal(dp.decode(g["fft_c"], g["product"].size), g["product"])
+    prod = dp.mul_limbs(int_to_u32(a, dp.info["operand_limbs"]), int_to_u32(b, dp.info["operand_limbs"]),
+                        dp.info["product_limbs"])
+    assert np.array_equal(prod[: g["product"].size], g["product"])
+
+
+@pytest.mark.parametrize("tag", ["m16", "m32"])
+def test_rmul_equal_reference(cuda_ok, golden_dir, tag):
+    g = np.load(os.path.join(golden_dir, f"rmul_{tag}.npz"))
+    m = g["x"].shape[1]
+    pl = P.make_plan(1 << 16 if m == 16 else 1 << 24, m, m, u32_to_int(g["p"]), check_bounds=False)
+    assert np.array_equal(r_mul_limbs(g["x"], g["y"], pl), g["z"])
+
+
+def test_reference_list_api(cuda_ok, rng):
+    # the reference-shaped stage functions (lists of ints in and out)
+    pl = P.dkss_select_params(1 << 12)
+    a = rng.getrandbits(4000)
+    poly = dkss_encode(a, pl)
+    assert len(poly) == 2 * pl.M and all(len(c) == pl.m for c in poly)
+    o = OraclePlan(pl)
+    want = o.fft(o.encode(a))
+    dkss_fft(poly, pl)
+    assert poly == [[int.from_bytes(c.tobytes(), "little") for c in row] for row in want]
+    x, y = poly[3], poly[7]
+    z = r_mul(x, y, pl)
+    assert z == P.poly_mul_mod(x, y, pl.m, pl.p)   # schoolbook oracle, tests/test_dkss.py:111-119
+    # pipeline x enc(1) is the identity (tests/test_dkss.py:247-260)
+    one = dkss_encode(1, pl)
+    dkss_fft(one, pl)
+    prod = [r_mul(u, v, pl) for u, v in zip(poly, one)]
+    dkss_fft(prod, pl)
+    assert dkss_decode(prod, pl).to_int() == a
+
+
+@pytest.mark.parametrize("e", [10, 12, 14, 16, 18, 20])
+def test_dmul_powers_of_two(cuda_ok, e):
+    rng = random.Random(e)
+    N = 1 << e
+    a = rng.getrandbits(N) | 1 << (N - 1)
+    b = rng.getrandbits(N) | 1 << (N - 1)
+    assert dmul(a, b) == a * b
+
+
+def test_dmul_adversarial_all_ones(cuda_ok):
+    # config 2b: (2^N - 1)^2, longest carry chains (BASELINE.json configs[1])
+    for N in (1 << 16, 1 << 20):
+        a = (1 << N) - 1
+        assert dmul(a, a) == a * a
+
+
+def test_dmul_matches_oracle_2_20(cuda_ok):
+    rng = random.Random(2)
+    N = 1 << 20
+    a = rng.getrandbits(N) | 1 << (N - 1)
+    b = rng.getrandbits(N) | 1 << (N - 1)
+    o = OraclePlan(P.dkss_select_params(N))
+    assert dmul(a, b).to_int() == o.dmul(a, b) == a * b
+
+
+def test_dmul_odd_sizes_and_unbalanced(cuda_ok, rng):
+    for bits in (1, 31, 1000, 1023, 2049, 3648 * 64 - 5, 99_999):
+        a = rng.getrandbits(bits) | 1 << (bits - 1)
+        b = rng.getrandbits(max(1, bits // 3) + 1)
+        assert dmul(a, b) == a * b
+    a = rng.getrandbits(2000 * 64)          # tests/test_dkss.py:284-287
+    b = rng.getrandbits(37 * 64)
+    assert dmul(Natural.from_int(a), Natural.from_int(b)).to_int() == a * b
+
+
+def test_dmul_result_length_and_word_sizes(cuda_ok, rng):
+    a = Natural.from_int(rng.getrandbits(640), length=12)
+    b = Natural.from_int(rng.getrandbits(640), length=10)
+    r = dmul(a, b)
+    assert len(r) == 22 and r.to_int() == a.to_int() * b.to_int()
+    for w, words in ((8, 900), (32, 700)):    # tests/test_dkss.py:292-300
+        with using_word_bits(w):
+            bits = words * w
+            x = rng.getrandbits(bits) | 1 << (bits - 1)
+            y = rng.getrandbits(bits) | 1 << (bits - 1)
+            assert dmul(Natural.from_int(x, length=words), Natural.from_int(y, length=words)).to_int() == x * y
+
+
+def test_mul_routes_dmul(cuda_ok, rng):
+    a, b = rng.getrandbits(600 * 64), rng.getrandbits(600 * 64)
+    assert mul(a, b, algorithm="dmul") == a * b
+    from paper_1503_04955_b200 import ThresholdTable
+
+    # tests/test_bench.py:24-30: 600-word inputs routed to dmul by the table
+    assert mul(a, b, thresholds=ThresholdTable(kmul=4, t3mul=16, smul=128, dmul=512)) == a * b
+
+
+def test_plan_info_op_counts(cuda_ok):
+    # ring products per multiply == the reference's ks_calls (bigmul/dkss.py:412)
+    for e, (rf, tot) in {16: (465, 1907), 20: (14849, 52739)}.items():
+        dp = device_plan(P.dkss_select_params(1 << e))
+        assert dp.info["twiddles_per_fft"] == rf and dp.info["ring_products"] == tot
+
+
+def test_batched_products(cuda_ok):
+    # config 3 shape (smaller batch): pair i from Random(seed0 + i)
+    pairs = []
+    for i in range(64):
+        r = random.Random(3 + i)
+        N = 1 << 18
+        pairs.append((r.getrandbits(N) | 1 << (N - 1), r.getrandbits(N) | 1 << (N - 1)))
+    got = dmul_many(pairs)
+    assert got == [a * b for a, b in pairs]
+
+
+def test_device_api_graph_replay(cuda_ok):
+    import torch
+
+    N = 1 << 18
+    pl = P.dkss_select_params(N)
+    dp = device_plan(pl)
+    nl, npl = dp.info["operand_limbs"], dp.info["product_limbs"]
+    rng = random.Random(9)
+    pairs = [(rng.getrandbits(N), rng.getrandbits(N)) for _ in range(4)]
+    A = torch.from_numpy(np.stack([int_to_u32(a, nl) for a, _ in pairs]).view(np.int32)).cuda()
+    B = torch.from_numpy(np.stack([int_to_u32(b, nl) for _, b in pairs]).view(np.int32)).cuda()
+    C = torch.zeros((4, npl), dtype=torch.int32, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    for rep in range(3):   # first call captures the CUDA graph, later calls replay it
+        C.zero_()
+        dp.mul_device(4, A.data_ptr(), B.data_ptr(), nl, C.data_ptr(), npl, s)
+        torch.cuda.synchronize()
+        out = C.cpu().numpy().view(np.uint32)
+        assert [u32_to_int(row) for row in out] == [a * b for a, b in pairs]
+    prof = dp.profile_device(4, A.data_ptr(), B.data_ptr(), nl, C.data_ptr(), s)
+    kinds = [k for k, *_ in prof]
+    assert kinds.count("fwd_pass") == pl.levels and kinds.count("inv_pass") == pl.levels
+    assert all(ms > 0 for _, ms, _, _ in prof)
+
+
+def test_errors_are_reported(cuda_ok):
+    pl = P.dkss_select_params(1 << 12)
+    dp = device_plan(pl)
+    with pytest.raises(ValueError):
+        dp.encode(int_to_u32(1 << 5000, 200))      # operand >= 2^N (bigmul/dkss.py:389-390)
+    with pytest.raises(ValueError):
+        dp.mul_limbs(int_to_u32((1 << 4096) - 1, 128), int_to_u32((1 << 4096) - 1, 128), 10)  # nc too small
+
+
+@pytest.mark.slow
+def test_dmul_2_24(cuda_ok):
+    rng = random.Random(4)
+    N = 1 << 24
+    a = rng.getrandbits(N) | 1 << (N - 1)
+    b = rng.getrandbits(N) | 1 << (N - 1)
+    c = dmul(a, b).to_int()
+    # residue check (cheap) plus the full product
+    for q in (2**61 - 1, 2**62 - 57, 2**59 - 55):
+        assert c % q == (a % q) * (b % q) % q
+    assert c == a * b
+
+
+def test_dmul_2_26_residues(cuda_ok):
+    # config 5: checked by residues modulo 64 seeded random 62-bit primes (BASELINE.json configs[4])
+    from paper_1503_04955_b200.numtheory import lucas_prime_test, factor_smooth
+
+    rng = random.Random(5)
+    N = 1 << 26
+    a = rng.getrandbits(N) | 1 << (N - 1)
+    b = rng.getrandbits(N) | 1 << (N - 1)
+    c = dmul(a, b).to_int()
+    assert c.bit_length() in (2 * N - 1, 2 * N)
+    pr = random.Random(12345)
+    primes = []
+    while len(primes) < 64:
+        q = pr.getrandbits(62) | 1 << 61 | 1
+        if all(pow(w, q - 1, q) == 1 for w in (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37)):
+            primes.append(q)
+    for q in primes:
+        assert c % q == (a % q) * (b % q) % q

@@ -144,11 +144,33 @@ def ref_test_vectors():
     out["paper_3648"] = [pl.M, pl.m, pl.iclen, pl.u]
     M, m, u, p, g = R.select_geometry(42991616 * 64, w=64)
     out["paper_42991616"] = [M, m, u, str(p), g]
+    # dkss_fft / r_mul on the toy plans the reference tests use (tests/test_dkss.py:185-202, :111-119)
+    rng = random.Random(0xC0FFEE)
+    toy = []
+    for M, m, p in [(2, 2, 17), (4, 2, 17), (8, 2, 17), (8, 4, 97), (16, 4, 97)]:
+        plan = R.make_plan(0, M, m, p, check_bounds=False)
+        vals = [[rng.randrange(p) for _ in range(m)] for _ in range(2 * M)]
+        work = [list(v) for v in vals]
+        R.dkss_fft(work, plan, FAST)
+        xs = [[rng.randrange(p) for _ in range(m)] for _ in range(8)]
+        ys = [[rng.randrange(p) for _ in range(m)] for _ in range(8)]
+        zs = [R.r_mul(x, y, plan, FAST) for x, y in zip(xs, ys)]
+        toy.append(dict(M=M, m=m, p=p, rho_powers=plan.rho_powers, fft_in=vals, fft_out=work, x=xs, y=ys, z=zs))
+    out["toy_plans"] = toy
     return out
+
+
+def proth_digest():
+    """sha256 of the reference prime table's (bits, h, g) records (bigmul/data/proth_primes.txt)."""
+    rows = R.proth_table()
+    text = "\n".join(f"{bits} {h} {g}" for bits, (p, h, g) in sorted(rows.items()))
+    return {"rows": len(rows), "sha256": hashlib.sha256(text.encode()).hexdigest()}
 
 
 def main():
     os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, "proth_digest.json"), "w") as f:
+        json.dump(proth_digest(), f)
     t0 = time.time()
     plans = []
     for w in (64, 32, 8):
