@@ -168,7 +168,7 @@ int ensure_ws(dkss_plan* P, int batch) {
   if (batch <= P->cap_batch) return 0;
   free_ws(P);
   const size_t poly_b = (size_t)P->poly_words * 4;
-  const size_t nwarps = (size_t)dec_blocks(P) * 32;
+  const size_t nwarps = (size_t)dec_blocks(P) * kDecWarps;
   CUCHK(cudaMalloc(&P->d_poly, 2 * (size_t)batch * poly_b));
   CUCHK(cudaMalloc(&P->d_ops, 2 * (size_t)batch * P->op_limbs * 4));
   CUCHK(cudaMalloc(&P->d_prod, (size_t)batch * P->prod_limbs * 4));
@@ -222,7 +222,8 @@ int launch_encode(dkss_plan* P, const uint32_t* ops, long long na, uint32_t* pol
   return 0;
 }
 
-int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s) {
+int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s, const uint32_t* ops_a = nullptr,
+                      const uint32_t* ops_b = nullptr, long long na = 0, int enc_split = 0) {
   const long long cols = (long long)npoly << P->log_top_mu;
   const int grid = (int)std::min<long long>((cols + P->kt.cols - 1) / P->kt.cols, P->grid_pass);
   for (int lv = 0; lv < P->levels; ++lv) {
@@ -236,6 +237,14 @@ int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s) {
     A.twr = P->d_twr;
     A.scale = 0;
     A.total_cols = cols;
+    if (lv == 0 && ops_a) {
+      A.ops_a = ops_a;
+      A.ops_b = ops_b;
+      A.na = na;
+      A.enc_split = enc_split;
+      A.u = P->u;
+      A.M = P->M;
+    }
     P->kt.fwd<<<grid, P->kt.nt, smem_pass(P), s>>>(A, P->mc);
     CUCHK(cudaGetLastError());
     mark(P, s, DKSS_K_FWD_PASS, rp_work(P, npoly * level_twiddles(P, lv)), 2LL * npoly * P->poly_words * 4);
@@ -312,9 +321,13 @@ int run_mul(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, long 
   uint32_t* pa = P->d_poly;
   uint32_t* pb = P->d_poly + (size_t)batch * P->poly_words;
   int rc;
-  if ((rc = launch_encode(P, a, nl, pa, batch, s))) return rc;
-  if ((rc = launch_encode(P, b, nl, pb, batch, s))) return rc;
-  if ((rc = launch_fwd_levels(P, P->d_poly, 2 * batch, s))) return rc;
+  if (P->levels > 0) {
+    // encode fused into the first forward pass
+    if ((rc = launch_fwd_levels(P, P->d_poly, 2 * batch, s, a, b, nl, batch))) return rc;
+  } else {
+    if ((rc = launch_encode(P, a, nl, pa, batch, s))) return rc;
+    if ((rc = launch_encode(P, b, nl, pb, batch, s))) return rc;
+  }
   if ((rc = launch_bottom(P, pa, pb, batch, 1, P->levels == 0, s))) return rc;
   if ((rc = launch_inv_levels(P, pa, batch, true, s))) return rc;
   if ((rc = launch_decode(P, pa, prod, batch, s))) return rc;
@@ -493,7 +506,7 @@ int dkss_plan_get_info(const dkss_plan* P, dkss_plan_info* o) {
   o->product_limbs = P->prod_limbs;
   o->twiddles_per_fft = P->twiddles;
   o->ring_products = 3 * P->twiddles + 2LL * P->M;
-  o->launches_per_mul = 2 + P->levels + 1 + P->levels + 2;
+  o->launches_per_mul = (P->levels > 0 ? 0 : 2) + P->levels + 1 + P->levels + 2;
   o->workspace_bytes = (int64_t)P->ws_bytes;
   return DKSS_OK;
 }

@@ -336,6 +336,14 @@ struct PassArgs {
   const uint32_t* twr;   // [M/m][2MM][L]: rho~_s = rho^s R mod p, then W_s (see ring_mul)
   int scale;             // inverse pass: multiply outputs by mc.kscale
   long long total_cols;  // columns in the launch (npoly * M/m)
+  // fused encode (first forward level): elements are sliced from the operands instead of
+  // loaded -- poly q < enc_split takes operand q of ops_a, others operand q-enc_split of ops_b
+  const uint32_t* ops_a;
+  const uint32_t* ops_b;
+  long long na;          // limbs per operand
+  int enc_split;
+  int u;                 // bits per inner coefficient
+  int M;                 // outer length (elements e >= M are zero)
 };
 
 template <int MM>
@@ -364,7 +372,7 @@ __device__ __forceinline__ long long tw_exp(const PassArgs& A, int j, long long 
 // staged, the twiddle row of every element needing a ring product
 template <int MM, int L, bool FWD>
 __device__ __forceinline__ void issue_pass_tile(const PassArgs& A, long long tile, uint64_t* bar, uint32_t* buf,
-                                                uint32_t* tws) {
+                                                uint32_t* tws, bool load_elems = true) {
   constexpr int ES = Smem<MM, L>::ES, EST = Smem<MM, L>::EST;
   constexpr int NE = Cfg<MM>::NE, COLS = Cfg<MM>::COLS, E = 2 * MM, LOGE = Geo<MM>::LOGE;
   constexpr uint32_t EB = MM * L * 4, TB = 2 * MM * L * 4;
@@ -373,7 +381,7 @@ __device__ __forceinline__ void issue_pass_tile(const PassArgs& A, long long til
   for (int e = lane; e < NE; e += 32) {
     const long long cg = tile * COLS + e / E;
     if (cg >= A.total_cols) continue;
-    bytes += EB;
+    if (load_elems) bytes += EB;
     if constexpr (Cfg<MM>::TWS) {
       long long l;
       col_elem(A, cg, 0, LOGE, 0, &l);
@@ -391,7 +399,7 @@ __device__ __forceinline__ void issue_pass_tile(const PassArgs& A, long long til
     long long l;
     const long long off = col_elem(A, cg, j, LOGE, MM * L, &l);
     const int slot = FWD ? c * E + bitrev_n(j, LOGE) : e;
-    bulk_g2s(buf + slot * ES, A.poly + off, EB, bar);
+    if (load_elems) bulk_g2s(buf + slot * ES, A.poly + off, EB, bar);
     if constexpr (Cfg<MM>::TWS) {
       int r;
       const long long s = tw_exp(A, j, l, &r);
@@ -409,6 +417,45 @@ __device__ __forceinline__ void twiddle_mul(const PassArgs& A, const uint32_t* x
   } else {
     const uint32_t* row = A.twr + s * (2 * MM * L);
     ring_mul<MM, L>(ResG<L>{row}, ResS<L>{xs}, ResG<L>{row + MM * L}, k0, mc, w);
+  }
+}
+
+// fused dkss_encode (bigmul/dkss.py:381-398) for the first forward level: coefficient k of
+// element pos is bits [u(pos*m/2 + k), +u) of the operand for pos < M, k < m/2, else 0;
+// written straight into the column buffer at the bit-reversed slot
+template <int MM, int L>
+__device__ __forceinline__ void cta_encode_tile(const PassArgs& A, long long tile, uint32_t* buf) {
+  constexpr int ES = Smem<MM, L>::ES, NT = Cfg<MM>::NT, NE = Cfg<MM>::NE, COLS = Cfg<MM>::COLS;
+  constexpr int E = 2 * MM, LOGE = Geo<MM>::LOGE, HALF = MM / 2;
+  for (int it = threadIdx.x; it < NE * MM; it += NT) {
+    const int el = it / MM, k = it % MM;
+    const int c = el / E, j = el % E;
+    const long long cg = tile * COLS + c;
+    uint32_t out[L];
+#pragma unroll
+    for (int q = 0; q < L; ++q) out[q] = 0;
+    if (cg < A.total_cols && k < HALF) {
+      const long long q = cg >> A.log_top_mu, cc = cg & ((1LL << A.log_top_mu) - 1);
+      const long long inst = cc >> A.log_mu, l = cc & ((1LL << A.log_mu) - 1);
+      const long long pos = (inst << (A.log_mu + LOGE)) + ((long long)j << A.log_mu) + l;
+      if (pos < A.M) {
+        const uint32_t* op = q < A.enc_split ? A.ops_a + q * A.na : A.ops_b + (q - A.enc_split) * A.na;
+        const long long bit = (long long)A.u * (pos * HALF + k);
+        const long long w0 = bit >> 5;
+        const int sh = (int)(bit & 31);
+        uint32_t src[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) src[w] = (w0 + w < A.na) ? __ldg(op + w0 + w) : 0u;
+        int rem = A.u;
+#pragma unroll
+        for (int w = 0; w < 3 && w < L; ++w) {
+          const uint32_t v = sh ? __funnelshift_r(src[w], src[w + 1], sh) : src[w];
+          out[w] = rem >= 32 ? v : (rem > 0 ? v & ((1u << rem) - 1u) : 0u);
+          rem -= 32;
+        }
+      }
+    }
+    st_res<L>(buf + (c * E + bitrev_n(j, LOGE)) * ES + k * L, out);
   }
 }
 
@@ -430,14 +477,20 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArg
   }
   __syncthreads();
   long long tile = blockIdx.x;
-  if (tile < ntiles && threadIdx.x < 32) issue_pass_tile<MM, L, true>(A, tile, &bar[0], smem, smem + NE * ES);
+  const bool enc = A.ops_a != nullptr;
+  if (tile < ntiles && threadIdx.x < 32) issue_pass_tile<MM, L, true>(A, tile, &bar[0], smem, smem + NE * ES, !enc);
   for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
     const int st = k & 1;
     uint32_t* buf = smem + st * STAGE;
     uint32_t* tws = buf + NE * ES;
     const long long nxt = tile + gridDim.x;
     if (nxt < ntiles && threadIdx.x < 32)
-      issue_pass_tile<MM, L, true>(A, nxt, &bar[st ^ 1], smem + (st ^ 1) * STAGE, smem + (st ^ 1) * STAGE + NE * ES);
+      issue_pass_tile<MM, L, true>(A, nxt, &bar[st ^ 1], smem + (st ^ 1) * STAGE, smem + (st ^ 1) * STAGE + NE * ES,
+                                   !enc);
+    if (enc) {
+      cta_encode_tile<MM, L>(A, tile, buf);
+      __syncthreads();
+    }
     mbar_wait(&bar[st], (k >> 1) & 1);
     const uint32_t* xv = dft_pingpong<MM, L, NE>(buf, smem + 2 * STAGE, LOGE, mc);
     for (int it = threadIdx.x; it < NE * TPE; it += NT) {
@@ -837,7 +890,8 @@ __global__ void k_permute(const uint32_t* in, uint32_t* out, long long elems, in
 // coefficient overlapping [32t, 32t+32); then w_t = lo32(S_t) + hi(S_{t-1}) < 2^32 + 2^6,
 // so every limb's carry-out is 0/1.  Warp and block (generate, propagate) masks are
 // resolved with the add-trick: carries = ((G|P) + G + cin) ^ (G|P) ^ G.
-constexpr int kDecThreads = 1024;
+constexpr int kDecThreads = 256;
+constexpr int kDecWarps = kDecThreads / 32;
 
 struct DecodeArgs {
   const uint32_t* v;   // natural-order coefficients, npoly polys
@@ -889,7 +943,7 @@ __global__ void __launch_bounds__(kDecThreads) k_decode1(DecodeArgs A) {
   const long long t = (long long)blk * kDecThreads + threadIdx.x;
   const uint32_t* v = A.v + (long long)pidx * A.poly_words;
   __shared__ unsigned long long sS[kDecThreads + 1];
-  __shared__ uint32_t wg[32], wp[32];
+  __shared__ uint32_t wg[kDecWarps], wp[kDecWarps];
   unsigned long long S = t < A.nout ? window_sum(A, v, t) : 0ull;
   sS[threadIdx.x + 1] = S;
   if (threadIdx.x == 0) sS[0] = (t < A.nout && t > 0) ? window_sum(A, v, t - 1) : 0ull;
@@ -902,7 +956,7 @@ __global__ void __launch_bounds__(kDecThreads) k_decode1(DecodeArgs A) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (t < A.nout) A.out[(long long)pidx * A.nout + t] = (uint32_t)w;
   if (lane == 0) {
-    const long long wi = ((long long)pidx * A.blocks_per_poly + blk) * 32 + warp;
+    const long long wi = ((long long)pidx * A.blocks_per_poly + blk) * kDecWarps + warp;
     A.gmask[wi] = G;
     A.pmask[wi] = P;
     // warp carry-out for cin = 0 / 1
@@ -912,11 +966,11 @@ __global__ void __launch_bounds__(kDecThreads) k_decode1(DecodeArgs A) {
   }
   __syncthreads();
   if (warp == 0) {
-    const bool c0 = wg[lane], c1 = wp[lane];
+    const bool c0 = lane < kDecWarps && wg[lane], c1 = lane < kDecWarps && wp[lane];
     const unsigned WG = __ballot_sync(0xFFFFFFFFu, c0), WP = __ballot_sync(0xFFFFFFFFu, c1 && !c0);
     if (lane == 0) {
       const unsigned long long a = (unsigned long long)(WG | WP), b = WG;
-      const unsigned co0 = (unsigned)((a + b) >> 32), co1 = (unsigned)((a + b + 1) >> 32);
+      const unsigned co0 = (unsigned)((a + b) >> kDecWarps) & 1u, co1 = (unsigned)((a + b + 1) >> kDecWarps) & 1u;
       A.bstat[(long long)pidx * A.blocks_per_poly + blk] = co0 | (co1 << 1);
     }
   }
@@ -928,7 +982,7 @@ __global__ void __launch_bounds__(kDecThreads) k_decode2(DecodeArgs A) {
   const long long t = (long long)blk * kDecThreads + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ unsigned s_cin_block;
-  __shared__ unsigned s_wcin[32];
+  __shared__ unsigned s_wcin[kDecWarps];
   if (warp == 0) {
     // carry into this block: scan the statuses of blocks 0..blk-1 of this poly
     unsigned cin = 0;
@@ -945,19 +999,19 @@ __global__ void __launch_bounds__(kDecThreads) k_decode2(DecodeArgs A) {
       cin = (unsigned)((sum >> n) & 1ull);
     }
     // carries into each warp of this block
-    const long long wi = ((long long)pidx * A.blocks_per_poly + blk) * 32 + lane;
-    const unsigned G = A.gmask[wi], P = A.pmask[wi];
+    const long long wi = ((long long)pidx * A.blocks_per_poly + blk) * kDecWarps + lane;
+    const unsigned G = lane < kDecWarps ? A.gmask[wi] : 0u, P = lane < kDecWarps ? A.pmask[wi] : 0u;
     const unsigned long long a = (unsigned long long)(G | P), b = G;
     const bool c0 = (unsigned)((a + b) >> 32), c1 = (unsigned)((a + b + 1) >> 32);
     const unsigned WG = __ballot_sync(0xFFFFFFFFu, c0), WP = __ballot_sync(0xFFFFFFFFu, c1 && !c0);
     const unsigned long long wa = (unsigned long long)(WG | WP), wb = WG;
     const unsigned long long carries = (wa + wb + cin) ^ wa ^ wb;  // bit i = carry into warp i
-    s_wcin[lane] = (unsigned)((carries >> lane) & 1ull);
+    if (lane < kDecWarps) s_wcin[lane] = (unsigned)((carries >> lane) & 1ull);
     if (lane == 0) s_cin_block = cin;
   }
   __syncthreads();
   if (t >= A.nout) return;
-  const long long wi = ((long long)pidx * A.blocks_per_poly + blk) * 32 + warp;
+  const long long wi = ((long long)pidx * A.blocks_per_poly + blk) * kDecWarps + warp;
   const unsigned G = A.gmask[wi], P = A.pmask[wi];
   const unsigned long long a = (unsigned long long)(G | P), b = G;
   const unsigned long long carries = (a + b + s_wcin[warp]) ^ a ^ b;
