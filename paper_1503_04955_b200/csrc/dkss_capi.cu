@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -123,6 +124,7 @@ struct dkss_plan {
   uint32_t* d_tw = nullptr;   // Montgomery-form rho table [M/m][m][L]
   uint32_t* d_twr = nullptr;  // twiddle rows [M/m][2m][L]: Montgomery-form rho^s, then W_s
   int grid_pass = 0, grid_bot = 0;  // persistent grid sizes (SMs x resident CTAs)
+  int grid_fw = 0, grid_iw = 0;     // warp-per-column kernels (0 = not used)
   // workspace
   int cap_batch = 0;
   uint32_t* d_poly = nullptr;  // 2 * cap_batch polynomials
@@ -237,6 +239,7 @@ int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s, c
     A.twr = P->d_twr;
     A.scale = 0;
     A.total_cols = cols;
+    A.wpc = 1;
     if (lv == 0 && ops_a) {
       A.ops_a = ops_a;
       A.ops_b = ops_b;
@@ -245,7 +248,18 @@ int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s, c
       A.u = P->u;
       A.M = P->M;
     }
-    P->kt.fwd<<<grid, P->kt.nt, smem_pass(P), s>>>(A, P->mc);
+    if (P->grid_fw && cols >= 4LL * P->grid_fw * kWarpsPerCta) {
+      // warp-per-column only when every resident warp gets several columns (large batches);
+      // small transforms keep the CTA-wide kernel, which spreads a column over 8 warps
+      const long long wres = (long long)P->grid_fw * kWarpsPerCta;
+      int wpc = 1;
+      while (wpc < 8 && cols * wpc * 2 <= wres) wpc *= 2;
+      A.wpc = wpc;
+      const int gw = (int)std::min<long long>(P->grid_fw, (cols * wpc + kWarpsPerCta - 1) / kWarpsPerCta);
+      P->kt.fwd_w<<<gw, kWarpsPerCta * 32, P->kt.smem_fwd_w, s>>>(A, P->mc);
+    } else {
+      P->kt.fwd<<<grid, P->kt.nt, smem_pass(P), s>>>(A, P->mc);
+    }
     CUCHK(cudaGetLastError());
     mark(P, s, DKSS_K_FWD_PASS, rp_work(P, npoly * level_twiddles(P, lv)), 2LL * npoly * P->poly_words * 4);
   }
@@ -265,7 +279,13 @@ int launch_inv_levels(dkss_plan* P, uint32_t* poly, int npoly, bool scale_last, 
     A.twr = P->d_twr;
     A.scale = (lv == 0 && scale_last) ? 1 : 0;
     A.total_cols = cols;
-    P->kt.inv<<<grid, P->kt.nt, smem_pass(P), s>>>(A, P->mc);
+    if (P->grid_iw && cols >= 4LL * P->grid_iw * kWarpsPerCta) {
+      A.wpc = 1;
+      const int gw = (int)std::min<long long>(P->grid_iw, (cols + kWarpsPerCta - 1) / kWarpsPerCta);
+      P->kt.inv_w<<<gw, kWarpsPerCta * 32, P->kt.smem_inv_w, s>>>(A, P->mc);
+    } else {
+      P->kt.inv<<<grid, P->kt.nt, smem_pass(P), s>>>(A, P->mc);
+    }
     CUCHK(cudaGetLastError());
     mark(P, s, DKSS_K_INV_PASS, rp_work(P, npoly * level_twiddles(P, lv)), 2LL * npoly * P->poly_words * 4);
   }
@@ -438,6 +458,18 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
     }
     P->grid_pass = sms * std::min(occ_f, occ_i);
     P->grid_bot = sms * occ_b;
+    const char* nowarp = getenv("DKSS_NO_WARP_PASS");
+    if (kt.fwd_w && !(nowarp && *nowarp == '1')) {
+      int ofw = 0, oiw = 0;
+      CUCHK(cudaFuncSetAttribute((const void*)kt.fwd_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kt.smem_fwd_w));
+      CUCHK(cudaFuncSetAttribute((const void*)kt.inv_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kt.smem_inv_w));
+      CUCHK(cudaFuncSetAttribute((const void*)kt.fwd_w, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      CUCHK(cudaFuncSetAttribute((const void*)kt.inv_w, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      CUCHK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ofw, kt.fwd_w, kWarpsPerCta * 32, kt.smem_fwd_w));
+      CUCHK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oiw, kt.inv_w, kWarpsPerCta * 32, kt.smem_inv_w));
+      P->grid_fw = ofw > 0 ? sms * ofw : 0;
+      P->grid_iw = oiw > 0 ? sms * oiw : 0;
+    }
   }
   // cbias = -(2^(32L) - 1) * R mod p = (p - ((R mod p) - 1)) * R mod p  (ring_mul bias correction)
   {
@@ -511,16 +543,14 @@ int dkss_plan_get_info(const dkss_plan* P, dkss_plan_info* o) {
   return DKSS_OK;
 }
 
-int dkss_mul_device(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, size_t nl, uint32_t* c, size_t nc,
-                    void* stream) {
-  if (!P || batch < 1 || !a || !b || !c) return fail(DKSS_EINVAL, "bad argument");
-  if ((long long)nl > P->op_limbs) return fail(DKSS_ERANGE, "operand limbs %zu exceed plan (%lld)", nl, P->op_limbs);
-  if ((long long)nc < P->prod_limbs) return fail(DKSS_EINVAL, "nc=%zu below product limbs %lld", nc, P->prod_limbs);
-  std::lock_guard<std::mutex> lk(P->mu);
-  CUCHK(cudaSetDevice(P->device));
+}  // extern "C"
+
+namespace {
+// capture (once) and replay the whole multiply for fixed (pointers, batch, sizes)
+int launch_graph(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, size_t nl, uint32_t* c, size_t nc,
+                 cudaStream_t s) {
   int rc;
   if ((rc = ensure_ws(P, batch))) return rc;
-  cudaStream_t s = (cudaStream_t)stream;
   GraphKey key{batch, a, b, c, nl, nc};
   auto it = P->graphs.find(key);
   if (it == P->graphs.end()) {
@@ -528,13 +558,14 @@ int dkss_mul_device(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* 
     CUCHK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     CUCHK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
     rc = run_mul(P, batch, a, b, (long long)nl, P->d_prod, cap);
-    if (!rc && (long long)nc == P->prod_limbs) {
-      // decode wrote into d_prod; copy into the caller's buffer
-      cudaMemcpyAsync(c, P->d_prod, (size_t)batch * P->prod_limbs * 4, cudaMemcpyDeviceToDevice, cap);
-    } else if (!rc) {
-      cudaMemsetAsync(c, 0, (size_t)batch * nc * 4, cap);
-      cudaMemcpy2DAsync(c, nc * 4, P->d_prod, P->prod_limbs * 4, P->prod_limbs * 4, batch, cudaMemcpyDeviceToDevice,
-                        cap);
+    if (!rc && c != P->d_prod) {
+      if ((long long)nc == P->prod_limbs) {
+        cudaMemcpyAsync(c, P->d_prod, (size_t)batch * P->prod_limbs * 4, cudaMemcpyDeviceToDevice, cap);
+      } else {
+        cudaMemsetAsync(c, 0, (size_t)batch * nc * 4, cap);
+        cudaMemcpy2DAsync(c, nc * 4, P->d_prod, P->prod_limbs * 4, P->prod_limbs * 4, batch,
+                          cudaMemcpyDeviceToDevice, cap);
+      }
     }
     cudaGraph_t g;
     cudaError_t e = cudaStreamEndCapture(cap, &g);
@@ -548,7 +579,20 @@ int dkss_mul_device(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* 
     it = P->graphs.emplace(key, ge).first;
   }
   CUCHK(cudaGraphLaunch(it->second, s));
-  return DKSS_OK;
+  return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int dkss_mul_device(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, size_t nl, uint32_t* c, size_t nc,
+                    void* stream) {
+  if (!P || batch < 1 || !a || !b || !c) return fail(DKSS_EINVAL, "bad argument");
+  if ((long long)nl > P->op_limbs) return fail(DKSS_ERANGE, "operand limbs %zu exceed plan (%lld)", nl, P->op_limbs);
+  if ((long long)nc < P->prod_limbs) return fail(DKSS_EINVAL, "nc=%zu below product limbs %lld", nc, P->prod_limbs);
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  return launch_graph(P, batch, a, b, nl, c, nc, (cudaStream_t)stream);
 }
 
 int dkss_profile_device(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, size_t nl, uint32_t* c,
@@ -601,7 +645,7 @@ int dkss_mul_batch(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b
   memcpy(P->h_pin, a, opw * 4);
   memcpy(P->h_pin + opw, b, opw * 4);
   CUCHK(cudaMemcpyAsync(P->d_ops, P->h_pin, 2 * opw * 4, cudaMemcpyHostToDevice, s));
-  if ((rc = run_mul(P, batch, P->d_ops, P->d_ops + opw, (long long)nl, P->d_prod, s))) return rc;
+  if ((rc = launch_graph(P, batch, P->d_ops, P->d_ops + opw, nl, P->d_prod, P->prod_limbs, s))) return rc;
   CUCHK(cudaMemcpyAsync(P->h_pin, P->d_prod, prw * 4, cudaMemcpyDeviceToHost, s));
   CUCHK(cudaStreamSynchronize(s));
   for (int i = 0; i < batch; ++i) {

@@ -344,6 +344,7 @@ struct PassArgs {
   int enc_split;
   int u;                 // bits per inner coefficient
   int M;                 // outer length (elements e >= M are zero)
+  int wpc;               // warp-per-column kernels: warps sharing one column (power of 2)
 };
 
 template <int MM>

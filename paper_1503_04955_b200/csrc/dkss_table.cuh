@@ -2,12 +2,16 @@
 // translation unit (dkss_inst_m*.cu) so the build parallelises.
 #pragma once
 #include "dkss_kernels.cuh"
+#include "dkss_warp.cuh"
 
 namespace dkss {
 
 struct KTable {
   void (*fwd)(PassArgs, ModCtx);
   void (*inv)(PassArgs, ModCtx);
+  void (*fwd_w)(PassArgs, ModCtx);  // warp-per-column variants (m <= 16), else null
+  void (*inv_w)(PassArgs, ModCtx);
+  size_t smem_fwd_w, smem_inv_w;    // dynamic shared memory per CTA (kWarpsPerCta warps)
   void (*bottom)(BottomArgs, ModCtx);
   void (*rmul)(const uint32_t*, const uint32_t*, uint32_t*, long long, ModCtx);
   void (*mscale)(uint32_t*, long long, int, ModCtx);
@@ -22,9 +26,18 @@ struct KTable {
 
 template <int MM, int L>
 KTable make_table() {
-  KTable t;
+  KTable t{};
   t.fwd = k_fwd_pass<MM, L>;
   t.inv = k_inv_pass<MM, L>;
+  if constexpr (MM <= 16) {
+    t.fwd_w = k_fwd_warp<MM, L>;
+    t.inv_w = k_inv_warp<MM, L>;
+    t.smem_fwd_w = (size_t)kWarpsPerCta * 2 * MM * Smem<MM, L>::ES * 4;
+    t.smem_inv_w = 2 * t.smem_fwd_w;
+  } else {
+    t.fwd_w = t.inv_w = nullptr;
+    t.smem_fwd_w = t.smem_inv_w = 0;
+  }
   t.bottom = k_bottom<MM, L>;
   t.rmul = k_rmul<MM, L>;
   t.mscale = k_mont_scale<L>;

@@ -36,6 +36,24 @@ _MIN_PLAN_BITS = 1024
 
 _dev_lock = threading.Lock()
 _dev_plans: dict = {}
+_host_plans: dict = {}
+
+
+def _plan_for(N: int, w: int) -> DkssPlan:
+    """Host plan for inputs below 2^N at word size w, built (and verified) once.
+
+    The reference re-runs dkss_select_params on every dmul (the rho-power table is
+    cached in make_plan, bigmul/dkss.py:220-233, but rho is re-verified each call);
+    the plan is a pure function of (N, w), so caching it changes no result.
+    """
+    key = (N, w)
+    with _dev_lock:
+        pl = _host_plans.get(key)
+    if pl is None:
+        pl = dkss_select_params(N, w)
+        with _dev_lock:
+            _host_plans.setdefault(key, pl)
+    return pl
 
 
 def _device() -> int:
@@ -139,28 +157,40 @@ def dkss_decode(v, plan: DkssPlan, arena: ScratchArena | None = None) -> Natural
 # ---------------------------------------------------------------------------
 # the multiply
 
+def _as_int_len(x, w: int):
+    """(value, word length) exactly as as_natural(x) would give (bigmul/words.py:112-117)."""
+    if isinstance(x, Natural):
+        return x.to_int(), len(x)
+    if isinstance(x, int) and not isinstance(x, bool):
+        if x < 0:
+            raise ValueError("Natural is nonnegative")
+        return x, max(1, -(-x.bit_length() // w))
+    n = as_natural(x)
+    return n.to_int(), len(n)
+
+
 def dmul(a, b, thresholds=None, arena: ScratchArena | None = None) -> Natural:
     """Full product via DKSS on the GPU (bigmul/dkss.py:520-548)."""
-    a, b = as_natural(a), as_natural(b)
+    w = word_bits()
+    ai, la = _as_int_len(a, w)
+    bi, lb = _as_int_len(b, w)
     arena = arena or current_arena()
-    ai, bi = a.to_int(), b.to_int()
-    outlen = max(1, len(a) + len(b))
+    outlen = max(1, la + lb)
     if ai == 0 or bi == 0:
         return Natural([0] * outlen)
     n_bits = max(ai.bit_length(), bi.bit_length())
     N = max(n_bits, _MIN_PLAN_BITS)
-    plan = dkss_select_params(N, word_bits(), thresholds)
+    plan = _plan_for(N, w)
     dp = device_plan(plan)
     info = dp.info
     nl = info["operand_limbs"]
-    w = word_bits()
     nc = max(info["product_limbs"], -(-outlen * w // 32))
     with arena.frame():
         # device workspace per multiply: 2 polynomials + operands + product, in words
         arena.alloc_words((2 * info["poly_bytes"] + 4 * (2 * nl + nc)) * 8 // w)
         c = dp.mul_limbs(int_to_u32(ai, nl), int_to_u32(bi, nl), nc)
     plan.ks_calls += ring_products_per_multiply(plan)
-    return Natural.from_int(u32_to_int(c), length=outlen)
+    return Natural._from_u32(c, outlen, w)
 
 
 def dmul_many(pairs, thresholds=None) -> list:
@@ -170,7 +200,7 @@ def dmul_many(pairs, thresholds=None) -> list:
         return []
     n_bits = max(max(int(a).bit_length(), int(b).bit_length()) for a, b in pairs)
     N = max(n_bits, _MIN_PLAN_BITS)
-    plan = dkss_select_params(N, word_bits(), thresholds)
+    plan = _plan_for(N, word_bits())
     dp = device_plan(plan)
     nl = dp.info["operand_limbs"]
     A = np.stack([int_to_u32(int(a), nl) for a, _ in pairs])

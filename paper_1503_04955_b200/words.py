@@ -79,13 +79,41 @@ class Natural:
 
     Mirrors ``bigmul.words.Natural``: leading zero words are allowed, the
     object is treated as immutable, equality compares values (also against
-    plain ints).
+    plain ints).  Products coming back from the device keep their limb array
+    and build the word list only when ``words`` is first read.
     """
 
-    __slots__ = ("words",)
+    __slots__ = ("_words", "_limbs", "_w", "_len")
 
     def __init__(self, words):
-        self.words = list(words)
+        self._words = list(words)
+        self._limbs = None
+        self._w = None
+        self._len = len(self._words)
+
+    @classmethod
+    def _from_u32(cls, limbs: np.ndarray, length: int, w: int) -> "Natural":
+        """Natural of `length` w-bit words from little-endian u32 limbs (no per-word Python work)."""
+        obj = cls.__new__(cls)
+        need = -(-length * w // 32)
+        if limbs.size < need:
+            limbs = np.concatenate([limbs, np.zeros(need - limbs.size, dtype=np.uint32)])
+        obj._limbs = limbs[:need] if (length * w) % 32 == 0 else limbs
+        obj._w = w
+        obj._len = length
+        obj._words = None
+        return obj
+
+    @property
+    def words(self) -> list:
+        if self._words is None:
+            dt = {8: np.uint8, 16: np.uint16, 32: np.uint32, 64: np.uint64}[self._w]
+            raw = np.ascontiguousarray(self._limbs, dtype=np.uint32).tobytes()
+            nbytes = self._len * self._w // 8
+            raw = raw[:nbytes] + b"\0" * max(0, nbytes - len(raw))
+            self._words = np.frombuffer(raw, dtype=dt).tolist()
+            self._limbs = None
+        return self._words
 
     @classmethod
     def from_int(cls, value: int, length: int | None = None, w: int | None = None) -> "Natural":
@@ -100,19 +128,23 @@ class Natural:
         return cls(int_to_words(value, length, w))
 
     def to_int(self, w: int | None = None) -> int:
-        return words_to_int(self.words, word_bits() if w is None else w)
+        w = word_bits() if w is None else w
+        if self._words is None and w == self._w:
+            return int.from_bytes(np.ascontiguousarray(self._limbs, dtype=np.uint32).tobytes(), "little")
+        return words_to_int(self.words, w)
 
     def normalized(self) -> "Natural":
-        n = len(self.words)
-        while n > 1 and self.words[n - 1] == 0:
+        ws = self.words
+        n = len(ws)
+        while n > 1 and ws[n - 1] == 0:
             n -= 1
-        return Natural(self.words[:n])
+        return Natural(ws[:n])
 
     def bit_length(self, w: int | None = None) -> int:
         return self.to_int(w).bit_length()
 
     def __len__(self) -> int:
-        return len(self.words)
+        return self._len
 
     def __eq__(self, other) -> bool:
         if isinstance(other, Natural):
