@@ -125,6 +125,8 @@ struct dkss_plan {
   uint32_t* d_twr = nullptr;  // twiddle rows [M/m][2m][L]: Montgomery-form rho^s, then W_s
   int grid_pass = 0, grid_bot = 0;  // persistent grid sizes (SMs x resident CTAs)
   int grid_fw = 0, grid_iw = 0;     // warp-per-column kernels (0 = not used)
+  int grid_dft = 0, grid_tw = 0;    // split passes (column DFT kernel + elementwise twiddles)
+  int pass_mode = 0;                // 0 auto, 1 CTA-fused, 2 warp-fused, 3 split
   // workspace
   int cap_batch = 0;
   uint32_t* d_poly = nullptr;  // 2 * cap_batch polynomials
@@ -224,6 +226,24 @@ int launch_encode(dkss_plan* P, const uint32_t* ops, long long na, uint32_t* pol
   return 0;
 }
 
+// pass implementation for a launch over `cols` columns: 1 CTA-fused, 2 warp-fused, 3 split
+int pass_kind(const dkss_plan* P, long long cols) {
+  if (P->pass_mode) return (P->pass_mode == 3 && !P->grid_dft) ? 1 : (P->pass_mode == 2 && !P->grid_fw) ? 1 : P->pass_mode;
+  if (P->grid_fw && cols >= 4LL * P->grid_fw * kWarpsPerCta) return 2;
+  return 1;
+}
+
+void launch_dft(dkss_plan* P, const PassArgs& A, long long cols, cudaStream_t s) {
+  const int g = (int)std::min<long long>(P->grid_dft, (cols + kWarpsPerCta - 1) / kWarpsPerCta);
+  P->kt.dft<<<g, kWarpsPerCta * 32, P->kt.smem_dft, s>>>(A, P->mc);
+}
+
+void launch_tw(dkss_plan* P, const PassArgs& A, long long cols, cudaStream_t s) {
+  const long long items = cols * 2 * P->m * (P->m / 2);  // T = 2 outputs per item
+  const int g = (int)std::min<long long>(P->grid_tw, (items + 255) / 256);
+  P->kt.tw<<<g, 256, 0, s>>>(A, P->mc);
+}
+
 int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s, const uint32_t* ops_a = nullptr,
                       const uint32_t* ops_b = nullptr, long long na = 0, int enc_split = 0) {
   const long long cols = (long long)npoly << P->log_top_mu;
@@ -248,7 +268,14 @@ int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s, c
       A.u = P->u;
       A.M = P->M;
     }
-    if (P->grid_fw && cols >= 4LL * P->grid_fw * kWarpsPerCta) {
+    const int kind = pass_kind(P, cols);
+    if (kind == 3) {
+      launch_dft(P, A, cols, s);
+      CUCHK(cudaGetLastError());
+      PassArgs B = A;
+      B.ops_a = B.ops_b = nullptr;
+      launch_tw(P, B, cols, s);
+    } else if (kind == 2) {
       // warp-per-column only when every resident warp gets several columns (large batches);
       // small transforms keep the CTA-wide kernel, which spreads a column over 8 warps
       const long long wres = (long long)P->grid_fw * kWarpsPerCta;
@@ -279,7 +306,14 @@ int launch_inv_levels(dkss_plan* P, uint32_t* poly, int npoly, bool scale_last, 
     A.twr = P->d_twr;
     A.scale = (lv == 0 && scale_last) ? 1 : 0;
     A.total_cols = cols;
-    if (P->grid_iw && cols >= 4LL * P->grid_iw * kWarpsPerCta) {
+    const int kind = pass_kind(P, cols);
+    if (kind == 3) {
+      PassArgs B = A;
+      B.scale = 0;
+      launch_tw(P, B, cols, s);
+      CUCHK(cudaGetLastError());
+      launch_dft(P, A, cols, s);
+    } else if (kind == 2 && P->grid_iw) {
       A.wpc = 1;
       const int gw = (int)std::min<long long>(P->grid_iw, (cols + kWarpsPerCta - 1) / kWarpsPerCta);
       P->kt.inv_w<<<gw, kWarpsPerCta * 32, P->kt.smem_inv_w, s>>>(A, P->mc);
@@ -327,6 +361,8 @@ int launch_decode(dkss_plan* P, const uint32_t* v, uint32_t* out, int npoly, cud
   A.u = P->u;
   const int grid = A.blocks_per_poly * npoly;
   k_decode1<<<grid, kDecThreads, 0, s>>>(A);
+  CUCHK(cudaGetLastError());
+  k_decode_scan<<<npoly, kScanThreads, 0, s>>>(A);
   CUCHK(cudaGetLastError());
   mark(P, s, DKSS_K_DECODE1, 0, npoly * (P->poly_words * 4 + P->prod_limbs * 4));
   k_decode2<<<grid, kDecThreads, 0, s>>>(A);
@@ -470,6 +506,19 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
       P->grid_fw = ofw > 0 ? sms * ofw : 0;
       P->grid_iw = oiw > 0 ? sms * oiw : 0;
     }
+    if (kt.dft) {
+      int od = 0;
+      CUCHK(cudaFuncSetAttribute((const void*)kt.dft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kt.smem_dft));
+      CUCHK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&od, kt.dft, kWarpsPerCta * 32, kt.smem_dft));
+      P->grid_dft = od > 0 ? sms * od : 0;
+    }
+    {
+      int ot = 0;
+      CUCHK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ot, kt.tw, 256, 0));
+      P->grid_tw = sms * std::max(ot, 1);
+    }
+    const char* pm = getenv("DKSS_PASS_MODE");
+    if (pm) P->pass_mode = atoi(pm);
   }
   // cbias = -(2^(32L) - 1) * R mod p = (p - ((R mod p) - 1)) * R mod p  (ring_mul bias correction)
   {
@@ -538,7 +587,7 @@ int dkss_plan_get_info(const dkss_plan* P, dkss_plan_info* o) {
   o->product_limbs = P->prod_limbs;
   o->twiddles_per_fft = P->twiddles;
   o->ring_products = 3 * P->twiddles + 2LL * P->M;
-  o->launches_per_mul = (P->levels > 0 ? 0 : 2) + P->levels + 1 + P->levels + 2;
+  o->launches_per_mul = (P->levels > 0 ? 0 : 2) + P->levels + 1 + P->levels + 3;
   o->workspace_bytes = (int64_t)P->ws_bytes;
   return DKSS_OK;
 }

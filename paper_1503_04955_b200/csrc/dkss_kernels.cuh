@@ -910,14 +910,34 @@ __device__ __forceinline__ unsigned long long window_sum(const DecodeArgs& A, co
   if (t < 0) return 0ull;
   const long long twoM = 2LL * A.M;
   const int half = A.MM / 2;
+  const int lh = __ffs(half) - 1;
+  unsigned long long S = 0;
+  if (A.u == 32) {
+    // slot s = t - q contributes limb q of its two coefficients (l = s/half, l - 1)
+#pragma unroll 1
+    for (int q = 0; q < A.L; ++q) {
+      const long long s = t - q;
+      if (s < 0) break;
+      const long long lq = s >> lh;
+      const int kk = (int)(s & (half - 1));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const long long l = lq - h;
+        const int k = kk + h * half;
+        if (l < 0 || l >= twoM) continue;
+        const long long src = (twoM - l) & (twoM - 1);
+        S += __ldg(v + (src * A.MM + k) * A.L + q);
+      }
+    }
+    return S;
+  }
   const long long wbits = 32LL * A.L;
   long long s_lo = (32 * t - wbits) / A.u + 1;
   if (32 * t - wbits < 0) s_lo = 0;
   const long long s_hi = (32 * t + 31) / A.u;
-  unsigned long long S = 0;
   for (long long s = s_lo; s <= s_hi; ++s) {
     const long long off = 32 * t - (long long)A.u * s;  // bit offset of window inside coefficient
-    const long long lq = s / half;
+    const long long lq = s >> lh;
     for (int h = 0; h < 2; ++h) {
       const long long l = lq - h;
       const long long k = s - l * half;
@@ -927,10 +947,10 @@ __device__ __forceinline__ unsigned long long window_sum(const DecodeArgs& A, co
       uint32_t word;
       if (off >= 0) {
         const int q = (int)(off >> 5), sh = (int)(off & 31);
-        const uint32_t lo = q < A.L ? c[q] : 0u, hi = q + 1 < A.L ? c[q + 1] : 0u;
+        const uint32_t lo = q < A.L ? __ldg(c + q) : 0u, hi = q + 1 < A.L ? __ldg(c + q + 1) : 0u;
         word = sh ? __funnelshift_r(lo, hi, sh) : lo;
       } else {
-        word = c[0] << (int)(-off);
+        word = __ldg(c) << (int)(-off);
       }
       S += word;
     }
@@ -938,6 +958,7 @@ __device__ __forceinline__ unsigned long long window_sum(const DecodeArgs& A, co
   return S;
 }
 
+// phase 1: per-limb sums, per-warp (generate, propagate) masks, per-block carry function
 __global__ void __launch_bounds__(kDecThreads) k_decode1(DecodeArgs A) {
   const int pidx = blockIdx.x / A.blocks_per_poly;
   const int blk = blockIdx.x % A.blocks_per_poly;
@@ -977,29 +998,61 @@ __global__ void __launch_bounds__(kDecThreads) k_decode1(DecodeArgs A) {
   }
 }
 
+// phase 2: one CTA per product turns the block carry functions into block carry-ins
+// (bit 2 of bstat).  Carry functions of a block are kill (c0=c1=0), propagate (c0=0,c1=1)
+// or generate (c0=c1=1); thread chunks are composed sequentially, the 1024 chunk results
+// with the (generate | propagate) + generate add trick at warp and CTA level.
+constexpr int kScanThreads = 1024;
+__global__ void __launch_bounds__(kScanThreads) k_decode_scan(DecodeArgs A) {
+  const int B = A.blocks_per_poly;
+  uint32_t* st = A.bstat + (long long)blockIdx.x * B;
+  const int per = (B + kScanThreads - 1) / kScanThreads;
+  const int b0 = threadIdx.x * per, b1 = min(B, b0 + per);
+  // compose this thread's chunk: f(cin) = cout
+  unsigned f0 = 0, f1 = 1;  // identity
+  for (int b = b0; b < b1; ++b) {
+    const unsigned s = st[b];
+    const unsigned c0 = s & 1u, c1 = (s >> 1) & 1u;
+    f0 = f0 ? c1 : c0;
+    f1 = f1 ? c1 : c0;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool g = f0, p = f1 && !f0;
+  const unsigned G = __ballot_sync(0xFFFFFFFFu, g), P = __ballot_sync(0xFFFFFFFFu, p);
+  __shared__ unsigned wg[32], wp[32], wcin[32];
+  if (lane == 0) {
+    const unsigned long long a = (unsigned long long)(G | P), b = G;
+    wg[warp] = (unsigned)((a + b) >> 32);
+    wp[warp] = (unsigned)((a + b + 1) >> 32);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const bool c0 = wg[lane], c1 = wp[lane];
+    const unsigned WG = __ballot_sync(0xFFFFFFFFu, c0), WP = __ballot_sync(0xFFFFFFFFu, c1 && !c0);
+    const unsigned long long a = (unsigned long long)(WG | WP), b = WG;
+    const unsigned long long carries = (a + b) ^ a ^ b;  // carry into each warp, product cin = 0
+    wcin[lane] = (unsigned)((carries >> lane) & 1ull);
+  }
+  __syncthreads();
+  const unsigned long long a = (unsigned long long)(G | P), b = G;
+  const unsigned long long carries = (a + b + wcin[warp]) ^ a ^ b;
+  unsigned cin = (unsigned)((carries >> lane) & 1ull);
+  for (int bb = b0; bb < b1; ++bb) {
+    const unsigned s = st[bb];
+    st[bb] = (s & 3u) | (cin << 2);
+    cin = cin ? (s >> 1) & 1u : s & 1u;
+  }
+}
+
+// phase 3: apply carries inside each block
 __global__ void __launch_bounds__(kDecThreads) k_decode2(DecodeArgs A) {
   const int pidx = blockIdx.x / A.blocks_per_poly;
   const int blk = blockIdx.x % A.blocks_per_poly;
   const long long t = (long long)blk * kDecThreads + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ unsigned s_cin_block;
   __shared__ unsigned s_wcin[kDecWarps];
   if (warp == 0) {
-    // carry into this block: scan the statuses of blocks 0..blk-1 of this poly
-    unsigned cin = 0;
-    const uint32_t* st = A.bstat + (long long)pidx * A.blocks_per_poly;
-    for (int base = 0; base < blk; base += 32) {
-      const int bi = base + lane;
-      const unsigned sv = bi < blk ? st[bi] : 0u;
-      const bool c0 = sv & 1u, c1 = (sv >> 1) & 1u;
-      const unsigned G = __ballot_sync(0xFFFFFFFFu, bi < blk && c0);
-      const unsigned P = __ballot_sync(0xFFFFFFFFu, bi < blk && c1 && !c0);
-      const int n = min(32, blk - base);
-      const unsigned long long a = (unsigned long long)(G | P), b = G;
-      const unsigned long long sum = a + b + cin;
-      cin = (unsigned)((sum >> n) & 1ull);
-    }
-    // carries into each warp of this block
+    const unsigned cin = (A.bstat[(long long)pidx * A.blocks_per_poly + blk] >> 2) & 1u;
     const long long wi = ((long long)pidx * A.blocks_per_poly + blk) * kDecWarps + lane;
     const unsigned G = lane < kDecWarps ? A.gmask[wi] : 0u, P = lane < kDecWarps ? A.pmask[wi] : 0u;
     const unsigned long long a = (unsigned long long)(G | P), b = G;
@@ -1008,7 +1061,6 @@ __global__ void __launch_bounds__(kDecThreads) k_decode2(DecodeArgs A) {
     const unsigned long long wa = (unsigned long long)(WG | WP), wb = WG;
     const unsigned long long carries = (wa + wb + cin) ^ wa ^ wb;  // bit i = carry into warp i
     if (lane < kDecWarps) s_wcin[lane] = (unsigned)((carries >> lane) & 1ull);
-    if (lane == 0) s_cin_block = cin;
   }
   __syncthreads();
   if (t >= A.nout) return;

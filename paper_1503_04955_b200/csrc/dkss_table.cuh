@@ -12,6 +12,9 @@ struct KTable {
   void (*fwd_w)(PassArgs, ModCtx);  // warp-per-column variants (m <= 16), else null
   void (*inv_w)(PassArgs, ModCtx);
   size_t smem_fwd_w, smem_inv_w;    // dynamic shared memory per CTA (kWarpsPerCta warps)
+  void (*dft)(PassArgs, ModCtx);    // split passes: column DFT (m <= 16) and elementwise twiddle
+  void (*tw)(PassArgs, ModCtx);
+  size_t smem_dft;
   void (*bottom)(BottomArgs, ModCtx);
   void (*rmul)(const uint32_t*, const uint32_t*, uint32_t*, long long, ModCtx);
   void (*mscale)(uint32_t*, long long, int, ModCtx);
@@ -29,11 +32,14 @@ KTable make_table() {
   KTable t{};
   t.fwd = k_fwd_pass<MM, L>;
   t.inv = k_inv_pass<MM, L>;
+  t.tw = k_twiddle<MM, L>;
   if constexpr (MM <= 16) {
     t.fwd_w = k_fwd_warp<MM, L>;
     t.inv_w = k_inv_warp<MM, L>;
     t.smem_fwd_w = (size_t)kWarpsPerCta * 2 * MM * Smem<MM, L>::ES * 4;
     t.smem_inv_w = 2 * t.smem_fwd_w;
+    t.dft = k_dft_cols<MM, L>;
+    t.smem_dft = t.smem_fwd_w;
   } else {
     t.fwd_w = t.inv_w = nullptr;
     t.smem_fwd_w = t.smem_inv_w = 0;

@@ -248,3 +248,98 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_inv_warp(PassArgs A, M
 }
 
 }  // namespace dkss
+
+namespace dkss {
+
+// ---------------------------------------------------------------------------
+// Split passes: column DFT kernel + elementwise twiddle kernel.
+//
+// k_dft_cols: one warp per 2m-element column (m <= 16), register DFT, in place.  Input
+// slots are read in bit-reversed order (TMA into the warp's slice), output element vv is
+// written back to position vv of the column.  Optional fused encode (first forward level)
+// and (2M)^-1 scaling (last inverse level).
+template <int MM, int L>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_dft_cols(PassArgs A, ModCtx mc) {
+  constexpr int ES = Smem<MM, L>::ES, E = 2 * MM, EPT = WG<MM>::EPT, LOGE = Geo<MM>::LOGE;
+  extern __shared__ __align__(16) uint32_t smem[];
+  __shared__ __align__(8) uint64_t bars[kWarpsPerCta];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = lane & (MM - 1), g = lane / MM;
+  uint32_t* buf = smem + warp * E * ES;
+  uint64_t* bar = &bars[warp];
+  if (lane == 0) mbar_init(bar, 1);
+  __syncwarp();
+  const long long gw = (long long)blockIdx.x * kWarpsPerCta + warp;
+  const long long nw = (long long)gridDim.x * kWarpsPerCta;
+  const bool enc = A.ops_a != nullptr;
+  uint32_t phase = 0;
+  long long cg = gw;
+  if (!enc && cg < A.total_cols) warp_issue_column<MM, L, true>(A, cg, bar, buf);
+  uint32_t ks[L];
+#pragma unroll
+  for (int q = 0; q < L; ++q) ks[q] = mc.kscale[q];
+  for (; cg < A.total_cols; cg += nw) {
+    uint32_t X[EPT][L];
+    if (enc) {
+#pragma unroll
+      for (int i = 0; i < EPT; ++i) encode_coef<MM, L>(A, cg, bitrev_n(g * EPT + i, LOGE), c, X[i]);
+    } else {
+      mbar_wait(bar, phase);
+      phase ^= 1;
+#pragma unroll
+      for (int i = 0; i < EPT; ++i) ld_res<L>(X[i], buf + (g * EPT + i) * ES + c * L);
+      fence_proxy_async();
+      __syncwarp();
+      if (cg + nw < A.total_cols) warp_issue_column<MM, L, true>(A, cg + nw, bar, buf);
+    }
+    warp_dft<MM, L>(X, mc);
+    long long l;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      if (A.scale) mont_mul<L>(X[i], X[i], ks, mc);
+      st_res<L>(A.poly + col_elem(A, cg, g * EPT + i, LOGE, MM * L, &l) + c * L, X[i]);
+    }
+  }
+}
+
+// k_twiddle: elementwise twiddle ring products of one level, in place.  Work item = (element
+// position (j, l) of a column, kT output coefficients); the MM/kT items of an element are
+// adjacent lanes of one warp, so the element is read completely before any lane stores
+// (warp-synchronous in-place update).  Exponent j*l*base_pow (bigmul/dkss.py:480-492);
+// forward levels run it after k_dft_cols, inverse levels before.
+template <int MM, int L>
+__global__ void __launch_bounds__(256, 2) k_twiddle(PassArgs A, ModCtx mc) {
+  constexpr int kT = Cfg<MM>::T, TPE = MM / kT, E = 2 * MM, LOGE = Geo<MM>::LOGE;
+  static_assert(32 % TPE == 0, "an element's work items must share a warp");
+  const long long total = A.total_cols * E * TPE;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  // all lanes iterate the same number of times (warp-synchronous stores below)
+  const long long iters = (total + stride - 1) / stride;
+  long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (long long n = 0; n < iters; ++n, it += stride) {
+    const bool live = it < total;
+    const long long el = it / TPE;
+    const int k0 = (int)(it % TPE) * kT;
+    const long long cg = el / E;
+    const int j = (int)(el % E);
+    uint32_t w[kT][L];
+    int r = 0;
+    uint32_t* dst = nullptr;
+    if (live) {
+      long long l;
+      dst = A.poly + col_elem(A, cg, j, LOGE, MM * L, &l);
+      const long long s = tw_exp(A, j, l, &r);
+      if (s == 0) {
+#pragma unroll
+        for (int t = 0; t < kT; ++t) ld_res<L>(w[t], dst + (k0 + t) * L);
+      } else {
+        const uint32_t* row = A.twr + s * (2 * MM * L);
+        ring_mul<MM, L>(ResG<L>{row}, ResG<L>{dst}, ResG<L>{row + MM * L}, k0, mc, w);
+      }
+    }
+    __syncwarp();
+    if (live) store_rot<MM, L, kT>(dst, w, k0, r, mc);
+  }
+}
+
+}  // namespace dkss

@@ -84,9 +84,10 @@ int main() {
 
   run<16, 4, 2, 256, 2>("m16 T2 NT256 minb2", seed, out, mc);
   run<16, 4, 2, 256, 3>("m16 T2 NT256 minb3", seed, out, mc);
-  run<16, 4, 2, 128, 6>("m16 T2 NT128 minb6", seed, out, mc);
+  run<16, 4, 1, 256, 3>("m16 T1 NT256 minb3", seed, out, mc);
+  run<16, 4, 1, 256, 4>("m16 T1 NT256 minb4", seed, out, mc);
   run<32, 4, 2, 256, 2>("m32 T2 NT256 minb2", seed, out, mc);
-  run<32, 4, 2, 256, 3>("m32 T2 NT256 minb3", seed, out, mc);
-  run<8, 2, 2, 256, 2>("m8 L2 T2 NT256", seed, out, mc);
+  run<32, 4, 1, 256, 3>("m32 T1 NT256 minb3", seed, out, mc);
+  run<32, 4, 1, 256, 4>("m32 T1 NT256 minb4", seed, out, mc);
   return 0;
 }
