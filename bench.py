@@ -7,9 +7,10 @@ One JSON line on rank 0.  A "step" is one pass of the hot path over one batch
 of synthetic input: for the default workload (BASELINE.json configs[1],
 2^20 x 2^20 bits, uniform random with the top bit set) one full DKSS
 multiply.  `value` = product Gbit/s (2N bits per product / device time), whole
-job over all ranks; multi-GPU runs are weak-scaled independent multiplies (one
-per rank per step, no data-path collective -- the single-multiply path does not
-shard).
+job over all ranks.  Multi-GPU runs are weak-scaled independent multiplies (one
+per rank per step, no data-path collective) unless `--split` is given: then ONE
+multiply per step is split over the ranks with the four-step layout (SURVEY.md
+§8(e); NCCL all-to-all between the column and row phases, strong scaling).
 
 Timing: CUDA events on the launching stream around every step, an L2 flush
 (256 MiB memset, outside the events) before every timed step, barrier +
@@ -191,6 +192,90 @@ def run_reference(args, cfg_name):
     print(json.dumps(line), flush=True)
 
 
+def run_split(args):
+    """One multiply per step, split over all ranks (four-step, NCCL all-to-all)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1503_04955_b200.fourstep import DistExchange, _operands, dmul_fourstep, make_rank, run_rank
+    from paper_1503_04955_b200.plan import dkss_select_params, ring_products_per_multiply
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world < 2:
+        raise SystemExit("--split needs torchrun with >= 2 ranks (tests emulate ranks on one GPU)")
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    os.environ["DKSS_DEVICE"] = str(local)
+    N, batch, seed, ones = CONFIGS[args.config]
+    if batch != 1:
+        raise SystemExit("--split applies to single-multiply configs")
+    a, b = operands(N, 1, seed, ones, 0)[0]  # every rank holds the same operands
+    plan = dkss_select_params(N)
+    fs = make_rank(plan, rank, world, dev)
+    A, B = _operands(plan, a, b, dev)
+    ex = DistExchange()
+    stream = torch.cuda.current_stream(dev)
+    prod = run_rank(fs, ex, A, B)
+    torch.cuda.synchronize(dev)
+    if rank == 0 and int.from_bytes(prod.cpu().numpy().view("uint32").tobytes(), "little") != a * b:
+        raise SystemExit("split product mismatch")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        flush.zero_()
+        run_rank(fs, ex, A, B)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    with clocks:
+        for k in range(args.steps):
+            flush.zero_()
+            dist.barrier()
+            starts[k].record(stream)
+            run_rank(fs, ex, A, B)
+            ends[k].record(stream)
+        torch.cuda.synchronize(dev)
+    dist.barrier()
+    t = torch.tensor([sum(s.elapsed_time(e) for s, e in zip(starts, ends))], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / args.steps
+    e2e = []
+    for _ in range(3):
+        dist.barrier()
+        t0 = time.perf_counter()
+        dmul_fourstep(a, b)
+        e2e.append(time.perf_counter() - t0)
+    e2e_s = sorted(e2e)[1]
+    if rank == 0:
+        peak, peak_src = imad_peak()
+        info = fs.stages.dp.info
+        w_mul = ring_products_per_multiply(plan) * plan.m * plan.m * info["L"] * info["L"]
+        per_gpu = w_mul / world / (ms_per_step * 1e-3)
+        lay = fs.stages.layout(world)
+        line = {
+            "metric": "N x N-bit DKSS multiply: product Gbit/s", "value": round(2 * N / (ms_per_step * 1e-3) / 1e9, 4),
+            "unit": "Gbit/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_per_step, 5), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic (seeded random operands, SURVEY.md §8(d))",
+            "config": {"workload": args.config, "bits": N, "batch": 1, "parallelism": f"four-step split x{world}",
+                       "exchange_bytes_per_rank": 3 * 4 * lay["block_words"] * (world - 1) // world,
+                       "l2": "flushed (256 MiB memset) before every timed step"},
+            "roofline": {"bound": "imad", "achieved": round(per_gpu / 1e12, 4), "peak": round(peak / 1e12, 4),
+                         "unit": "T limb-products/s per GPU", "frac": round(per_gpu / peak, 4), "traffic": None,
+                         "kernel": "whole split multiply", "peak_source": peak_src},
+            "e2e": {"value": round(2 * N / e2e_s / 1e9, 4), "unit": "Gbit/s", "ms": round(e2e_s * 1e3, 3),
+                    "h2d_bytes_per_step": 2 * A.numel() * 4 * world, "d2h_bytes_per_step": fs.prod.numel() * 4,
+                    "api": "paper_1503_04955_b200.fourstep.dmul_fourstep(int, int)"},
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -201,10 +286,14 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--split", action="store_true", help="four-step split of one multiply over the ranks")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args, args.config)
+        return
+    if args.split:
+        run_split(args)
         return
 
     import numpy as np
@@ -221,7 +310,7 @@ def main():
     torch.cuda.set_device(dev)
     os.environ["DKSS_DEVICE"] = str(local)
 
-    from paper_1503_04955_b200.dkss import device_plan, dmul
+    from paper_1503_04955_b200.dkss import device_plan, dmul, dmul_many
     from paper_1503_04955_b200.plan import dkss_select_params, ring_products_per_multiply
     from paper_1503_04955_b200.words import int_to_u32, u32_to_int
 
@@ -312,15 +401,22 @@ def main():
         with open(tpath) as f:
             traffic = json.load(f).get(args.config, {}).get(dom)
 
-    # end to end through the public API (Python ints in, Natural out; H2D + D2H inside)
+    # end to end through the public API (Python ints in, Natural / ints out; H2D + D2H inside):
+    # dmul for one product, dmul_many for the batched workload (one device call per step)
     e2e_times = []
     a0, b0 = pairs[0]
-    dmul(a0, b0)
-    for _ in range(args.e2e_steps):
+    if batch == 1:
+        def e2e_call():
+            return [dmul(a0, b0).to_int()]
+    else:
+        def e2e_call():
+            return dmul_many(pairs)
+    e2e_call()
+    for _ in range(max(3, args.e2e_steps if batch == 1 else args.e2e_steps // 4)):
         t0 = time.perf_counter()
-        r = dmul(a0, b0)
+        r = e2e_call()
         e2e_times.append(time.perf_counter() - t0)
-    if r.to_int() != a0 * b0:
+    if r[0] != a0 * b0 or r[-1] != pairs[-1][0] * pairs[-1][1]:
         raise SystemExit("e2e product mismatch")
     e2e_times.sort()
     e2e_s = e2e_times[len(e2e_times) // 2]
@@ -350,11 +446,13 @@ def main():
                         for k, v in per_kind.items()},
             "profile_total_ms": round(prof_total_ms, 5),
             "ring_products_per_mul": rp, "w_mul_limb_products": w_mul,
-            "gpu_launches": launches * args.steps + args.steps,  # DKSS kernels + the flush memset per step
-            "gpu_launches_dkss_per_step": launches,
-            "e2e": {"value": round(2 * N / e2e_s / 1e9, 4), "unit": "Gbit/s", "ms": round(e2e_s * 1e3, 4),
-                    "h2d_bytes_per_step": 2 * nl * 4, "d2h_bytes_per_step": npl * 4,
-                    "api": "paper_1503_04955_b200.dmul(int, int) (host ints -> Natural)"},
+            "gpu_launches": launches * args.steps,  # libdkss kernels in the timed region (flush memset excluded)
+            "gpu_launches_per_step": launches,
+            "e2e": {"value": round(2 * N * batch * world / e2e_s / 1e9, 4), "unit": "Gbit/s",
+                    "ms": round(e2e_s * 1e3, 4),
+                    "h2d_bytes_per_step": 2 * nl * 4 * batch, "d2h_bytes_per_step": npl * 4 * batch,
+                    "api": "paper_1503_04955_b200.dmul(int, int) -> Natural" if batch == 1 else
+                           "paper_1503_04955_b200.dmul_many([(int, int)] * batch) -> [int]"},
             "clocks": clocks.summary(),
         }
         if cpu:

@@ -95,9 +95,44 @@ int dkss_mul_device(dkss_plan* plan, int batch, const uint32_t* a_dev, const uin
 #define DKSS_K_INV_PASS 3
 #define DKSS_K_DECODE1 4
 #define DKSS_K_DECODE2 5
+#define DKSS_K_TRANSPOSE 6
 int dkss_profile_device(dkss_plan* plan, int batch, const uint32_t* a_dev, const uint32_t* b_dev, size_t n_limbs,
                         uint32_t* c_dev, void* stream, int max_launches, int32_t* kinds, float* ms, int64_t* work,
                         int64_t* bytes, int* n_launches);
+
+/* four-step split of ONE multiply over `world` GPUs (the reference's radix
+ * split of dkss_fft, bigmul/dkss.py:465-495).  E = 2m, mu0 = 2M/E; an element is m*L limbs.
+ * Rank r owns the global columns [r*C, (r+1)*C), C = mu0/world, of the first transform level,
+ * stored [E][C] per polynomial; after the exchange rank h owns the rows [h*R, (h+1)*R),
+ * R = E/world, stored [R][mu0] per polynomial.  world: power of 2, <= E, dividing mu0.
+ * All buffers are device pointers; every call is stream-ordered; the exchange itself (an
+ * all-to-all of world blocks of block_words/world limbs per polynomial) is the caller's, e.g.
+ * NCCL through torch.distributed (paper_1503_04955_b200/fourstep.py). */
+typedef struct {
+  int64_t cols;        /* C, first-level columns per rank */
+  int64_t rows;        /* R, rows per rank after the exchange */
+  int64_t elem_words;  /* m*L */
+  int64_t block_words; /* one polynomial's share per rank: poly_words / world */
+} dkss_fs_layout;
+int dkss_fs_layout_get(const dkss_plan* plan, int world, dkss_fs_layout* out);
+/* encode (bigmul/dkss.py:381-398) fused with the first forward level (column DFTs + twiddles,
+ * bigmul/dkss.py:471-492) of a and b over this rank's columns: x = [2][E][C] elements */
+int dkss_fs_columns_fwd(dkss_plan* plan, int rank, int world, const uint32_t* a_dev, const uint32_t* b_dev,
+                        size_t n_limbs, uint32_t* x_dev, void* stream);
+/* rows phase: deeper forward levels of a and b (bigmul/dkss.py:493-495), pointwise r_mul
+ * (bigmul/dkss.py:544-545), deeper inverse levels of the product: z = [2][R][mu0] elements
+ * (a rows then b rows); the product rows are left in z[0] */
+int dkss_fs_rows(dkss_plan* plan, int world, uint32_t* z_dev, void* stream);
+/* last inverse level (columns) of the product with the 1/2M scaling (bigmul/dkss.py:507):
+ * x = [E][C] elements of this rank's columns */
+int dkss_fs_columns_inv(dkss_plan* plan, int rank, int world, uint32_t* x_dev, void* stream);
+/* exchange re-layout: src [n][A][B][run_words] -> dst [n][B][A][run_words] (16-byte aligned,
+ * run_words a multiple of 4, n*A*B <= 65535) */
+int dkss_block_transpose(dkss_plan* plan, const uint32_t* src_dev, uint32_t* dst_dev, int n, int A, int B,
+                         int64_t run_words, void* stream);
+/* dkss_decode (bigmul/dkss.py:498-513) on the device: v = the scaled inverse transform as
+ * left by the device pipeline (full [E][mu0] layout); nc >= product_limbs limbs written */
+int dkss_decode_device(dkss_plan* plan, const uint32_t* v_dev, uint32_t* out_dev, size_t nc, void* stream);
 
 /* stage entry points for parity checks (host buffers) ------------------------------ */
 /* dkss_encode, bigmul/dkss.py:381-398: poly = uint32[2M][m][L] */

@@ -22,6 +22,8 @@ EXPORTS = (
     "dkss_plan_create", "dkss_plan_destroy", "dkss_plan_get_info", "dkss_last_error", "dkss_version",
     "dkss_mul", "dkss_mul_batch", "dkss_mul_device", "dkss_profile_device",
     "dkss_encode_host", "dkss_fft_host", "dkss_rmul_host", "dkss_decode_host",
+    "dkss_fs_layout_get", "dkss_fs_columns_fwd", "dkss_fs_rows", "dkss_fs_columns_inv",
+    "dkss_block_transpose", "dkss_decode_device",
 )
 
 DKSS_OK, DKSS_EINVAL, DKSS_ECUDA, DKSS_ERANGE, DKSS_ENOMEM = 0, -1, -2, -3, -4
@@ -50,6 +52,11 @@ class PlanInfo(ctypes.Structure):
                 ("product_limbs", ctypes.c_int64), ("ring_products", ctypes.c_int64),
                 ("twiddles_per_fft", ctypes.c_int64), ("launches_per_mul", ctypes.c_int32),
                 ("workspace_bytes", ctypes.c_int64)]
+
+
+class FsLayout(ctypes.Structure):
+    _fields_ = [("cols", ctypes.c_int64), ("rows", ctypes.c_int64), ("elem_words", ctypes.c_int64),
+                ("block_words", ctypes.c_int64)]
 
 
 _u32p = ctypes.POINTER(ctypes.c_uint32)
@@ -86,6 +93,12 @@ def load(path: str = LIB_PATH):
         L.dkss_fft_host.argtypes = [vp, _u32p, ctypes.c_int]
         L.dkss_rmul_host.argtypes = [vp, _u32p, _u32p, _u32p, ctypes.c_size_t]
         L.dkss_decode_host.argtypes = [vp, _u32p, _u32p, ctypes.c_size_t]
+        L.dkss_fs_layout_get.argtypes = [vp, ctypes.c_int, ctypes.POINTER(FsLayout)]
+        L.dkss_fs_columns_fwd.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t, vp, vp]
+        L.dkss_fs_rows.argtypes = [vp, ctypes.c_int, vp, vp]
+        L.dkss_fs_columns_inv.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp]
+        L.dkss_block_transpose.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, vp]
+        L.dkss_decode_device.argtypes = [vp, vp, vp, ctypes.c_size_t, vp]
         for name in EXPORTS:
             if not hasattr(L, name):
                 raise NativeUnavailable(f"{path} lacks symbol {name}")
@@ -163,7 +176,8 @@ class DevicePlan:
         _check(self._lib.dkss_mul_device(self._h, batch, ctypes.c_void_p(a_ptr), ctypes.c_void_p(b_ptr), n_limbs,
                                          ctypes.c_void_p(c_ptr), nc, ctypes.c_void_p(stream)))
 
-    KIND_NAMES = {0: "encode", 1: "fwd_pass", 2: "bottom", 3: "inv_pass", 4: "decode1", 5: "decode2"}
+    KIND_NAMES = {0: "encode", 1: "fwd_pass", 2: "bottom", 3: "inv_pass", 4: "decode1", 5: "decode2",
+                  6: "transpose"}
 
     def profile_device(self, batch: int, a_ptr: int, b_ptr: int, n_limbs: int, c_ptr: int, stream: int = 0):
         """Per-launch (kind, ms, limb-products, bytes) of one multiply, timed with CUDA events."""
@@ -203,3 +217,27 @@ class DevicePlan:
         out = np.zeros(nout, dtype=np.uint32)
         _check(self._lib.dkss_decode_host(self._h, _ptr(v), _ptr(out), nout))
         return out
+
+    # -- four-step split (device pointers, stream-ordered; see include/dkss.h) ----
+    def fs_layout(self, world: int) -> dict:
+        lay = FsLayout()
+        _check(self._lib.dkss_fs_layout_get(self._h, world, ctypes.byref(lay)))
+        return {k: getattr(lay, k) for k, _ in FsLayout._fields_}
+
+    def fs_columns_fwd(self, rank: int, world: int, a_ptr: int, b_ptr: int, n_limbs: int, x_ptr: int, stream: int = 0):
+        _check(self._lib.dkss_fs_columns_fwd(self._h, rank, world, ctypes.c_void_p(a_ptr), ctypes.c_void_p(b_ptr),
+                                             n_limbs, ctypes.c_void_p(x_ptr), ctypes.c_void_p(stream)))
+
+    def fs_rows(self, world: int, z_ptr: int, stream: int = 0):
+        _check(self._lib.dkss_fs_rows(self._h, world, ctypes.c_void_p(z_ptr), ctypes.c_void_p(stream)))
+
+    def fs_columns_inv(self, rank: int, world: int, x_ptr: int, stream: int = 0):
+        _check(self._lib.dkss_fs_columns_inv(self._h, rank, world, ctypes.c_void_p(x_ptr), ctypes.c_void_p(stream)))
+
+    def block_transpose(self, src_ptr: int, dst_ptr: int, n: int, a: int, b: int, run_words: int, stream: int = 0):
+        _check(self._lib.dkss_block_transpose(self._h, ctypes.c_void_p(src_ptr), ctypes.c_void_p(dst_ptr), n, a, b,
+                                              run_words, ctypes.c_void_p(stream)))
+
+    def decode_device(self, v_ptr: int, out_ptr: int, nc: int, stream: int = 0):
+        _check(self._lib.dkss_decode_device(self._h, ctypes.c_void_p(v_ptr), ctypes.c_void_p(out_ptr), nc,
+                                            ctypes.c_void_p(stream)))

@@ -244,22 +244,47 @@ void launch_tw(dkss_plan* P, const PassArgs& A, long long cols, cudaStream_t s) 
   P->kt.tw<<<g, 256, 0, s>>>(A, P->mc);
 }
 
+// layout of the polynomials a pass launch walks (see PassArgs): the whole transform
+// (full_geom), the local column block of a sharded first level, or the rows of a
+// sharded second phase (four-step split, dkss_fs_*)
+struct Geom {
+  long long poly_words;  // words per polynomial in this layout
+  int log_cpp;           // log2 columns per polynomial
+  long long l_off;       // global column offset (first level of a column shard)
+  int log_mu0;           // column stride at level 0 in this layout (-1: 2M/2m)
+};
+
+Geom full_geom(const dkss_plan* P) { return Geom{P->poly_words, P->log_top_mu, 0, -1}; }
+
+PassArgs pass_args(const dkss_plan* P, const Geom& g, uint32_t* poly, int npoly, int lv) {
+  PassArgs A{};
+  A.poly = poly;
+  A.poly_words = g.poly_words;
+  // column stride at level lv: mu_lv = 2M / (2m)^(lv+1)
+  A.log_mu = (lv == 0 && g.log_mu0 >= 0) ? g.log_mu0 : ilog2i(2LL * P->M) - P->logE * (lv + 1);
+  A.log_top_mu = P->log_top_mu;
+  A.log_cpp = g.log_cpp;
+  A.l_off = g.l_off;
+  A.log_mu_enc = P->log_top_mu;
+  A.base_pow = 1LL << (P->logE * lv);
+  A.twr = P->d_twr;
+  A.scale = 0;
+  A.total_cols = (long long)npoly << g.log_cpp;
+  A.wpc = 1;
+  return A;
+}
+
 int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s, const uint32_t* ops_a = nullptr,
-                      const uint32_t* ops_b = nullptr, long long na = 0, int enc_split = 0) {
-  const long long cols = (long long)npoly << P->log_top_mu;
+                      const uint32_t* ops_b = nullptr, long long na = 0, int enc_split = 0, int lv_lo = 0,
+                      int lv_hi = -1, const Geom* geom = nullptr) {
+  const Geom g = geom ? *geom : full_geom(P);
+  if (lv_hi < 0) lv_hi = P->levels;
+  const long long cols = (long long)npoly << g.log_cpp;
   const int grid = (int)std::min<long long>((cols + P->kt.cols - 1) / P->kt.cols, P->grid_pass);
-  for (int lv = 0; lv < P->levels; ++lv) {
-    PassArgs A{};
-    A.poly = poly;
-    A.poly_words = P->poly_words;
-    // column stride at level lv: mu_lv = 2M / (2m)^(lv+1)
-    A.log_mu = ilog2i(2LL * P->M) - P->logE * (lv + 1);
-    A.log_top_mu = P->log_top_mu;
-    A.base_pow = 1LL << (P->logE * lv);
-    A.twr = P->d_twr;
-    A.scale = 0;
-    A.total_cols = cols;
-    A.wpc = 1;
+  // ring products per level scale with the share of columns this launch covers
+  const double share = (double)cols / ((double)npoly * (1LL << P->log_top_mu));
+  for (int lv = lv_lo; lv < lv_hi; ++lv) {
+    PassArgs A = pass_args(P, g, poly, npoly, lv);
     if (lv == 0 && ops_a) {
       A.ops_a = ops_a;
       A.ops_b = ops_b;
@@ -288,24 +313,22 @@ int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s, c
       P->kt.fwd<<<grid, P->kt.nt, smem_pass(P), s>>>(A, P->mc);
     }
     CUCHK(cudaGetLastError());
-    mark(P, s, DKSS_K_FWD_PASS, rp_work(P, npoly * level_twiddles(P, lv)), 2LL * npoly * P->poly_words * 4);
+    mark(P, s, DKSS_K_FWD_PASS, (long long)(share * rp_work(P, npoly * level_twiddles(P, lv))),
+         2LL * cols * 2 * P->m * P->m * P->L * 4);
   }
   return 0;
 }
 
-int launch_inv_levels(dkss_plan* P, uint32_t* poly, int npoly, bool scale_last, cudaStream_t s) {
-  const long long cols = (long long)npoly << P->log_top_mu;
+int launch_inv_levels(dkss_plan* P, uint32_t* poly, int npoly, bool scale_last, cudaStream_t s, int lv_lo = 0,
+                      int lv_hi = -1, const Geom* geom = nullptr) {
+  const Geom g = geom ? *geom : full_geom(P);
+  if (lv_hi < 0) lv_hi = P->levels;
+  const long long cols = (long long)npoly << g.log_cpp;
   const int grid = (int)std::min<long long>((cols + P->kt.cols - 1) / P->kt.cols, P->grid_pass);
-  for (int lv = P->levels - 1; lv >= 0; --lv) {
-    PassArgs A{};
-    A.poly = poly;
-    A.poly_words = P->poly_words;
-    A.log_mu = ilog2i(2LL * P->M) - P->logE * (lv + 1);
-    A.log_top_mu = P->log_top_mu;
-    A.base_pow = 1LL << (P->logE * lv);
-    A.twr = P->d_twr;
+  const double share = (double)cols / ((double)npoly * (1LL << P->log_top_mu));
+  for (int lv = lv_hi - 1; lv >= lv_lo; --lv) {
+    PassArgs A = pass_args(P, g, poly, npoly, lv);
     A.scale = (lv == 0 && scale_last) ? 1 : 0;
-    A.total_cols = cols;
     const int kind = pass_kind(P, cols);
     if (kind == 3) {
       PassArgs B = A;
@@ -321,7 +344,8 @@ int launch_inv_levels(dkss_plan* P, uint32_t* poly, int npoly, bool scale_last, 
       P->kt.inv<<<grid, P->kt.nt, smem_pass(P), s>>>(A, P->mc);
     }
     CUCHK(cudaGetLastError());
-    mark(P, s, DKSS_K_INV_PASS, rp_work(P, npoly * level_twiddles(P, lv)), 2LL * npoly * P->poly_words * 4);
+    mark(P, s, DKSS_K_INV_PASS, (long long)(share * rp_work(P, npoly * level_twiddles(P, lv))),
+         2LL * cols * 2 * P->m * P->m * P->L * 4);
   }
   return 0;
 }
@@ -725,6 +749,116 @@ int dkss_mul(dkss_plan* P, const uint32_t* a, size_t na, const uint32_t* b, size
   memcpy(A.data(), a, na * 4);
   memcpy(B.data(), b, nb * 4);
   return dkss_mul_batch(P, 1, A.data(), B.data(), (size_t)P->op_limbs, c, nc);
+}
+
+// --- four-step split of one multiply over `world` ranks -------------
+// The first transform level is the reference's column step (bigmul/dkss.py:471-492): with
+// E = 2m and mu0 = 2M/E, rank r owns global columns [r*C, (r+1)*C), C = mu0/world, held as
+// [E][C] elements. Every deeper level and the bottom stay inside one of the E rows of mu0
+// elements (bigmul/dkss.py:493-495), so after one exchange rank h owns rows [h*R, (h+1)*R),
+// R = E/world, as [R][mu0]. The inverse walks the same split backwards.
+namespace {
+int fs_check(const dkss_plan* P, int rank, int world) {
+  if (!P) return fail(DKSS_EINVAL, "bad argument");
+  const long long E = 2LL * P->m, mu0 = 1LL << P->log_top_mu;
+  if (world < 1 || (world & (world - 1)) || world > E || mu0 % world)
+    return fail(DKSS_EINVAL, "world=%d must be a power of 2 dividing 2m=%lld and mu0=%lld", world, E, mu0);
+  if (rank < 0 || rank >= world) return fail(DKSS_EINVAL, "rank %d outside [0, %d)", rank, world);
+  if (P->levels < 1) return fail(DKSS_EINVAL, "plan has a single transform level; nothing to split");
+  return 0;
+}
+}  // namespace
+
+int dkss_fs_layout_get(const dkss_plan* P, int world, dkss_fs_layout* o) {
+  int rc;
+  if ((rc = fs_check(P, 0, world))) return rc;
+  if (!o) return fail(DKSS_EINVAL, "bad argument");
+  const long long mu0 = 1LL << P->log_top_mu;
+  o->cols = mu0 / world;
+  o->rows = 2LL * P->m / world;
+  o->elem_words = (long long)P->m * P->L;
+  o->block_words = P->poly_words / world;
+  return DKSS_OK;
+}
+
+int dkss_fs_columns_fwd(dkss_plan* P, int rank, int world, const uint32_t* a, const uint32_t* b, size_t nl,
+                        uint32_t* x, void* stream) {
+  int rc;
+  if ((rc = fs_check(P, rank, world))) return rc;
+  if (!a || !b || !x) return fail(DKSS_EINVAL, "bad argument");
+  if ((long long)nl > P->op_limbs) return fail(DKSS_ERANGE, "operand limbs %zu exceed plan (%lld)", nl, P->op_limbs);
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  const int logC = P->log_top_mu - ilog2i(world);
+  const Geom g{P->poly_words / world, logC, (long long)rank << logC, logC};
+  return launch_fwd_levels(P, x, 2, (cudaStream_t)stream, a, b, (long long)nl, 1, 0, 1, &g);
+}
+
+int dkss_fs_rows(dkss_plan* P, int world, uint32_t* z, void* stream) {
+  int rc;
+  if ((rc = fs_check(P, 0, world))) return rc;
+  if (!z) return fail(DKSS_EINVAL, "bad argument");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int rows = 2 * P->m / world;
+  const long long row_words = P->poly_words / (2LL * P->m);
+  const Geom g{row_words, P->log_top_mu - P->logE, 0, -1};
+  if ((rc = launch_fwd_levels(P, z, 2 * rows, s, nullptr, nullptr, 0, 0, 1, P->levels, &g))) return rc;
+  BottomArgs A{};
+  A.a = z;
+  A.b = z + (size_t)rows * row_words;
+  A.poly_words = row_words;
+  A.elems_per_poly = 1LL << P->log_top_mu;
+  A.logb = P->logb;
+  A.mode = 1;
+  A.scale = 0;
+  A.total_elems = (long long)rows << P->log_top_mu;
+  const int grid = (int)std::min<long long>((A.total_elems + P->kt.ne - 1) / P->kt.ne, P->grid_bot);
+  P->kt.bottom<<<grid, P->kt.nt, smem_two(P), s>>>(A, P->mc);
+  CUCHK(cudaGetLastError());
+  mark(P, s, DKSS_K_BOTTOM, rp_work(P, A.total_elems), 3LL * A.total_elems * P->m * P->L * 4);
+  return launch_inv_levels(P, z, rows, false, s, 1, P->levels, &g);
+}
+
+int dkss_fs_columns_inv(dkss_plan* P, int rank, int world, uint32_t* x, void* stream) {
+  int rc;
+  if ((rc = fs_check(P, rank, world))) return rc;
+  if (!x) return fail(DKSS_EINVAL, "bad argument");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  const int logC = P->log_top_mu - ilog2i(world);
+  const Geom g{P->poly_words / world, logC, (long long)rank << logC, logC};
+  return launch_inv_levels(P, x, 1, true, (cudaStream_t)stream, 0, 1, &g);
+}
+
+int dkss_block_transpose(dkss_plan* P, const uint32_t* src, uint32_t* dst, int n, int A, int B, int64_t run_words,
+                         void* stream) {
+  if (!P || !src || !dst || n < 1 || A < 1 || B < 1 || run_words < 4 || (run_words & 3) || src == dst)
+    return fail(DKSS_EINVAL, "bad argument");
+  if (((uintptr_t)src | (uintptr_t)dst) & 15) return fail(DKSS_EINVAL, "buffers must be 16-byte aligned");
+  if ((long long)n * A * B > 65535) return fail(DKSS_EINVAL, "too many blocks");
+  CUCHK(cudaSetDevice(P->device));
+  const long long run = run_words / 4;
+  const int gx = (int)std::max<long long>(1, std::min<long long>((run + 255) / 256, std::max(1, 1184 / (n * A * B))));
+  k_block_transpose<<<dim3(gx, n * A * B), 256, 0, (cudaStream_t)stream>>>((const uint4*)src, (uint4*)dst, A, B, run);
+  CUCHK(cudaGetLastError());
+  mark(P, (cudaStream_t)stream, DKSS_K_TRANSPOSE, 0, 2LL * n * A * B * run_words * 4);
+  return DKSS_OK;
+}
+
+int dkss_decode_device(dkss_plan* P, const uint32_t* v, uint32_t* out, size_t nc, void* stream) {
+  if (!P || !v || !out) return fail(DKSS_EINVAL, "bad argument");
+  if ((long long)nc < P->prod_limbs) return fail(DKSS_EINVAL, "nc=%zu below product limbs %lld", nc, P->prod_limbs);
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  int rc;
+  if ((rc = ensure_ws(P, 1))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if ((rc = launch_decode(P, v, out, 1, s))) return rc;
+  if ((long long)nc > P->prod_limbs)
+    CUCHK(cudaMemsetAsync(out + P->prod_limbs, 0, ((long long)nc - P->prod_limbs) * 4, s));
+  return DKSS_OK;
 }
 
 int dkss_encode_host(dkss_plan* P, const uint32_t* a, size_t na, uint32_t* poly) {

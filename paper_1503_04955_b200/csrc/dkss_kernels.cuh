@@ -331,7 +331,10 @@ struct PassArgs {
   uint32_t* poly;        // first polynomial of the launch
   long long poly_words;  // 2M * MM * L
   int log_mu;            // column stride mu = 2^log_mu (elements)
-  int log_top_mu;        // log2(M/m)
+  int log_top_mu;        // log2(M/m): twiddle exponents are split at this bit (alpha shift | row)
+  int log_cpp;           // log2 columns per polynomial in this launch's layout (log_top_mu unless sharded)
+  long long l_off;       // global column offset of local column 0 (sharded first level; else 0)
+  int log_mu_enc;        // fused encode: log2 of the global column count mu_0 (operand position stride)
   long long base_pow;    // (2m)^level
   const uint32_t* twr;   // [M/m][2MM][L]: rho~_s = rho^s R mod p, then W_s (see ring_mul)
   int scale;             // inverse pass: multiply outputs by mc.kscale
@@ -356,9 +359,9 @@ struct Geo {
 // element j of launch column cg: global word offset, and the column index l in its row
 __device__ __forceinline__ long long col_elem(const PassArgs& A, long long cg, int j, int loge, int elem_words,
                                               long long* l_out) {
-  const long long poly = cg >> A.log_top_mu, cc = cg & ((1LL << A.log_top_mu) - 1);
+  const long long poly = cg >> A.log_cpp, cc = cg & ((1LL << A.log_cpp) - 1);
   const long long inst = cc >> A.log_mu, l = cc & ((1LL << A.log_mu) - 1);
-  *l_out = l;
+  *l_out = l + A.l_off;
   return poly * A.poly_words + ((inst << (A.log_mu + loge)) + ((long long)j << A.log_mu) + l) * elem_words;
 }
 
@@ -436,9 +439,9 @@ __device__ __forceinline__ void cta_encode_tile(const PassArgs& A, long long til
 #pragma unroll
     for (int q = 0; q < L; ++q) out[q] = 0;
     if (cg < A.total_cols && k < HALF) {
-      const long long q = cg >> A.log_top_mu, cc = cg & ((1LL << A.log_top_mu) - 1);
+      const long long q = cg >> A.log_cpp, cc = cg & ((1LL << A.log_cpp) - 1);
       const long long inst = cc >> A.log_mu, l = cc & ((1LL << A.log_mu) - 1);
-      const long long pos = (inst << (A.log_mu + LOGE)) + ((long long)j << A.log_mu) + l;
+      const long long pos = (inst << (A.log_mu_enc + LOGE)) + ((long long)j << A.log_mu_enc) + l + A.l_off;
       if (pos < A.M) {
         const uint32_t* op = q < A.enc_split ? A.ops_a + q * A.na : A.ops_b + (q - A.enc_split) * A.na;
         const long long bit = (long long)A.u * (pos * HALF + k);
@@ -1070,6 +1073,20 @@ __global__ void __launch_bounds__(kDecThreads) k_decode2(DecodeArgs A) {
   const unsigned long long carries = (a + b + s_wcin[warp]) ^ a ^ b;
   const unsigned c = (unsigned)((carries >> lane) & 1ull);
   A.out[(long long)pidx * A.nout + t] += c;
+}
+
+// ---------------------------------------------------------------------------
+// block transpose for the four-step exchange: src [n][A][B][run] -> dst [n][B][A][run]
+// (run = contiguous uint4 per block); blockIdx.y walks the (n, a, b) blocks of src
+__global__ void k_block_transpose(const uint4* __restrict__ src, uint4* __restrict__ dst, int A, int B,
+                                  long long run) {
+  const int blk = blockIdx.y;
+  const int b = blk % B, t = blk / B;
+  const int a = t % A, n = t / A;
+  const uint4* s = src + (long long)blk * run;
+  uint4* d = dst + (((long long)n * B + b) * A + a) * run;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < run; i += (long long)gridDim.x * blockDim.x)
+    d[i] = s[i];
 }
 
 #endif  // DKSS_COMMON_KERNELS

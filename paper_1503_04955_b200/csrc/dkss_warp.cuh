@@ -109,9 +109,9 @@ __device__ __forceinline__ void encode_coef(const PassArgs& A, long long cg, int
 #pragma unroll
   for (int q = 0; q < L; ++q) out[q] = 0;
   if (k >= HALF) return;
-  const long long qp = cg >> A.log_top_mu, cc = cg & ((1LL << A.log_top_mu) - 1);
+  const long long qp = cg >> A.log_cpp, cc = cg & ((1LL << A.log_cpp) - 1);
   const long long inst = cc >> A.log_mu, l = cc & ((1LL << A.log_mu) - 1);
-  const long long pos = (inst << (A.log_mu + LOGE)) + ((long long)j << A.log_mu) + l;
+  const long long pos = (inst << (A.log_mu_enc + LOGE)) + ((long long)j << A.log_mu_enc) + l + A.l_off;
   if (pos >= A.M) return;
   const uint32_t* op = qp < A.enc_split ? A.ops_a + qp * A.na : A.ops_b + (qp - A.enc_split) * A.na;
   const long long bit = (long long)A.u * (pos * HALF + k);

@@ -1,0 +1,128 @@
+"""Four-step split of one multiply: the host orchestration's data movement.
+
+The device stages are replaced by a stand-in that tags every element with (polynomial,
+global element index) and asserts, at every phase, that each element sits where the
+layout of include/dkss.h says it must: columns [E][C] per rank, rows [R][mu0] after the
+exchange, columns again after the way back, [E][mu0] after the gather.  Runs with the
+emulated ranks in one process and over gloo with world size 2 (CPU).  The device stages
+themselves are checked against a*b in tests/test_gpu_parity.py.
+"""
+import os
+import socket
+
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from paper_1503_04955_b200.fourstep import DistExchange, FourStepRank, run_rank, run_virtual
+
+M, MM, LL = 64, 4, 2  # toy geometry: E = 8, mu0 = 16, element = 8 words
+E, MU0, EW = 2 * MM, 2 * M // (2 * MM), MM * LL
+A_TAG, B_TAG, PROD_TAG, SCALED_TAG = 1, 2, 7, 9
+
+
+class TagStages:
+    def __init__(self):
+        self.calls = []
+
+    def layout(self, world):
+        return {"cols": MU0 // world, "rows": E // world, "elem_words": EW, "block_words": 2 * M * EW // world}
+
+    def columns_fwd(self, rank, world, a, b, x):
+        C = MU0 // world
+        v = x.view(2, E, C, EW)
+        v.zero_()
+        for q, tag in enumerate((A_TAG, B_TAG)):
+            v[q, :, :, 0] = tag
+            j = torch.arange(E).view(E, 1)
+            c = torch.arange(C).view(1, C)
+            v[q, :, :, 1] = (j * MU0 + rank * C + c).to(torch.int32)
+        self.calls.append("columns_fwd")
+
+    def rows(self, rank, world, z):
+        R = E // world
+        v = z.view(2, R, MU0, EW)
+        want = (torch.arange(R).view(R, 1) + rank * R) * MU0 + torch.arange(MU0).view(1, MU0)
+        for q, tag in enumerate((A_TAG, B_TAG)):
+            assert bool((v[q, :, :, 0] == tag).all()), "row phase got elements of the wrong polynomial"
+            assert torch.equal(v[q, :, :, 1], want.to(torch.int32)), "row phase got misplaced elements"
+        v[0, :, :, 0] = PROD_TAG
+        self.calls.append("rows")
+
+    def columns_inv(self, rank, world, x):
+        C = MU0 // world
+        v = x.view(E, C, EW)
+        want = torch.arange(E).view(E, 1) * MU0 + rank * C + torch.arange(C).view(1, C)
+        assert bool((v[:, :, 0] == PROD_TAG).all())
+        assert torch.equal(v[:, :, 1], want.to(torch.int32))
+        v[:, :, 0] = SCALED_TAG
+        self.calls.append("columns_inv")
+
+    def block_transpose(self, src, dst, n, A, B, run_words):
+        dst.view(n, B, A, run_words).copy_(src.view(n, A, B, run_words).transpose(1, 2))
+
+    def decode(self, v, out):
+        w = v.view(2 * M, EW)
+        assert bool((w[:, 0] == SCALED_TAG).all())
+        assert torch.equal(w[:, 1], torch.arange(2 * M, dtype=torch.int32))
+        out.fill_(1)
+        self.calls.append("decode")
+
+
+def _ranks(world):
+    st = TagStages()
+    return st, [FourStepRank(st, r, world, M, MM, torch.device("cpu"), 4) for r in range(world)]
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_virtual_ranks_move_every_element(world):
+    st, ranks = _ranks(world)
+    a = torch.zeros(4, dtype=torch.int32)
+    out = run_virtual(ranks, a, a)
+    assert out.tolist() == [1, 1, 1, 1]
+    assert st.calls.count("columns_fwd") == world and st.calls.count("rows") == world
+    assert st.calls.count("columns_inv") == world and st.calls[-1] == "decode"
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        st = TagStages()
+        fs = FourStepRank(st, rank, world, M, MM, torch.device("cpu"), 4)
+        a = torch.zeros(4, dtype=torch.int32)
+        out = run_rank(fs, DistExchange(), a, a)
+        q.put((rank, None if out is None else out.tolist(), st.calls, None))
+    except Exception as e:  # report, do not hang the peer
+        q.put((rank, None, [], repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+def test_two_rank_gloo_fourstep_exchange():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=150) for _ in procs)
+    for p in procs:
+        p.join(timeout=30)
+    for rank, out, calls, err in res:
+        assert err is None, f"rank {rank}: {err}"
+        assert calls[:3] == ["columns_fwd", "rows", "columns_inv"]
+    assert res[0][1] == [1, 1, 1, 1] and res[0][2][-1] == "decode"
+    assert res[1][1] is None

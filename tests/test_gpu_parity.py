@@ -211,3 +211,44 @@ def test_dmul_2_26_residues(cuda_ok):
             primes.append(q)
     for q in primes:
         assert c % q == (a % q) * (b % q) % q
+
+
+# --- four-step split of one multiply, G ranks emulated on one GPU ---------
+@pytest.mark.parametrize("e,world", [(16, 2), (16, 16), (18, 4), (20, 2), (20, 8), (20, 32)])
+def test_fourstep_virtual_ranks(cuda_ok, e, world):
+    from paper_1503_04955_b200.fourstep import dmul_fourstep_virtual
+
+    rng = random.Random(100 + e + world)
+    N = 1 << e
+    a = rng.getrandbits(N) | 1 << (N - 1)
+    b = rng.getrandbits(N) | 1 << (N - 1)
+    assert dmul_fourstep_virtual(a, b, world) == a * b
+
+
+def test_fourstep_virtual_all_ones(cuda_ok):
+    from paper_1503_04955_b200.fourstep import dmul_fourstep_virtual
+
+    N = 1 << 20
+    a = (1 << N) - 1
+    assert dmul_fourstep_virtual(a, a, 4) == a * a
+
+
+def test_fourstep_virtual_2_24_matches_single_gpu(cuda_ok):
+    from paper_1503_04955_b200.fourstep import dmul_fourstep_virtual
+
+    rng = random.Random(4)
+    N = 1 << 24
+    a = rng.getrandbits(N) | 1 << (N - 1)
+    b = rng.getrandbits(N) | 1 << (N - 1)
+    c = dmul_fourstep_virtual(a, b, 8)
+    assert c == dmul(a, b).to_int()
+    for q in (2**61 - 1, 2**62 - 57):
+        assert c % q == (a % q) * (b % q) % q
+
+
+def test_fourstep_rejects_bad_world(cuda_ok):
+    pl = P.dkss_select_params(1 << 20)
+    dp = device_plan(pl)
+    for world in (3, 64, 0):
+        with pytest.raises(ValueError):
+            dp.fs_layout(world)
