@@ -73,6 +73,16 @@ int dkss_version(void);
  * fails with DKSS_ERANGE if the product does not fit nc limbs. */
 int dkss_mul(dkss_plan* plan, const uint32_t* a, size_t na, const uint32_t* b, size_t nb, uint32_t* c, size_t nc);
 
+/* dmul with operands given as little-endian radix-2^digit_bits digit strings, one digit
+ * per uint32 (8 <= digit_bits <= 32) -- e.g. the 30-bit digits of a CPython int, so the
+ * host does no radix conversion (the device repacks them to 32-bit limbs).  The product
+ * is written as nc 32-bit limbs, as dkss_mul. */
+int dkss_mul_digits(dkss_plan* plan, const uint32_t* a, size_t na, const uint32_t* b, size_t nb, int digit_bits,
+                    uint32_t* c, size_t nc);
+/* batched form: pair i is a[i] (na[i] digits) x b[i] (nb[i] digits); c is batch x nc limbs */
+int dkss_mul_batch_digits(dkss_plan* plan, int batch, const uint32_t* const* a, const size_t* na,
+                          const uint32_t* const* b, const size_t* nb, int digit_bits, uint32_t* c, size_t nc);
+
 /* batched independent products sharing one plan (config 3): a, b are batch x n_limbs,
  * c is batch x nc.  Host buffers. */
 int dkss_mul_batch(dkss_plan* plan, int batch, const uint32_t* a, const uint32_t* b, size_t n_limbs, uint32_t* c,

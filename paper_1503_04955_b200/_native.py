@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(HERE, "_lib", "libdkss.so")
 # every symbol include/dkss.h declares (checked by tests/test_native_abi.py)
 EXPORTS = (
     "dkss_plan_create", "dkss_plan_destroy", "dkss_plan_get_info", "dkss_last_error", "dkss_version",
-    "dkss_mul", "dkss_mul_batch", "dkss_mul_device", "dkss_profile_device",
+    "dkss_mul", "dkss_mul_digits", "dkss_mul_batch_digits", "dkss_mul_batch", "dkss_mul_device", "dkss_profile_device",
     "dkss_encode_host", "dkss_fft_host", "dkss_rmul_host", "dkss_decode_host",
     "dkss_fs_layout_get", "dkss_fs_columns_fwd", "dkss_fs_rows", "dkss_fs_columns_inv",
     "dkss_block_transpose", "dkss_decode_device",
@@ -83,6 +83,11 @@ def load(path: str = LIB_PATH):
         L.dkss_plan_get_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]
         L.dkss_last_error.restype = ctypes.c_char_p
         L.dkss_mul.argtypes = [vp, _u32p, ctypes.c_size_t, _u32p, ctypes.c_size_t, _u32p, ctypes.c_size_t]
+        L.dkss_mul_digits.argtypes = [vp, vp, ctypes.c_size_t, vp, ctypes.c_size_t, ctypes.c_int, _u32p,
+                                      ctypes.c_size_t]
+        L.dkss_mul_batch_digits.argtypes = [vp, ctypes.c_int, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t),
+                                            ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t), ctypes.c_int, _u32p,
+                                            ctypes.c_size_t]
         L.dkss_mul_batch.argtypes = [vp, ctypes.c_int, _u32p, _u32p, ctypes.c_size_t, _u32p, ctypes.c_size_t]
         L.dkss_mul_device.argtypes = [vp, ctypes.c_int, vp, vp, ctypes.c_size_t, vp, ctypes.c_size_t, vp]
         L.dkss_profile_device.argtypes = [vp, ctypes.c_int, vp, vp, ctypes.c_size_t, vp, vp, ctypes.c_int,
@@ -161,6 +166,24 @@ class DevicePlan:
     def mul_limbs(self, a: np.ndarray, b: np.ndarray, nc: int) -> np.ndarray:
         out = np.zeros(nc, dtype=np.uint32)
         _check(self._lib.dkss_mul(self._h, _ptr(a), a.size, _ptr(b), b.size, _ptr(out), nc))
+        return out
+
+    def mul_digits(self, a_ptr: int, na: int, b_ptr: int, nb: int, digit_bits: int, nc: int) -> np.ndarray:
+        """Product of two radix-2^digit_bits digit strings at host addresses a_ptr / b_ptr."""
+        out = np.empty(nc, dtype=np.uint32)
+        _check(self._lib.dkss_mul_digits(self._h, ctypes.c_void_p(a_ptr), na, ctypes.c_void_p(b_ptr), nb, digit_bits,
+                                         _ptr(out), nc))
+        return out
+
+    def mul_batch_digits(self, a_ptrs, na, b_ptrs, nb, digit_bits: int, nc: int) -> np.ndarray:
+        """Products of pairs of radix-2^digit_bits digit strings (host addresses + counts)."""
+        batch = len(a_ptrs)
+        vpa = (ctypes.c_void_p * batch)(*a_ptrs)
+        vpb = (ctypes.c_void_p * batch)(*b_ptrs)
+        cna = (ctypes.c_size_t * batch)(*na)
+        cnb = (ctypes.c_size_t * batch)(*nb)
+        out = np.empty((batch, nc), dtype=np.uint32)
+        _check(self._lib.dkss_mul_batch_digits(self._h, batch, vpa, cna, vpb, cnb, digit_bits, _ptr(out), nc))
         return out
 
     def mul_batch(self, a: np.ndarray, b: np.ndarray, nc: int | None = None) -> np.ndarray:

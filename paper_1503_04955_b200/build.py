@@ -69,7 +69,7 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -
             list(ex.map(compile_one, todo))
     objs = [u[0] for u in _units()]
     if force or todo or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")

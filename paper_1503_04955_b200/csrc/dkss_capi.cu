@@ -9,6 +9,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -136,6 +137,8 @@ struct dkss_plan {
   uint32_t* d_pmask = nullptr;
   uint32_t* d_bstat = nullptr;
   uint32_t* h_pin = nullptr;   // pinned staging
+  uint32_t* d_stage = nullptr; // device copy of radix-2^k operand digits (dkss_mul_digits)
+  size_t stage_words = 0;
   size_t h_pin_words = 0;
   size_t ws_bytes = 0;
   cudaStream_t stream = nullptr;
@@ -593,6 +596,7 @@ void dkss_plan_destroy(dkss_plan* P) {
   cudaFree(P->d_tw);
   cudaFree(P->d_twr);
   if (P->h_pin) cudaFreeHost(P->h_pin);
+  cudaFree(P->d_stage);
   if (P->stream) cudaStreamDestroy(P->stream);
   delete P;
 }
@@ -731,6 +735,141 @@ int dkss_mul_batch(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b
     if (nc > ncopy) memset(dst + ncopy, 0, (nc - ncopy) * 4);
   }
   return DKSS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// fn(i) for i in [0, n), spread over up to 8 host threads when `bytes` of copying is large
+template <class F>
+void host_par(size_t n, size_t bytes, F fn) {
+  unsigned nt = bytes >= (8u << 20) ? std::min(8u, std::max(1u, std::thread::hardware_concurrency())) : 1u;
+  nt = (unsigned)std::min<size_t>(nt, n);
+  if (nt <= 1) {
+    for (size_t i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      for (size_t i = t; i < n; i += nt) fn(i);
+    });
+  for (auto& x : th) x.join();
+}
+
+// validate `nops` digit strings, pack them (offsets, then digits) into pinned staging, copy
+// to the device and repack into 32-bit limbs at d_ops (operand q at d_ops + q*op_limbs)
+int stage_digits(dkss_plan* P, int nops, const uint32_t* const* ptrs, const size_t* counts, int digit_bits,
+                 cudaStream_t s) {
+  std::vector<size_t> nd(nops);
+  size_t total = 0;
+  for (int q = 0; q < nops; ++q) {
+    const uint32_t* d = ptrs[q];
+    size_t n = counts[q];
+    if (n && !d) return fail(DKSS_EINVAL, "null digit pointer");
+    while (n > 0 && d[n - 1] == 0) --n;
+    if (digit_bits < 32) {
+      uint32_t any = 0;
+      for (size_t i = 0; i < n; ++i) any |= d[i];
+      if (any >> digit_bits) return fail(DKSS_EINVAL, "a digit exceeds %d bits", digit_bits);
+    }
+    if (n) {  // value < 2^N (bigmul/dkss.py:389-390)
+      const long long bits = (long long)(n - 1) * digit_bits + (32 - __builtin_clz(d[n - 1]));
+      if (bits > P->N) return fail(DKSS_ERANGE, "operand does not fit the plan (%lld bits > N=%lld)", bits, P->N);
+    }
+    nd[q] = n;
+    total += n;
+  }
+  const size_t head = 2 * (size_t)(nops + 1);  // long long offsets, in u32 words
+  const size_t words = head + total;
+  int rc;
+  if ((rc = ensure_pin(P, words))) return rc;
+  if (words > P->stage_words) {
+    cudaFree(P->d_stage);
+    P->d_stage = nullptr;
+    CUCHK(cudaMalloc(&P->d_stage, words * 4));
+    P->stage_words = words;
+  }
+  long long* off = reinterpret_cast<long long*>(P->h_pin);
+  uint32_t* dig = P->h_pin + head;
+  long long o = 0;
+  for (int q = 0; q < nops; ++q) {
+    off[q] = o;
+    o += (long long)nd[q];
+  }
+  off[nops] = o;
+  host_par((size_t)nops, total * 4, [&](size_t q) {
+    if (nd[q]) memcpy(dig + off[q], ptrs[q], nd[q] * 4);
+  });
+  CUCHK(cudaMemcpyAsync(P->d_stage, P->h_pin, words * 4, cudaMemcpyHostToDevice, s));
+  RepackArgs R{};
+  R.stage = P->d_stage + head;
+  R.off = reinterpret_cast<const long long*>(P->d_stage);
+  R.dst = P->d_ops;
+  R.ndst = P->op_limbs;
+  R.sbits = digit_bits;
+  const int gx = (int)std::max<long long>(1, std::min<long long>((P->op_limbs + 255) / 256, 1184 / nops + 1));
+  k_repack_bits<<<dim3(gx, nops), 256, 0, s>>>(R);
+  CUCHK(cudaGetLastError());
+  return 0;
+}
+
+// products of `batch` staged operand pairs (d_ops) -> host c (batch x nc limbs)
+int run_staged(dkss_plan* P, int batch, uint32_t* c, size_t nc, cudaStream_t s) {
+  int rc;
+  const size_t prw = (size_t)batch * P->prod_limbs;
+  if ((rc = launch_graph(P, batch, P->d_ops, P->d_ops + (size_t)batch * P->op_limbs, (size_t)P->op_limbs, P->d_prod,
+                         P->prod_limbs, s)))
+    return rc;
+  if ((rc = ensure_pin(P, prw))) return rc;
+  CUCHK(cudaMemcpyAsync(P->h_pin, P->d_prod, prw * 4, cudaMemcpyDeviceToHost, s));
+  CUCHK(cudaStreamSynchronize(s));
+  const size_t ncopy = std::min<size_t>(nc, P->prod_limbs);
+  std::vector<char> over((size_t)batch, 0);
+  host_par((size_t)batch, prw * 4, [&](size_t i) {
+    const uint32_t* src = P->h_pin + i * P->prod_limbs;
+    uint32_t* dst = c + i * nc;
+    memcpy(dst, src, ncopy * 4);
+    for (size_t k = ncopy; k < (size_t)P->prod_limbs; ++k)
+      if (src[k]) over[i] = 1;
+    if (nc > ncopy) memset(dst + ncopy, 0, (nc - ncopy) * 4);
+  });
+  for (int i = 0; i < batch; ++i)
+    if (over[i]) return fail(DKSS_ERANGE, "product %d does not fit nc=%zu limbs", i, nc);
+  return DKSS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int dkss_mul_batch_digits(dkss_plan* P, int batch, const uint32_t* const* a, const size_t* na,
+                          const uint32_t* const* b, const size_t* nb, int digit_bits, uint32_t* c, size_t nc) {
+  if (!P || batch < 1 || !a || !na || !b || !nb || !c) return fail(DKSS_EINVAL, "bad argument");
+  if (digit_bits < 8 || digit_bits > 32) return fail(DKSS_EINVAL, "digit_bits=%d outside [8, 32]", digit_bits);
+  if (2LL * batch > 65535) return fail(DKSS_EINVAL, "batch %d too large", batch);
+  std::vector<const uint32_t*> ptrs(2 * (size_t)batch);
+  std::vector<size_t> counts(2 * (size_t)batch);
+  for (int i = 0; i < batch; ++i) {
+    ptrs[i] = a[i];
+    counts[i] = na[i];
+    ptrs[batch + i] = b[i];
+    counts[batch + i] = nb[i];
+  }
+  size_t total = 2 * (2 * (size_t)batch + 1);
+  for (size_t q = 0; q < counts.size(); ++q) total += counts[q];
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  int rc;
+  if ((rc = ensure_ws(P, batch))) return rc;
+  // staging sized once for both directions: it must not be reallocated while a copy is in flight
+  if ((rc = ensure_pin(P, std::max<size_t>(total, (size_t)batch * (size_t)P->prod_limbs)))) return rc;
+  if ((rc = stage_digits(P, 2 * batch, ptrs.data(), counts.data(), digit_bits, P->stream))) return rc;
+  return run_staged(P, batch, c, nc, P->stream);
+}
+
+int dkss_mul_digits(dkss_plan* P, const uint32_t* a, size_t na, const uint32_t* b, size_t nb, int digit_bits,
+                    uint32_t* c, size_t nc) {
+  return dkss_mul_batch_digits(P, 1, &a, &na, &b, &nb, digit_bits, c, nc);
 }
 
 int dkss_mul(dkss_plan* P, const uint32_t* a, size_t na, const uint32_t* b, size_t nb, uint32_t* c, size_t nc) {

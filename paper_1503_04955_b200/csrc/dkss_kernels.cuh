@@ -1089,6 +1089,43 @@ __global__ void k_block_transpose(const uint4* __restrict__ src, uint4* __restri
     d[i] = s[i];
 }
 
+// ---------------------------------------------------------------------------
+// radix change of little-endian digit strings: `sbits`-bit digits (stored one per u32,
+// 8 <= sbits <= 32; e.g. CPython's 30-bit int digits) -> 32-bit limbs.  Operand q
+// (blockIdx.y) is digits [off[q], off[q+1]) of `stage` and becomes limbs
+// dst[q*ndst, (q+1)*ndst); limb i holds bits [32i, 32i+32), gathered from at most five
+// consecutive digits.
+struct RepackArgs {
+  const uint32_t* stage;
+  const long long* off;
+  uint32_t* dst;
+  long long ndst;
+  int sbits;
+};
+
+__global__ void k_repack_bits(RepackArgs A) {
+  const int q = blockIdx.y;
+  const long long o0 = A.off[q], ns = A.off[q + 1] - o0;
+  const uint32_t* src = A.stage + o0;
+  uint32_t* dst = A.dst + (long long)q * A.ndst;
+  const uint64_t mask = A.sbits == 32 ? 0xFFFFFFFFull : ((1ull << A.sbits) - 1);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < A.ndst; i += (long long)gridDim.x * blockDim.x) {
+    const long long bit = 32 * i;
+    const long long d = bit / A.sbits;
+    const int o = (int)(bit - d * A.sbits);
+    uint64_t acc = 0;
+    int sh = -o;
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {
+      if (sh >= 32) break;
+      const uint64_t dig = (d + t < ns) ? (src[d + t] & mask) : 0;
+      acc |= sh >= 0 ? dig << sh : dig >> (-sh);
+      sh += A.sbits;
+    }
+    dst[i] = (uint32_t)acc;
+  }
+}
+
 #endif  // DKSS_COMMON_KERNELS
 
 }  // namespace dkss

@@ -26,7 +26,8 @@ import numpy as np
 
 from ._native import DevicePlan
 from .plan import DkssPlan, dkss_select_params, ring_products_per_multiply, twiddle_count
-from .words import (Natural, ScratchArena, as_natural, current_arena, int_to_u32, u32_to_int, word_bits)
+from .words import (Natural, ScratchArena, as_natural, current_arena, int_to_u32, pylong_digits, u32_to_int,
+                    word_bits, PYLONG_DIGIT_BITS)
 
 # The reference hands products below 2048 result bits to smul (bigmul/dkss.py:517,
 # 533-535); that rung is out of scope here, so such inputs run through DKSS on the GPU
@@ -169,6 +170,18 @@ def _as_int_len(x, w: int):
     return n.to_int(), len(n)
 
 
+def _digits(x, value: int):
+    """(keepalive, host address, digit count, digit bits) of an operand for dkss_mul_digits."""
+    if isinstance(x, Natural) and x._words is None and x._w == word_bits():
+        arr = np.ascontiguousarray(x._limbs, dtype=np.uint32)
+        return arr, arr.ctypes.data, arr.size, 32
+    d = pylong_digits(value)
+    if d is not None:
+        return value, d[0], d[1], PYLONG_DIGIT_BITS
+    arr = int_to_u32(value, max(1, -(-value.bit_length() // 32)))
+    return arr, arr.ctypes.data, arr.size, 32
+
+
 def dmul(a, b, thresholds=None, arena: ScratchArena | None = None) -> Natural:
     """Full product via DKSS on the GPU (bigmul/dkss.py:520-548)."""
     w = word_bits()
@@ -188,22 +201,42 @@ def dmul(a, b, thresholds=None, arena: ScratchArena | None = None) -> Natural:
     with arena.frame():
         # device workspace per multiply: 2 polynomials + operands + product, in words
         arena.alloc_words((2 * info["poly_bytes"] + 4 * (2 * nl + nc)) * 8 // w)
-        c = dp.mul_limbs(int_to_u32(ai, nl), int_to_u32(bi, nl), nc)
+        ka, pa, na, ba = _digits(a, ai)
+        kb, pb, nb, bb = _digits(b, bi)
+        if ba == bb:
+            c = dp.mul_digits(pa, na, pb, nb, ba, nc)
+        else:
+            c = dp.mul_limbs(int_to_u32(ai, nl), int_to_u32(bi, nl), nc)
+        del ka, kb
     plan.ks_calls += ring_products_per_multiply(plan)
     return Natural._from_u32(c, outlen, w)
 
 
 def dmul_many(pairs, thresholds=None) -> list:
-    """Independent products sharing one plan, batched in one device call (config 3)."""
+    """Independent products sharing one plan, batched in one device call (config 3).
+
+    Returns one Natural per pair, as dmul would (len(a) + len(b) words)."""
     pairs = list(pairs)
     if not pairs:
         return []
-    n_bits = max(max(int(a).bit_length(), int(b).bit_length()) for a, b in pairs)
-    N = max(n_bits, _MIN_PLAN_BITS)
-    plan = _plan_for(N, word_bits())
+    w = word_bits()
+    vals = [(_as_int_len(a, w), _as_int_len(b, w)) for a, b in pairs]
+    n_bits = max(max(ai.bit_length(), bi.bit_length()) for (ai, _), (bi, _) in vals)
+    plan = _plan_for(max(n_bits, _MIN_PLAN_BITS), w)
     dp = device_plan(plan)
     nl = dp.info["operand_limbs"]
-    A = np.stack([int_to_u32(int(a), nl) for a, _ in pairs])
-    B = np.stack([int_to_u32(int(b), nl) for _, b in pairs])
-    C = dp.mul_batch(A, B)
-    return [u32_to_int(row) for row in C]
+    lens = [max(1, la + lb) for (_, la), (_, lb) in vals]
+    nc = max(dp.info["product_limbs"], -(-max(lens) * w // 32))
+    da = [_digits(a, ai) for (a, _), ((ai, _), _) in zip(pairs, vals)]
+    db = [_digits(b, bi) for (_, b), (_, (bi, _)) in zip(pairs, vals)]
+    bits = {d[3] for d in da} | {d[3] for d in db}
+    if len(bits) == 1:
+        C = dp.mul_batch_digits([d[1] for d in da], [d[2] for d in da], [d[1] for d in db], [d[2] for d in db],
+                                bits.pop(), nc)
+    else:
+        A = np.stack([int_to_u32(ai, nl) for (ai, _), _ in vals])
+        B = np.stack([int_to_u32(bi, nl) for _, (bi, _) in vals])
+        C = dp.mul_batch(A, B, nc)
+    del da, db
+    plan.ks_calls += len(pairs) * ring_products_per_multiply(plan)
+    return [Natural._from_u32(C[i], lens[i], w) for i in range(len(pairs))]

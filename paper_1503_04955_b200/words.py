@@ -22,6 +22,8 @@ with ``int.to_bytes`` / ``numpy.frombuffer`` (no per-word Python loops).
 
 from __future__ import annotations
 
+import ctypes
+import sys
 import threading
 from contextlib import contextmanager
 
@@ -269,3 +271,46 @@ def int_to_u32(value: int, nlimbs: int) -> np.ndarray:
 
 def u32_to_int(limbs) -> int:
     return int.from_bytes(np.ascontiguousarray(limbs, dtype=np.uint32).tobytes(), "little")
+
+
+# ---------------------------------------------------------------------------
+# zero-copy view of a CPython int's digits (CPython >= 3.12 object layout: PyObject header,
+# then uintptr lv_tag = ndigits << 3 | sign, then the 30-bit digits, one per uint32).  The
+# multiply hands these digits to the C ABI as they are (dkss_mul_digits) instead of
+# converting the int with to_bytes, which is a byte-at-a-time loop in CPython.
+
+def _raw_digits(x: int):
+    tag = ctypes.c_size_t.from_address(id(x) + 16).value
+    return id(x) + 24, tag >> 3, tag & 3
+
+
+def _layout_ok() -> bool:
+    if sys.implementation.name != "cpython" or sys.version_info < (3, 12):
+        return False
+    if sys.int_info.bits_per_digit != 30 or sys.int_info.sizeof_digit != 4:
+        return False
+    try:
+        x = (7 << 60) | (3 << 30) | 5
+        addr, nd, sign = _raw_digits(x)
+        if (nd, sign) != (3, 0) or list((ctypes.c_uint32 * 3).from_address(addr)) != [5, 3, 7]:
+            return False
+        addr, nd, sign = _raw_digits(-x)
+        return (nd, sign) == (3, 2)
+    except Exception:  # noqa: BLE001
+        return False
+
+
+PYLONG_DIGIT_BITS = 30
+_PYLONG_OK = _layout_ok()
+
+
+def pylong_digits(x: int):
+    """(address, digit count) of the 30-bit digits of a nonnegative int, or None when the
+    interpreter's int layout is not the one checked above.  The int must stay alive while
+    the address is used."""
+    if not _PYLONG_OK or type(x) is not int:
+        return None
+    addr, nd, sign = _raw_digits(x)
+    if sign == 2:
+        raise ValueError("Natural is nonnegative")
+    return addr, (0 if sign == 1 else nd)

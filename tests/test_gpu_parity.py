@@ -252,3 +252,31 @@ def test_fourstep_rejects_bad_world(cuda_ok):
     for world in (3, 64, 0):
         with pytest.raises(ValueError):
             dp.fs_layout(world)
+
+
+@pytest.mark.parametrize("digit_bits", [8, 13, 16, 30, 32])
+def test_mul_digits_radix(cuda_ok, digit_bits):
+    # dkss_mul_digits: operands as radix-2^k digit strings (k = 30 is CPython's int digit)
+    rng = random.Random(digit_bits)
+    pl = P.dkss_select_params(1 << 16)
+    dp = device_plan(pl)
+    a, b = rng.getrandbits(1 << 16), rng.getrandbits((1 << 16) - 77)
+    mask = (1 << digit_bits) - 1
+    da = np.array([(a >> (digit_bits * i)) & mask for i in range(-(-a.bit_length() // digit_bits) + 3)], np.uint32)
+    db = np.array([(b >> (digit_bits * i)) & mask for i in range(-(-b.bit_length() // digit_bits))], np.uint32)
+    c = dp.mul_digits(da.ctypes.data, da.size, db.ctypes.data, db.size, digit_bits, dp.info["product_limbs"])
+    assert u32_to_int(c) == a * b
+    if digit_bits < 32:
+        bad = da.copy()
+        bad[0] = 1 << digit_bits
+        with pytest.raises(ValueError):
+            dp.mul_digits(bad.ctypes.data, bad.size, db.ctypes.data, db.size, digit_bits, dp.info["product_limbs"])
+
+
+def test_dmul_chain_natural_operands(cuda_ok, rng):
+    # a lazy Natural product fed back as an operand takes the 32-bit limb route
+    a, b, c = rng.getrandbits(20000), rng.getrandbits(30000), rng.getrandbits(50000)
+    ab = dmul(a, b)
+    abc = dmul(ab, c)
+    assert abc.to_int() == a * b * c and len(abc) == len(ab) + -(-c.bit_length() // 64)
+    assert dmul(c, Natural.from_int(a)).to_int() == a * c
