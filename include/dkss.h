@@ -90,7 +90,8 @@ int dkss_mul_batch(dkss_plan* plan, int batch, const uint32_t* a, const uint32_t
 
 /* device-resident variant: a_dev, b_dev, c_dev are device pointers with the same shapes,
  * `stream` is a cudaStream_t (NULL = legacy default stream).  Stream-ordered; replays a
- * cached CUDA graph per (pointers, batch, sizes). */
+ * cached CUDA graph per (pointers, batch, sizes).  b_dev == NULL squares a (one forward
+ * transform instead of two). */
 int dkss_mul_device(dkss_plan* plan, int batch, const uint32_t* a_dev, const uint32_t* b_dev, size_t n_limbs,
                     uint32_t* c_dev, size_t nc, void* stream);
 
@@ -143,6 +144,12 @@ int dkss_block_transpose(dkss_plan* plan, const uint32_t* src_dev, uint32_t* dst
 /* dkss_decode (bigmul/dkss.py:498-513) on the device: v = the scaled inverse transform as
  * left by the device pipeline (full [E][mu0] layout); nc >= product_limbs limbs written */
 int dkss_decode_device(dkss_plan* plan, const uint32_t* v_dev, uint32_t* out_dev, size_t nc, void* stream);
+
+/* Lucas-Lehmer iterations (bigmul/bench.py:197-217) on the device: `iters` times
+ * s <- (s^2 - 2) mod (2^p - 1), canonical in [0, 2^p - 1) (mersenne_reduce, :187-194),
+ * each square through the DKSS pipeline in squaring mode.  s: host, ns >= ceil(p/32) limbs,
+ * in and out; requires 2 <= p <= N of the plan. */
+int dkss_lucas_lehmer(dkss_plan* plan, int64_t p, int64_t iters, uint32_t* s, size_t ns);
 
 /* stage entry points for parity checks (host buffers) ------------------------------ */
 /* dkss_encode, bigmul/dkss.py:381-398: poly = uint32[2M][m][L] */

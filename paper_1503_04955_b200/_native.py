@@ -15,7 +15,7 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libdkss.so")
+LIB_PATH = os.environ.get("DKSS_LIB") or os.path.join(HERE, "_lib", "libdkss.so")
 
 # every symbol include/dkss.h declares (checked by tests/test_native_abi.py)
 EXPORTS = (
@@ -23,7 +23,7 @@ EXPORTS = (
     "dkss_mul", "dkss_mul_digits", "dkss_mul_batch_digits", "dkss_mul_batch", "dkss_mul_device", "dkss_profile_device",
     "dkss_encode_host", "dkss_fft_host", "dkss_rmul_host", "dkss_decode_host",
     "dkss_fs_layout_get", "dkss_fs_columns_fwd", "dkss_fs_rows", "dkss_fs_columns_inv",
-    "dkss_block_transpose", "dkss_decode_device",
+    "dkss_block_transpose", "dkss_decode_device", "dkss_lucas_lehmer",
 )
 
 DKSS_OK, DKSS_EINVAL, DKSS_ECUDA, DKSS_ERANGE, DKSS_ENOMEM = 0, -1, -2, -3, -4
@@ -104,6 +104,7 @@ def load(path: str = LIB_PATH):
         L.dkss_fs_columns_inv.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp]
         L.dkss_block_transpose.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, vp]
         L.dkss_decode_device.argtypes = [vp, vp, vp, ctypes.c_size_t, vp]
+        L.dkss_lucas_lehmer.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, _u32p, ctypes.c_size_t]
         for name in EXPORTS:
             if not hasattr(L, name):
                 raise NativeUnavailable(f"{path} lacks symbol {name}")
@@ -264,3 +265,9 @@ class DevicePlan:
     def decode_device(self, v_ptr: int, out_ptr: int, nc: int, stream: int = 0):
         _check(self._lib.dkss_decode_device(self._h, ctypes.c_void_p(v_ptr), ctypes.c_void_p(out_ptr), nc,
                                             ctypes.c_void_p(stream)))
+
+    def lucas_lehmer(self, p: int, iters: int, s: np.ndarray) -> np.ndarray:
+        """`iters` Lucas-Lehmer steps s <- s^2 - 2 mod 2^p - 1 on the device (s: u32 limbs)."""
+        s = np.ascontiguousarray(s, dtype=np.uint32).copy()
+        _check(self._lib.dkss_lucas_lehmer(self._h, p, iters, _ptr(s), s.size))
+        return s

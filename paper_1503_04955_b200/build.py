@@ -17,14 +17,18 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "_build")
+# DKSS_VARIANT=name builds an experiment library _lib/libdkss_<name>.so with the extra
+# nvcc flags in DKSS_EXTRA_FLAGS (loaded when DKSS_LIB points at it); default: the product
+VARIANT = os.environ.get("DKSS_VARIANT", "")
+OBJ = os.path.join(HERE, "_build" + (f"_{VARIANT}" if VARIANT else ""))
 LIBDIR = os.path.join(HERE, "_lib")
-LIB = os.path.join(LIBDIR, "libdkss.so")
+LIB = os.path.join(LIBDIR, f"libdkss_{VARIANT}.so" if VARIANT else "libdkss.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE,
+         *os.environ.get("DKSS_EXTRA_FLAGS", "").split()]
 
 INSTANCES = [(m, L) for m in (8, 16, 32) for L in (2, 3, 4, 5, 6)]
 

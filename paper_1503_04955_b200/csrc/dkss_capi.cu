@@ -143,6 +143,7 @@ struct dkss_plan {
   size_t ws_bytes = 0;
   cudaStream_t stream = nullptr;
   std::map<GraphKey, cudaGraphExec_t> graphs;
+  std::map<std::pair<long long, int>, cudaGraphExec_t> ll_graphs;  // (p, iterations per graph)
   std::mutex mu;
   struct Prof {
     static constexpr int kMax = 64;
@@ -167,6 +168,8 @@ void free_ws(dkss_plan* P) {
   P->d_poly = P->d_ops = P->d_prod = P->d_gmask = P->d_pmask = P->d_bstat = nullptr;
   for (auto& kv : P->graphs) cudaGraphExecDestroy(kv.second);
   P->graphs.clear();
+  for (auto& kv : P->ll_graphs) cudaGraphExecDestroy(kv.second);
+  P->ll_graphs.clear();
   P->cap_batch = 0;
   P->ws_bytes = 0;
 }
@@ -218,12 +221,37 @@ long long level_twiddles(const dkss_plan* P, int lv) {
 size_t smem_pass(const dkss_plan* P) { return P->kt.smem_pass; }
 size_t smem_two(const dkss_plan* P) { return P->kt.smem_bot; }
 
+// kernel launch with programmatic dependent launch allowed (the kernels call griddep_wait()
+// before touching their predecessor's output); DKSS_NO_PDL=1 turns it off
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DKSS_NO_PDL");
+    return !(e && *e && *e != '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 // --- launch helpers (all stream-ordered) ---------------------------------------------
 int launch_encode(dkss_plan* P, const uint32_t* ops, long long na, uint32_t* poly, int npoly, cudaStream_t s) {
   EncodeArgs A{ops, na, poly, P->poly_words, npoly, P->M, P->m, P->L, P->u};
   const long long total = 2LL * P->M * P->m * npoly;
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
-  k_encode<<<blocks, 256, 0, s>>>(A);
+  launch_k(k_encode, dim3(blocks), dim3(256), 0, s, A);
   CUCHK(cudaGetLastError());
   mark(P, s, DKSS_K_ENCODE, 0, npoly * (P->op_limbs * 4 + P->poly_words * 4));
   return 0;
@@ -238,13 +266,13 @@ int pass_kind(const dkss_plan* P, long long cols) {
 
 void launch_dft(dkss_plan* P, const PassArgs& A, long long cols, cudaStream_t s) {
   const int g = (int)std::min<long long>(P->grid_dft, (cols + kWarpsPerCta - 1) / kWarpsPerCta);
-  P->kt.dft<<<g, kWarpsPerCta * 32, P->kt.smem_dft, s>>>(A, P->mc);
+  launch_k(P->kt.dft, dim3(g), dim3(kWarpsPerCta * 32), P->kt.smem_dft, s, A, P->mc);
 }
 
 void launch_tw(dkss_plan* P, const PassArgs& A, long long cols, cudaStream_t s) {
   const long long items = cols * 2 * P->m * (P->m / 2);  // T = 2 outputs per item
   const int g = (int)std::min<long long>(P->grid_tw, (items + 255) / 256);
-  P->kt.tw<<<g, 256, 0, s>>>(A, P->mc);
+  launch_k(P->kt.tw, dim3(g), dim3(256), 0, s, A, P->mc);
 }
 
 // layout of the polynomials a pass launch walks (see PassArgs): the whole transform
@@ -311,9 +339,9 @@ int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s, c
       while (wpc < 8 && cols * wpc * 2 <= wres) wpc *= 2;
       A.wpc = wpc;
       const int gw = (int)std::min<long long>(P->grid_fw, (cols * wpc + kWarpsPerCta - 1) / kWarpsPerCta);
-      P->kt.fwd_w<<<gw, kWarpsPerCta * 32, P->kt.smem_fwd_w, s>>>(A, P->mc);
+      launch_k(P->kt.fwd_w, dim3(gw), dim3(kWarpsPerCta * 32), P->kt.smem_fwd_w, s, A, P->mc);
     } else {
-      P->kt.fwd<<<grid, P->kt.nt, smem_pass(P), s>>>(A, P->mc);
+      launch_k(P->kt.fwd, dim3(grid), dim3(P->kt.nt), smem_pass(P), s, A, P->mc);
     }
     CUCHK(cudaGetLastError());
     mark(P, s, DKSS_K_FWD_PASS, (long long)(share * rp_work(P, npoly * level_twiddles(P, lv))),
@@ -342,9 +370,9 @@ int launch_inv_levels(dkss_plan* P, uint32_t* poly, int npoly, bool scale_last, 
     } else if (kind == 2 && P->grid_iw) {
       A.wpc = 1;
       const int gw = (int)std::min<long long>(P->grid_iw, (cols + kWarpsPerCta - 1) / kWarpsPerCta);
-      P->kt.inv_w<<<gw, kWarpsPerCta * 32, P->kt.smem_inv_w, s>>>(A, P->mc);
+      launch_k(P->kt.inv_w, dim3(gw), dim3(kWarpsPerCta * 32), P->kt.smem_inv_w, s, A, P->mc);
     } else {
-      P->kt.inv<<<grid, P->kt.nt, smem_pass(P), s>>>(A, P->mc);
+      launch_k(P->kt.inv, dim3(grid), dim3(P->kt.nt), smem_pass(P), s, A, P->mc);
     }
     CUCHK(cudaGetLastError());
     mark(P, s, DKSS_K_INV_PASS, (long long)(share * rp_work(P, npoly * level_twiddles(P, lv))),
@@ -365,7 +393,7 @@ int launch_bottom(dkss_plan* P, uint32_t* a, const uint32_t* b, int npoly, int m
   const long long elems = 2LL * P->M * npoly;
   const int grid = (int)std::min<long long>((elems + P->kt.ne - 1) / P->kt.ne, P->grid_bot);
   A.total_elems = elems;
-  P->kt.bottom<<<grid, P->kt.nt, smem_two(P), s>>>(A, P->mc);
+  launch_k(P->kt.bottom, dim3(grid), dim3(P->kt.nt), smem_two(P), s, A, P->mc);
   CUCHK(cudaGetLastError());
   mark(P, s, DKSS_K_BOTTOM, mode ? rp_work(P, 2LL * P->M * npoly) : 0,
        (mode ? 3LL : 2LL) * npoly * P->poly_words * 4);
@@ -387,29 +415,32 @@ int launch_decode(dkss_plan* P, const uint32_t* v, uint32_t* out, int npoly, cud
   A.L = P->L;
   A.u = P->u;
   const int grid = A.blocks_per_poly * npoly;
-  k_decode1<<<grid, kDecThreads, 0, s>>>(A);
+  launch_k(k_decode1, dim3(grid), dim3(kDecThreads), 0, s, A);
   CUCHK(cudaGetLastError());
-  k_decode_scan<<<npoly, kScanThreads, 0, s>>>(A);
+  launch_k(k_decode_scan, dim3(npoly), dim3(kScanThreads), 0, s, A);
   CUCHK(cudaGetLastError());
   mark(P, s, DKSS_K_DECODE1, 0, npoly * (P->poly_words * 4 + P->prod_limbs * 4));
-  k_decode2<<<grid, kDecThreads, 0, s>>>(A);
+  launch_k(k_decode2, dim3(grid), dim3(kDecThreads), 0, s, A);
   CUCHK(cudaGetLastError());
   mark(P, s, DKSS_K_DECODE2, 0, npoly * 2LL * P->prod_limbs * 4);
   return 0;
 }
 
 // whole multiply: operands already encoded-able in device memory
+// b == nullptr: squaring (one forward transform; the pointwise step multiplies each
+// transformed element by itself -- the reference's LL loop squares, bigmul/bench.py:214-215)
 int run_mul(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, long long nl, uint32_t* prod,
             cudaStream_t s) {
+  const bool sq = b == nullptr;
   uint32_t* pa = P->d_poly;
-  uint32_t* pb = P->d_poly + (size_t)batch * P->poly_words;
+  uint32_t* pb = sq ? pa : P->d_poly + (size_t)batch * P->poly_words;
   int rc;
   if (P->levels > 0) {
     // encode fused into the first forward pass
-    if ((rc = launch_fwd_levels(P, P->d_poly, 2 * batch, s, a, b, nl, batch))) return rc;
+    if ((rc = launch_fwd_levels(P, P->d_poly, (sq ? 1 : 2) * batch, s, a, b, nl, batch))) return rc;
   } else {
     if ((rc = launch_encode(P, a, nl, pa, batch, s))) return rc;
-    if ((rc = launch_encode(P, b, nl, pb, batch, s))) return rc;
+    if (!sq && (rc = launch_encode(P, b, nl, pb, batch, s))) return rc;
   }
   if ((rc = launch_bottom(P, pa, pb, batch, 1, P->levels == 0, s))) return rc;
   if ((rc = launch_inv_levels(P, pa, batch, true, s))) return rc;
@@ -664,7 +695,7 @@ extern "C" {
 
 int dkss_mul_device(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, size_t nl, uint32_t* c, size_t nc,
                     void* stream) {
-  if (!P || batch < 1 || !a || !b || !c) return fail(DKSS_EINVAL, "bad argument");
+  if (!P || batch < 1 || !a || !c) return fail(DKSS_EINVAL, "bad argument");
   if ((long long)nl > P->op_limbs) return fail(DKSS_ERANGE, "operand limbs %zu exceed plan (%lld)", nl, P->op_limbs);
   if ((long long)nc < P->prod_limbs) return fail(DKSS_EINVAL, "nc=%zu below product limbs %lld", nc, P->prod_limbs);
   std::lock_guard<std::mutex> lk(P->mu);
@@ -809,18 +840,17 @@ int stage_digits(dkss_plan* P, int nops, const uint32_t* const* ptrs, const size
   R.ndst = P->op_limbs;
   R.sbits = digit_bits;
   const int gx = (int)std::max<long long>(1, std::min<long long>((P->op_limbs + 255) / 256, 1184 / nops + 1));
-  k_repack_bits<<<dim3(gx, nops), 256, 0, s>>>(R);
+  launch_k(k_repack_bits, dim3(dim3(gx, nops)), dim3(256), 0, s, R);
   CUCHK(cudaGetLastError());
   return 0;
 }
 
 // products of `batch` staged operand pairs (d_ops) -> host c (batch x nc limbs)
-int run_staged(dkss_plan* P, int batch, uint32_t* c, size_t nc, cudaStream_t s) {
+int run_staged(dkss_plan* P, int batch, bool sq, uint32_t* c, size_t nc, cudaStream_t s) {
   int rc;
   const size_t prw = (size_t)batch * P->prod_limbs;
-  if ((rc = launch_graph(P, batch, P->d_ops, P->d_ops + (size_t)batch * P->op_limbs, (size_t)P->op_limbs, P->d_prod,
-                         P->prod_limbs, s)))
-    return rc;
+  const uint32_t* b = sq ? nullptr : P->d_ops + (size_t)batch * P->op_limbs;
+  if ((rc = launch_graph(P, batch, P->d_ops, b, (size_t)P->op_limbs, P->d_prod, P->prod_limbs, s))) return rc;
   if ((rc = ensure_pin(P, prw))) return rc;
   CUCHK(cudaMemcpyAsync(P->h_pin, P->d_prod, prw * 4, cudaMemcpyDeviceToHost, s));
   CUCHK(cudaStreamSynchronize(s));
@@ -847,15 +877,20 @@ int dkss_mul_batch_digits(dkss_plan* P, int batch, const uint32_t* const* a, con
   if (!P || batch < 1 || !a || !na || !b || !nb || !c) return fail(DKSS_EINVAL, "bad argument");
   if (digit_bits < 8 || digit_bits > 32) return fail(DKSS_EINVAL, "digit_bits=%d outside [8, 32]", digit_bits);
   if (2LL * batch > 65535) return fail(DKSS_EINVAL, "batch %d too large", batch);
-  std::vector<const uint32_t*> ptrs(2 * (size_t)batch);
-  std::vector<size_t> counts(2 * (size_t)batch);
+  bool sq = true;  // every pair is (x, x): square (one forward transform)
+  for (int i = 0; i < batch && sq; ++i) sq = a[i] == b[i] && na[i] == nb[i];
+  const int nops = (sq ? 1 : 2) * batch;
+  std::vector<const uint32_t*> ptrs((size_t)nops);
+  std::vector<size_t> counts((size_t)nops);
   for (int i = 0; i < batch; ++i) {
     ptrs[i] = a[i];
     counts[i] = na[i];
-    ptrs[batch + i] = b[i];
-    counts[batch + i] = nb[i];
+    if (!sq) {
+      ptrs[batch + i] = b[i];
+      counts[batch + i] = nb[i];
+    }
   }
-  size_t total = 2 * (2 * (size_t)batch + 1);
+  size_t total = 2 * ((size_t)nops + 1);
   for (size_t q = 0; q < counts.size(); ++q) total += counts[q];
   std::lock_guard<std::mutex> lk(P->mu);
   CUCHK(cudaSetDevice(P->device));
@@ -863,8 +898,8 @@ int dkss_mul_batch_digits(dkss_plan* P, int batch, const uint32_t* const* a, con
   if ((rc = ensure_ws(P, batch))) return rc;
   // staging sized once for both directions: it must not be reallocated while a copy is in flight
   if ((rc = ensure_pin(P, std::max<size_t>(total, (size_t)batch * (size_t)P->prod_limbs)))) return rc;
-  if ((rc = stage_digits(P, 2 * batch, ptrs.data(), counts.data(), digit_bits, P->stream))) return rc;
-  return run_staged(P, batch, c, nc, P->stream);
+  if ((rc = stage_digits(P, nops, ptrs.data(), counts.data(), digit_bits, P->stream))) return rc;
+  return run_staged(P, batch, sq, c, nc, P->stream);
 }
 
 int dkss_mul_digits(dkss_plan* P, const uint32_t* a, size_t na, const uint32_t* b, size_t nb, int digit_bits,
@@ -954,7 +989,7 @@ int dkss_fs_rows(dkss_plan* P, int world, uint32_t* z, void* stream) {
   A.scale = 0;
   A.total_elems = (long long)rows << P->log_top_mu;
   const int grid = (int)std::min<long long>((A.total_elems + P->kt.ne - 1) / P->kt.ne, P->grid_bot);
-  P->kt.bottom<<<grid, P->kt.nt, smem_two(P), s>>>(A, P->mc);
+  launch_k(P->kt.bottom, dim3(grid), dim3(P->kt.nt), smem_two(P), s, A, P->mc);
   CUCHK(cudaGetLastError());
   mark(P, s, DKSS_K_BOTTOM, rp_work(P, A.total_elems), 3LL * A.total_elems * P->m * P->L * 4);
   return launch_inv_levels(P, z, rows, false, s, 1, P->levels, &g);
@@ -997,6 +1032,66 @@ int dkss_decode_device(dkss_plan* P, const uint32_t* v, uint32_t* out, size_t nc
   if ((rc = launch_decode(P, v, out, 1, s))) return rc;
   if ((long long)nc > P->prod_limbs)
     CUCHK(cudaMemsetAsync(out + P->prod_limbs, 0, ((long long)nc - P->prod_limbs) * 4, s));
+  return DKSS_OK;
+}
+
+// --- Lucas-Lehmer driver (bigmul/bench.py:197-217) -----------------------------------
+namespace {
+int ll_graph(dkss_plan* P, long long p, int k, cudaGraphExec_t* out) {
+  auto it = P->ll_graphs.find({p, k});
+  if (it != P->ll_graphs.end()) {
+    *out = it->second;
+    return 0;
+  }
+  cudaStream_t cap;
+  CUCHK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  CUCHK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+  int rc = 0;
+  MersArgs M{P->d_prod, P->prod_limbs, p, P->d_ops};
+  for (int i = 0; i < k && !rc; ++i) {
+    rc = run_mul(P, 1, P->d_ops, nullptr, P->op_limbs, P->d_prod, cap);
+    if (!rc) launch_k(k_mersenne_sub2, dim3(1), dim3(kMersThreads), 0, cap, M);
+  }
+  cudaGraph_t g;
+  cudaError_t e = cudaStreamEndCapture(cap, &g);
+  cudaStreamDestroy(cap);
+  if (rc) return rc;
+  if (e != cudaSuccess) return fail(DKSS_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
+  cudaGraphExec_t ge;
+  e = cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(DKSS_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+  P->ll_graphs[{p, k}] = ge;
+  *out = ge;
+  return 0;
+}
+}  // namespace
+
+int dkss_lucas_lehmer(dkss_plan* P, int64_t p, int64_t iters, uint32_t* s, size_t ns) {
+  if (!P || !s || iters < 0) return fail(DKSS_EINVAL, "bad argument");
+  if (p < 2 || p > P->N) return fail(DKSS_EINVAL, "exponent p=%lld outside [2, N=%lld]", (long long)p, P->N);
+  const size_t n = (size_t)((p + 31) / 32);
+  if (ns < n) return fail(DKSS_EINVAL, "state needs %zu limbs, got %zu", n, ns);
+  for (size_t i = n; i < ns; ++i)
+    if (s[i]) return fail(DKSS_ERANGE, "state exceeds 2^p");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  int rc;
+  if ((rc = ensure_ws(P, 1))) return rc;
+  cudaStream_t st = P->stream;
+  CUCHK(cudaMemsetAsync(P->d_ops, 0, P->op_limbs * 4, st));
+  CUCHK(cudaMemcpyAsync(P->d_ops, s, n * 4, cudaMemcpyHostToDevice, st));
+  const int K = 16;
+  long long left = iters;
+  while (left > 0) {
+    const int k = left >= K ? K : (int)left;
+    cudaGraphExec_t ge;
+    if ((rc = ll_graph(P, p, k, &ge))) return rc;
+    CUCHK(cudaGraphLaunch(ge, st));
+    left -= k;
+  }
+  CUCHK(cudaMemcpyAsync(s, P->d_ops, n * 4, cudaMemcpyDeviceToHost, st));
+  CUCHK(cudaStreamSynchronize(st));
   return DKSS_OK;
 }
 

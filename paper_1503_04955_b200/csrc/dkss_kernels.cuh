@@ -22,6 +22,9 @@
 // twiddle rows into shared memory while tile k is transformed and multiplied.
 #pragma once
 #include <cstdint>
+#ifdef DKSS_EXP_TRACE
+#include <cstdio>
+#endif
 #include "dkss_arith.cuh"
 
 namespace dkss {
@@ -50,10 +53,23 @@ struct Cfg<8> {
   static constexpr int NT = 256, COLS = 4, NE = 64, MINB = 2, T = 2;
   static constexpr bool TWS = true;
 };
+#ifndef DKSS_CFG16_NT  // experiment overrides (tools/exp_run.sh)
+#define DKSS_CFG16_NT 256
+#endif
+#ifndef DKSS_CFG16_MINB
+#define DKSS_CFG16_MINB 2
+#endif
+#ifndef DKSS_CFG16_T
+#define DKSS_CFG16_T 2
+#endif
 template <>
 struct Cfg<16> {
-  static constexpr int NT = 256, COLS = 1, NE = 32, MINB = 2, T = 2;
+  static constexpr int NT = DKSS_CFG16_NT, COLS = 1, NE = 32, MINB = DKSS_CFG16_MINB, T = DKSS_CFG16_T;
+#ifdef DKSS_EXP_NOTWS
+  static constexpr bool TWS = false;
+#else
   static constexpr bool TWS = true;
+#endif
 };
 template <>
 struct Cfg<32> {
@@ -73,6 +89,13 @@ struct SmemPlan {
   static constexpr int BOT = BOT_STAGES * STAGE_BOT + C::NE * S::ESW;
   static constexpr int RMUL = 2 * C::NE * S::ES + C::NE * S::ESW;
 };
+
+// programmatic dependent launch: kernels of one multiply are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's CTAs may become resident
+// while its predecessor drains; griddep_wait() blocks until the predecessor grid has
+// completed and its memory is visible (a no-op without the attribute)
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
 __device__ __forceinline__ int bitrev_n(int x, int bits) { return bits ? (int)(__brev((unsigned)x) >> (32 - bits)) : 0; }
 
@@ -327,6 +350,45 @@ __device__ __forceinline__ uint32_t* dft_pingpong(uint32_t* buf, uint32_t* alt, 
 }
 
 // ---------------------------------------------------------------------------
+// timing experiments only (tools/exp_build.sh): drop the column DFT or the twiddle products
+#ifdef DKSS_EXP_NODFT
+constexpr bool kExpNoDft = true;
+#else
+constexpr bool kExpNoDft = false;
+#endif
+#ifdef DKSS_EXP_NOSPREAD
+constexpr bool kSpreadIssue = false;
+#else
+constexpr bool kSpreadIssue = true;
+#endif
+#ifdef DKSS_EXP_NOMAC
+constexpr bool kExpNoMac = true;
+#else
+constexpr bool kExpNoMac = false;
+#endif
+
+#ifdef DKSS_EXP_TRACE
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE_DECL unsigned long long tr_[12]; int trn_ = 0; tr_[trn_++] = gtime();
+#define TRACE_MARK if (trn_ < 12) tr_[trn_++] = gtime();
+#define TRACE_DUMP(name)                                                                                 \
+  if (threadIdx.x == 0 && (blockIdx.x % 37 == 0 || blockIdx.x == gridDim.x - 1)) {                        \
+    for (int q_ = trn_; q_ < 12; ++q_) tr_[q_] = tr_[0];                                                 \
+    printf("TRACE %s blk %d t0 %llu : %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", name, blockIdx.x, \
+           tr_[0] % 1000000000ull, tr_[1] - tr_[0], tr_[2] - tr_[0], tr_[3] - tr_[0], tr_[4] - tr_[0],        \
+           tr_[5] - tr_[0], tr_[6] - tr_[0], tr_[7] - tr_[0], tr_[8] - tr_[0], tr_[9] - tr_[0],             \
+           tr_[10] - tr_[0], tr_[11] - tr_[0]);                                                            \
+  }
+#else
+#define TRACE_DECL
+#define TRACE_MARK
+#define TRACE_DUMP(name)
+#endif
+
 struct PassArgs {
   uint32_t* poly;        // first polynomial of the launch
   long long poly_words;  // 2M * MM * L
@@ -372,39 +434,47 @@ __device__ __forceinline__ long long tw_exp(const PassArgs& A, int j, long long 
   return e & ((1LL << A.log_top_mu) - 1);
 }
 
-// warp 0: TMA-load the NE column elements of tile `tile` (FWD: bit-reversed slots) and, when
-// staged, the twiddle row of every element needing a ring product
+// TMA-load the NE column elements of tile `tile` (FWD: bit-reversed slots) and, when staged,
+// the twiddle row of every element needing a ring product.  Warp 0 counts the bytes and
+// arms the barrier; the copies themselves are issued by the calling threads (one warp, or
+// spread over the whole CTA when kSpreadIssue: a bulk copy's issue is serialised per
+// warp, so 2*NE copies from one warp cost microseconds)
 template <int MM, int L, bool FWD>
 __device__ __forceinline__ void issue_pass_tile(const PassArgs& A, long long tile, uint64_t* bar, uint32_t* buf,
                                                 uint32_t* tws, bool load_elems = true) {
   constexpr int ES = Smem<MM, L>::ES, EST = Smem<MM, L>::EST;
   constexpr int NE = Cfg<MM>::NE, COLS = Cfg<MM>::COLS, E = 2 * MM, LOGE = Geo<MM>::LOGE;
+  constexpr int NW = kSpreadIssue ? Cfg<MM>::NT / 32 : 1;
   constexpr uint32_t EB = MM * L * 4, TB = 2 * MM * L * 4;
-  const int lane = threadIdx.x & 31;
-  uint32_t bytes = 0;
-  for (int e = lane; e < NE; e += 32) {
-    const long long cg = tile * COLS + e / E;
-    if (cg >= A.total_cols) continue;
-    if (load_elems) bytes += EB;
-    if constexpr (Cfg<MM>::TWS) {
-      long long l;
-      col_elem(A, cg, 0, LOGE, 0, &l);
-      int r;
-      if (tw_exp(A, e % E, l, &r)) bytes += TB;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    uint32_t bytes = 0;
+    for (int e = lane; e < NE; e += 32) {
+      const long long cg = tile * COLS + e / E;
+      if (cg >= A.total_cols) continue;
+      if (load_elems) bytes += EB;
+      if constexpr (Cfg<MM>::TWS) {
+        long long l;
+        col_elem(A, cg, 0, LOGE, 0, &l);
+        int r;
+        if (tw_exp(A, e % E, l, &r)) bytes += TB;
+      }
     }
+    bytes = __reduce_add_sync(0xFFFFFFFFu, bytes);
+    if (lane == 0) mbar_expect_tx(bar, bytes);
+    __syncwarp();
   }
-  bytes = __reduce_add_sync(0xFFFFFFFFu, bytes);
-  if (lane == 0) mbar_expect_tx(bar, bytes);
-  __syncwarp();
-  for (int e = lane; e < NE; e += 32) {
+  for (int q = warp + NW * lane; q < 2 * NE; q += NW * 32) {
+    const int e = q % NE;
     const int c = e / E, j = e % E;
     const long long cg = tile * COLS + c;
     if (cg >= A.total_cols) continue;
     long long l;
     const long long off = col_elem(A, cg, j, LOGE, MM * L, &l);
-    const int slot = FWD ? c * E + bitrev_n(j, LOGE) : e;
-    if (load_elems) bulk_g2s(buf + slot * ES, A.poly + off, EB, bar);
-    if constexpr (Cfg<MM>::TWS) {
+    if (q < NE) {
+      const int slot = FWD ? c * E + bitrev_n(j, LOGE) : e;
+      if (load_elems) bulk_g2s(buf + slot * ES, A.poly + off, EB, bar);
+    } else if constexpr (Cfg<MM>::TWS) {
       int r;
       const long long s = tw_exp(A, j, l, &r);
       if (s) bulk_g2s(tws + e * EST, A.twr + s * (2 * MM * L), TB, bar);
@@ -467,6 +537,8 @@ __device__ __forceinline__ void cta_encode_tile(const PassArgs& A, long long til
 // rho^(vv*l*base_pow) = alpha^r * rho_table[s] (bigmul/dkss.py:480-492)
 template <int MM, int L>
 __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArgs A, ModCtx mc) {
+  griddep_wait();  // PDL: predecessor grid complete, its writes visible
+  griddep_launch();
   constexpr int kT = Cfg<MM>::T;
   constexpr int ES = Smem<MM, L>::ES, EST = Smem<MM, L>::EST;
   constexpr int NT = Cfg<MM>::NT, NE = Cfg<MM>::NE, COLS = Cfg<MM>::COLS, E = 2 * MM, LOGE = Geo<MM>::LOGE;
@@ -474,6 +546,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArg
   constexpr int TPE = MM / kT;
   extern __shared__ __align__(16) uint32_t smem[];
   __shared__ __align__(8) uint64_t bar[2];
+  TRACE_DECL
   const long long ntiles = (A.total_cols + COLS - 1) / COLS;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
@@ -482,21 +555,25 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArg
   __syncthreads();
   long long tile = blockIdx.x;
   const bool enc = A.ops_a != nullptr;
-  if (tile < ntiles && threadIdx.x < 32) issue_pass_tile<MM, L, true>(A, tile, &bar[0], smem, smem + NE * ES, !enc);
+  if (tile < ntiles && (kSpreadIssue || threadIdx.x < 32))
+    issue_pass_tile<MM, L, true>(A, tile, &bar[0], smem, smem + NE * ES, !enc);
   for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
     const int st = k & 1;
     uint32_t* buf = smem + st * STAGE;
     uint32_t* tws = buf + NE * ES;
     const long long nxt = tile + gridDim.x;
-    if (nxt < ntiles && threadIdx.x < 32)
+    if (nxt < ntiles && (kSpreadIssue || threadIdx.x < 32))
       issue_pass_tile<MM, L, true>(A, nxt, &bar[st ^ 1], smem + (st ^ 1) * STAGE, smem + (st ^ 1) * STAGE + NE * ES,
                                    !enc);
     if (enc) {
       cta_encode_tile<MM, L>(A, tile, buf);
       __syncthreads();
     }
+    TRACE_MARK
     mbar_wait(&bar[st], (k >> 1) & 1);
-    const uint32_t* xv = dft_pingpong<MM, L, NE>(buf, smem + 2 * STAGE, LOGE, mc);
+    TRACE_MARK
+    const uint32_t* xv = kExpNoDft ? buf : dft_pingpong<MM, L, NE>(buf, smem + 2 * STAGE, LOGE, mc);
+    TRACE_MARK
     for (int it = threadIdx.x; it < NE * TPE; it += NT) {
       const int el = it / TPE, k0 = (it % TPE) * kT;
       const int c = el / E, vv = el % E;
@@ -507,7 +584,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArg
       int r;
       const long long s = tw_exp(A, vv, l, &r);
       uint32_t w[kT][L];
-      if (s == 0) {
+      if (s == 0 || kExpNoMac) {
 #pragma unroll
         for (int t = 0; t < kT; ++t) ld_res<L>(w[t], xv + el * ES + (k0 + t) * L);
       } else {
@@ -517,12 +594,16 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArg
     }
     fence_proxy_async();
     __syncthreads();
+    TRACE_MARK
   }
+  TRACE_DUMP(enc ? "fwd0" : "fwd")
 }
 
 // inverse (transposed) column pass: twiddle ring product, then column DFT
 template <int MM, int L>
 __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArgs A, ModCtx mc) {
+  griddep_wait();  // PDL: predecessor grid complete, its writes visible
+  griddep_launch();
   constexpr int kT = Cfg<MM>::T;
   constexpr int ES = Smem<MM, L>::ES, EST = Smem<MM, L>::EST;
   constexpr int NT = Cfg<MM>::NT, NE = Cfg<MM>::NE, COLS = Cfg<MM>::COLS, E = 2 * MM, LOGE = Geo<MM>::LOGE;
@@ -531,6 +612,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArg
   constexpr int PER = (NE * TPE + NT - 1) / NT;
   extern __shared__ __align__(16) uint32_t smem[];
   __shared__ __align__(8) uint64_t bar[2];
+  TRACE_DECL
   const long long ntiles = (A.total_cols + COLS - 1) / COLS;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
@@ -538,15 +620,18 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArg
   }
   __syncthreads();
   long long tile = blockIdx.x;
-  if (tile < ntiles && threadIdx.x < 32) issue_pass_tile<MM, L, false>(A, tile, &bar[0], smem, smem + NE * ES);
+  if (tile < ntiles && (kSpreadIssue || threadIdx.x < 32))
+    issue_pass_tile<MM, L, false>(A, tile, &bar[0], smem, smem + NE * ES);
   for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
     const int st = k & 1;
     uint32_t* buf = smem + st * STAGE;
     uint32_t* tws = buf + NE * ES;
     const long long nxt = tile + gridDim.x;
-    if (nxt < ntiles && threadIdx.x < 32)
+    if (nxt < ntiles && (kSpreadIssue || threadIdx.x < 32))
       issue_pass_tile<MM, L, false>(A, nxt, &bar[st ^ 1], smem + (st ^ 1) * STAGE, smem + (st ^ 1) * STAGE + NE * ES);
+    TRACE_MARK
     mbar_wait(&bar[st], (k >> 1) & 1);
+    TRACE_MARK
     uint32_t res[PER][kT][L];
     int dsl[PER], rot[PER];
 #pragma unroll
@@ -574,6 +659,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArg
     for (int q = 0; q < PER; ++q)
       if (dsl[q] >= 0) store_rot<MM, L, kT>(buf + dsl[q], res[q], ((threadIdx.x + q * NT) % TPE) * kT, rot[q], mc);
     __syncthreads();
+    TRACE_MARK
     const uint32_t* ov = dft_pingpong<MM, L, NE>(buf, smem + 2 * STAGE, LOGE, mc);
     for (int it = threadIdx.x; it < NE * MM; it += NT) {
       const int el = it / MM, kk = it % MM;
@@ -594,7 +680,9 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArg
     }
     fence_proxy_async();
     __syncthreads();
+    TRACE_MARK
   }
+  TRACE_DUMP("inv")
 }
 
 // ---------------------------------------------------------------------------
@@ -639,6 +727,8 @@ __device__ __forceinline__ void issue_bottom_tile(const BottomArgs& A, long long
 
 template <int MM, int L>
 __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_bottom(BottomArgs A, ModCtx mc) {
+  griddep_wait();  // PDL: predecessor grid complete, its writes visible
+  griddep_launch();
   constexpr int kT = Cfg<MM>::T;
   constexpr int ES = Smem<MM, L>::ES, ESW = Smem<MM, L>::ESW;
   constexpr int NT = Cfg<MM>::NT, NE = Cfg<MM>::NE;
@@ -722,6 +812,8 @@ template <int MM, int L>
 __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_rmul(const uint32_t* __restrict__ x,
                                                                      const uint32_t* __restrict__ y, uint32_t* out,
                                                                      long long count, ModCtx mc) {
+  griddep_wait();  // PDL: predecessor grid complete, its writes visible
+  griddep_launch();
   constexpr int kT = Cfg<MM>::T;
   constexpr int ES = Smem<MM, L>::ES, ESW = Smem<MM, L>::ESW;
   constexpr int NT = Cfg<MM>::NT, NE = Cfg<MM>::NE;
@@ -823,6 +915,8 @@ struct EncodeArgs {
 };
 
 __global__ void k_encode(EncodeArgs A) {
+  griddep_wait();  // PDL: predecessor grid complete, its writes visible
+  griddep_launch();
   const long long per = 2LL * A.M * A.MM;
   const long long total = per * A.npoly;
   const int half = A.MM / 2;
@@ -963,6 +1057,8 @@ __device__ __forceinline__ unsigned long long window_sum(const DecodeArgs& A, co
 
 // phase 1: per-limb sums, per-warp (generate, propagate) masks, per-block carry function
 __global__ void __launch_bounds__(kDecThreads) k_decode1(DecodeArgs A) {
+  griddep_wait();  // PDL: predecessor grid complete, its writes visible
+  griddep_launch();
   const int pidx = blockIdx.x / A.blocks_per_poly;
   const int blk = blockIdx.x % A.blocks_per_poly;
   const long long t = (long long)blk * kDecThreads + threadIdx.x;
@@ -1007,6 +1103,8 @@ __global__ void __launch_bounds__(kDecThreads) k_decode1(DecodeArgs A) {
 // with the (generate | propagate) + generate add trick at warp and CTA level.
 constexpr int kScanThreads = 1024;
 __global__ void __launch_bounds__(kScanThreads) k_decode_scan(DecodeArgs A) {
+  griddep_wait();  // PDL: predecessor grid complete, its writes visible
+  griddep_launch();
   const int B = A.blocks_per_poly;
   uint32_t* st = A.bstat + (long long)blockIdx.x * B;
   const int per = (B + kScanThreads - 1) / kScanThreads;
@@ -1049,6 +1147,8 @@ __global__ void __launch_bounds__(kScanThreads) k_decode_scan(DecodeArgs A) {
 
 // phase 3: apply carries inside each block
 __global__ void __launch_bounds__(kDecThreads) k_decode2(DecodeArgs A) {
+  griddep_wait();  // PDL: predecessor grid complete, its writes visible
+  griddep_launch();
   const int pidx = blockIdx.x / A.blocks_per_poly;
   const int blk = blockIdx.x % A.blocks_per_poly;
   const long long t = (long long)blk * kDecThreads + threadIdx.x;
@@ -1080,6 +1180,8 @@ __global__ void __launch_bounds__(kDecThreads) k_decode2(DecodeArgs A) {
 // (run = contiguous uint4 per block); blockIdx.y walks the (n, a, b) blocks of src
 __global__ void k_block_transpose(const uint4* __restrict__ src, uint4* __restrict__ dst, int A, int B,
                                   long long run) {
+  griddep_wait();  // PDL: predecessor grid complete, its writes visible
+  griddep_launch();
   const int blk = blockIdx.y;
   const int b = blk % B, t = blk / B;
   const int a = t % A, n = t / A;
@@ -1104,6 +1206,8 @@ struct RepackArgs {
 };
 
 __global__ void k_repack_bits(RepackArgs A) {
+  griddep_wait();  // PDL: predecessor grid complete, its writes visible
+  griddep_launch();
   const int q = blockIdx.y;
   const long long o0 = A.off[q], ns = A.off[q + 1] - o0;
   const uint32_t* src = A.stage + o0;
@@ -1123,6 +1227,159 @@ __global__ void k_repack_bits(RepackArgs A) {
       sh += A.sbits;
     }
     dst[i] = (uint32_t)acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Lucas-Lehmer step tail (bigmul/bench.py:187-194, 214-216): s = (c - 2) mod (2^p - 1)
+// for a product c < 2^(2p), canonical in [0, 2^p - 1).  One CTA of kMersThreads threads;
+// n = ceil(p/32) limbs of s, thread t owns a contiguous chunk; every multi-limb add
+// resolves its carries with a block-wide (generate, propagate) scan.
+constexpr int kMersThreads = 1024;
+
+struct MersArgs {
+  const uint32_t* c;  // product limbs
+  long long nc;
+  long long p;
+  uint32_t* s;        // n = ceil(p/32) limbs out (limbs of s beyond n are left untouched)
+};
+
+// carry-in of this thread's chunk given its (g, p) and the carry into chunk 0; also
+// returns the carry out of the last chunk in *cout (all threads)
+__device__ __forceinline__ uint32_t block_carry(uint32_t g, uint32_t pr, uint32_t c0, uint32_t* cout) {
+  __shared__ uint32_t wg[32], wp[32], s_out;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // inclusive warp scan of (g, p): combine earlier (g', p') into later: g |= p & g'; p &= p'
+  uint32_t G = g, Pp = pr;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t g2 = __shfl_up_sync(0xFFFFFFFFu, G, d), p2 = __shfl_up_sync(0xFFFFFFFFu, Pp, d);
+    if (lane >= d) {
+      G |= Pp & g2;
+      Pp &= p2;
+    }
+  }
+  if (lane == 31) {
+    wg[warp] = G;
+    wp[warp] = Pp;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t g1 = lane < (int)(blockDim.x >> 5) ? wg[lane] : 0u, p1 = lane < (int)(blockDim.x >> 5) ? wp[lane] : 1u;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t g2 = __shfl_up_sync(0xFFFFFFFFu, g1, d), p2 = __shfl_up_sync(0xFFFFFFFFu, p1, d);
+      if (lane >= d) {
+        g1 |= p1 & g2;
+        p1 &= p2;
+      }
+    }
+    // exclusive carry into warp `lane`, with the external carry c0
+    const uint32_t ge = __shfl_up_sync(0xFFFFFFFFu, g1, 1), pe = __shfl_up_sync(0xFFFFFFFFu, p1, 1);
+    const uint32_t cin_w = lane == 0 ? c0 : (ge | (pe & c0));
+    wg[lane] = cin_w;
+    if (lane == 31) s_out = g1 | (p1 & c0);
+  }
+  __syncthreads();
+  const uint32_t cw = wg[warp];
+  const uint32_t ge = __shfl_up_sync(0xFFFFFFFFu, G, 1), pe = __shfl_up_sync(0xFFFFFFFFu, Pp, 1);
+  const uint32_t cin = lane == 0 ? cw : (ge | (pe & cw));
+  *cout = s_out;
+  __syncthreads();
+  return cin;
+}
+
+// limb i of (c >> sh) restricted to bits below 32*n (sh = bit offset)
+__device__ __forceinline__ uint32_t limb_at(const uint32_t* c, long long nc, long long bit) {
+  const long long w = bit >> 5;
+  const int o = (int)(bit & 31);
+  const uint32_t lo = w < nc ? c[w] : 0u, hi = (w + 1) < nc ? c[w + 1] : 0u;
+  return o ? __funnelshift_r(lo, hi, o) : lo;
+}
+
+__global__ void __launch_bounds__(kMersThreads) k_mersenne_sub2(MersArgs A) {
+  griddep_wait();
+  griddep_launch();
+  const long long p = A.p, n = (p + 31) >> 5;
+  const int topb = (int)(p - 32 * (n - 1));  // bits used in limb n-1 (1..32)
+  const uint32_t topmask = topb == 32 ? 0xFFFFFFFFu : ((1u << topb) - 1u);
+  const long long K = (n + blockDim.x - 1) / blockDim.x;
+  const long long i0 = threadIdx.x * K, i1 = min(n, i0 + K);
+  __shared__ uint32_t s_flag[2];
+  uint32_t cout;
+  // (1) t = lo + hi, lo = c mod 2^p, hi = c >> p
+  auto lo_at = [&](long long i) { return i < A.nc ? (i == n - 1 ? A.c[i] & topmask : A.c[i]) : 0u; };
+  auto hi_at = [&](long long i) { return limb_at(A.c, A.nc, p + 32 * i) & (i == n - 1 ? topmask : 0xFFFFFFFFu); };
+  uint32_t g = 0, pr = 1;
+  {
+    uint32_t cy = 0;
+    for (long long i = i0; i < i1; ++i) {
+      const uint64_t v = (uint64_t)lo_at(i) + hi_at(i) + cy;
+      cy = (uint32_t)(v >> 32);
+      pr &= ((uint32_t)v == 0xFFFFFFFFu);
+    }
+    g = cy;
+  }
+  uint32_t cin = block_carry(g, pr, 0u, &cout);
+  for (long long i = i0; i < i1; ++i) {
+    const uint64_t v = (uint64_t)lo_at(i) + hi_at(i) + cin;
+    cin = (uint32_t)(v >> 32);
+    A.s[i] = (uint32_t)v;
+  }
+  __syncthreads();
+  // (2) fold the bit at position p (t < 2^(p+1)): t = (t mod 2^p) + (t >> p)
+  uint32_t fold = cout;  // carry out of limb n-1 (bit 32n)
+  if (topb < 32) fold = (A.s[n - 1] >> topb) & 1u;
+  __syncthreads();
+  if (threadIdx.x == 0 && topb < 32) A.s[n - 1] &= topmask;
+  __syncthreads();
+  g = 0;
+  pr = 1;
+  for (long long i = i0; i < i1; ++i) pr &= (A.s[i] == 0xFFFFFFFFu);
+  cin = block_carry(0u, pr, fold, &cout);
+  for (long long i = i0; i < i1 && cin; ++i) {
+    const uint64_t v = (uint64_t)A.s[i] + cin;
+    cin = (uint32_t)(v >> 32);
+    A.s[i] = (uint32_t)v;
+  }
+  __syncthreads();
+  // (3) t - 2 mod (2^p - 1), t in [0, 2^p - 1]: t >= 2 -> t - 2, else t + 2^p - 3
+  if (threadIdx.x == 0) s_flag[0] = 0;
+  __syncthreads();
+  uint32_t any_hi = 0;
+  for (long long i = max(i0, 1LL); i < i1; ++i) any_hi |= A.s[i];
+  if (any_hi) atomicOr(&s_flag[0], 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) s_flag[1] = !s_flag[0] && A.s[0] < 2;
+  __syncthreads();
+  if (s_flag[1]) {
+    const uint32_t t0 = A.s[0];
+    for (long long i = i0; i < i1; ++i) A.s[i] = i == n - 1 ? topmask : 0xFFFFFFFFu;
+    __syncthreads();
+    if (threadIdx.x == 0) A.s[0] = (n == 1 ? topmask : 0xFFFFFFFFu) - 2u + t0;  // 2^p - 3 + t0
+    return;
+  }
+  // borrow chain of t - 2 (t >= 2 here): chunk 0 generates a borrow if its own limbs
+  // underflow; a later chunk passes a borrow on iff all its limbs are zero
+  g = 0;
+  pr = 1;
+  if (i0 == 0) {
+    uint32_t b = 0;
+    for (long long i = i0; i < i1; ++i) {
+      const uint32_t sub = (i == 0 ? 2u : 0u) + b;
+      b = (uint32_t)(A.s[i] < sub);
+    }
+    g = b;
+    pr = 0;
+  } else {
+    for (long long i = i0; i < i1; ++i) pr &= (A.s[i] == 0u);
+  }
+  cin = block_carry(g, pr, 0u, &cout);
+  for (long long i = i0; i < i1; ++i) {
+    const uint32_t sub = (i == 0 ? 2u : 0u) + cin;
+    const uint32_t v = A.s[i];
+    cin = (uint32_t)(v < sub);
+    A.s[i] = v - sub;
   }
 }
 

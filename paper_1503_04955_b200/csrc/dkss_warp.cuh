@@ -132,6 +132,8 @@ __device__ __forceinline__ void encode_coef(const PassArgs& A, long long cg, int
 // forward column pass, warp per column (A.wpc warps per column)
 template <int MM, int L>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_fwd_warp(PassArgs A, ModCtx mc) {
+  griddep_wait();  // PDL: predecessor grid complete, its writes visible
+  griddep_launch();
   constexpr int kT = Cfg<MM>::T;
   constexpr int ES = Smem<MM, L>::ES, E = 2 * MM, EPT = WG<MM>::EPT, TPE = MM / kT;
   extern __shared__ __align__(16) uint32_t smem[];
@@ -192,6 +194,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_fwd_warp(PassArgs A, M
 // bit-reversed slots, then the register DFT, then the store (optionally scaled by kscale)
 template <int MM, int L>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_inv_warp(PassArgs A, ModCtx mc) {
+  griddep_wait();  // PDL: predecessor grid complete, its writes visible
+  griddep_launch();
   constexpr int kT = Cfg<MM>::T;
   constexpr int ES = Smem<MM, L>::ES, E = 2 * MM, EPT = WG<MM>::EPT, TPE = MM / kT, LOGE = Geo<MM>::LOGE;
   extern __shared__ __align__(16) uint32_t smem[];
@@ -260,6 +264,8 @@ namespace dkss {
 // and (2M)^-1 scaling (last inverse level).
 template <int MM, int L>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) k_dft_cols(PassArgs A, ModCtx mc) {
+  griddep_wait();  // PDL: predecessor grid complete, its writes visible
+  griddep_launch();
   constexpr int ES = Smem<MM, L>::ES, E = 2 * MM, EPT = WG<MM>::EPT, LOGE = Geo<MM>::LOGE;
   extern __shared__ __align__(16) uint32_t smem[];
   __shared__ __align__(8) uint64_t bars[kWarpsPerCta];
@@ -309,6 +315,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_dft_cols(PassArgs A, ModC
 // forward levels run it after k_dft_cols, inverse levels before.
 template <int MM, int L>
 __global__ void __launch_bounds__(256, 2) k_twiddle(PassArgs A, ModCtx mc) {
+  griddep_wait();  // PDL: predecessor grid complete, its writes visible
+  griddep_launch();
   constexpr int kT = Cfg<MM>::T, TPE = MM / kT, E = 2 * MM, LOGE = Geo<MM>::LOGE;
   static_assert(32 % TPE == 0, "an element's work items must share a warp");
   const long long total = A.total_cols * E * TPE;
