@@ -439,15 +439,17 @@ __device__ __forceinline__ long long tw_exp(const PassArgs& A, int j, long long 
 // arms the barrier; the copies themselves are issued by the calling threads (one warp, or
 // spread over the whole CTA when kSpreadIssue: a bulk copy's issue is serialised per
 // warp, so 2*NE copies from one warp cost microseconds)
+// part: 3 = everything; 1 = arm the barrier + twiddle rows (independent of the previous
+// kernel's output, issued before griddep_wait); 2 = the column elements
 template <int MM, int L, bool FWD>
 __device__ __forceinline__ void issue_pass_tile(const PassArgs& A, long long tile, uint64_t* bar, uint32_t* buf,
-                                                uint32_t* tws, bool load_elems = true) {
+                                                uint32_t* tws, bool load_elems = true, int part = 3) {
   constexpr int ES = Smem<MM, L>::ES, EST = Smem<MM, L>::EST;
   constexpr int NE = Cfg<MM>::NE, COLS = Cfg<MM>::COLS, E = 2 * MM, LOGE = Geo<MM>::LOGE;
   constexpr int NW = kSpreadIssue ? Cfg<MM>::NT / 32 : 1;
   constexpr uint32_t EB = MM * L * 4, TB = 2 * MM * L * 4;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (warp == 0) {
+  if (warp == 0 && (part & 1)) {
     uint32_t bytes = 0;
     for (int e = lane; e < NE; e += 32) {
       const long long cg = tile * COLS + e / E;
@@ -473,8 +475,9 @@ __device__ __forceinline__ void issue_pass_tile(const PassArgs& A, long long til
     const long long off = col_elem(A, cg, j, LOGE, MM * L, &l);
     if (q < NE) {
       const int slot = FWD ? c * E + bitrev_n(j, LOGE) : e;
-      if (load_elems) bulk_g2s(buf + slot * ES, A.poly + off, EB, bar);
+      if (load_elems && (part & 2)) bulk_g2s(buf + slot * ES, A.poly + off, EB, bar);
     } else if constexpr (Cfg<MM>::TWS) {
+      if (!(part & 1)) continue;
       int r;
       const long long s = tw_exp(A, j, l, &r);
       if (s) bulk_g2s(tws + e * EST, A.twr + s * (2 * MM * L), TB, bar);
@@ -537,7 +540,6 @@ __device__ __forceinline__ void cta_encode_tile(const PassArgs& A, long long til
 // rho^(vv*l*base_pow) = alpha^r * rho_table[s] (bigmul/dkss.py:480-492)
 template <int MM, int L>
 __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArgs A, ModCtx mc) {
-  griddep_wait();  // PDL: predecessor grid complete, its writes visible
   griddep_launch();
   constexpr int kT = Cfg<MM>::T;
   constexpr int ES = Smem<MM, L>::ES, EST = Smem<MM, L>::EST;
@@ -555,8 +557,13 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArg
   __syncthreads();
   long long tile = blockIdx.x;
   const bool enc = A.ops_a != nullptr;
+  // PDL: the twiddle rows do not depend on the previous kernel; the elements (and, for the
+  // fused encode, the operands) do
   if (tile < ntiles && (kSpreadIssue || threadIdx.x < 32))
-    issue_pass_tile<MM, L, true>(A, tile, &bar[0], smem, smem + NE * ES, !enc);
+    issue_pass_tile<MM, L, true>(A, tile, &bar[0], smem, smem + NE * ES, !enc, 1);
+  griddep_wait();
+  if (tile < ntiles && (kSpreadIssue || threadIdx.x < 32))
+    issue_pass_tile<MM, L, true>(A, tile, &bar[0], smem, smem + NE * ES, !enc, 2);
   for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
     const int st = k & 1;
     uint32_t* buf = smem + st * STAGE;
@@ -602,7 +609,6 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArg
 // inverse (transposed) column pass: twiddle ring product, then column DFT
 template <int MM, int L>
 __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArgs A, ModCtx mc) {
-  griddep_wait();  // PDL: predecessor grid complete, its writes visible
   griddep_launch();
   constexpr int kT = Cfg<MM>::T;
   constexpr int ES = Smem<MM, L>::ES, EST = Smem<MM, L>::EST;
@@ -621,7 +627,10 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArg
   __syncthreads();
   long long tile = blockIdx.x;
   if (tile < ntiles && (kSpreadIssue || threadIdx.x < 32))
-    issue_pass_tile<MM, L, false>(A, tile, &bar[0], smem, smem + NE * ES);
+    issue_pass_tile<MM, L, false>(A, tile, &bar[0], smem, smem + NE * ES, true, 1);
+  griddep_wait();  // PDL: twiddle rows above are independent of the previous kernel
+  if (tile < ntiles && (kSpreadIssue || threadIdx.x < 32))
+    issue_pass_tile<MM, L, false>(A, tile, &bar[0], smem, smem + NE * ES, true, 2);
   for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
     const int st = k & 1;
     uint32_t* buf = smem + st * STAGE;
