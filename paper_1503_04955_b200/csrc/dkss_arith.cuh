@@ -27,6 +27,8 @@ struct ModCtx {
   uint32_t pinv;               // -p^-1 mod 2^32
   float pf_inv;                // 2^(32(L-2)) / p  (quotient estimate)
   uint32_t cbias[DKSS_MAXL];   // -(2^(32L) - 1) * R mod p  (ring_mul bias correction)
+  uint32_t proth;              // p = 1 + ptop * 2^(32(L-1)): p[0] = 1, middle limbs 0 (every
+                               // table prime at the configs, 81 * 2^121 + 1); REDC specialises
 };
 
 // r = (a + b) mod p and r = (a - b) mod p for canonical a, b (PTX carry chains, dkss_carry.cuh)
@@ -73,21 +75,47 @@ __device__ __forceinline__ void neg_mod_canon(uint32_t (&r)[L], const uint32_t (
 // Returns the canonical residue T*R^-1 mod p.
 template <int L>
 __device__ __forceinline__ void redc(uint32_t (&r)[L], uint32_t (&t)[2 * L + 1], const ModCtx& M) {
+  if (M.proth) {
+    // p = 1 + ptop 2^(32(L-1)), -p^-1 = -1 mod 2^32: q = -t_i, and q p touches two limbs only
+    // (t_i + q = 0 with carry t_i != 0; q ptop lands on limb i+L-1) -- one wide product per step
+    const uint32_t ptop = M.p[L - 1];
 #pragma unroll
-  for (int i = 0; i < L; ++i) {
-    const uint32_t q = t[i] * M.pinv;
-    uint64_t c = 0;
+    for (int i = 0; i < L; ++i) {
+      const uint32_t q = 0u - t[i];
+      uint64_t c = t[i] != 0u;
 #pragma unroll
-    for (int j = 0; j < L; ++j) {
-      c += (uint64_t)q * M.p[j] + t[i + j];
-      t[i + j] = (uint32_t)c;
+      for (int j = i + 1; j < i + L - 1; ++j) {
+        c += t[j];
+        t[j] = (uint32_t)c;
+        c >>= 32;
+      }
+      c += (uint64_t)q * ptop + t[i + L - 1];
+      t[i + L - 1] = (uint32_t)c;
       c >>= 32;
+#pragma unroll
+      for (int j = i + L; j < 2 * L + 1; ++j) {
+        c += t[j];
+        t[j] = (uint32_t)c;
+        c >>= 32;
+      }
     }
+  } else {
 #pragma unroll
-    for (int j = i + L; j < 2 * L + 1; ++j) {
-      c += t[j];
-      t[j] = (uint32_t)c;
-      c >>= 32;
+    for (int i = 0; i < L; ++i) {
+      const uint32_t q = t[i] * M.pinv;
+      uint64_t c = 0;
+#pragma unroll
+      for (int j = 0; j < L; ++j) {
+        c += (uint64_t)q * M.p[j] + t[i + j];
+        t[i + j] = (uint32_t)c;
+        c >>= 32;
+      }
+#pragma unroll
+      for (int j = i + L; j < 2 * L + 1; ++j) {
+        c += t[j];
+        t[j] = (uint32_t)c;
+        c >>= 32;
+      }
     }
   }
   // v = t[L .. 2L] (L+1 limbs), v < (2^32 + 1) p.  Estimate floor(v/p) from the top limbs.
@@ -96,15 +124,27 @@ __device__ __forceinline__ void redc(uint32_t (&r)[L], uint32_t (&t)[2 * L + 1],
   const uint32_t qh = (uint32_t)__float2uint_rz(vf * M.pf_inv);
   // v -= qh * p
   uint32_t v[L + 1];
-  uint64_t c = 0;
-  int64_t br = 0;
+  if (M.proth) {
+    const uint64_t qp = (uint64_t)qh * M.p[L - 1];
+    int64_t br = 0;
 #pragma unroll
-  for (int j = 0; j <= L; ++j) {
-    const uint64_t prod = (j < L ? (uint64_t)qh * M.p[j] : 0ull) + c;
-    c = prod >> 32;
-    int64_t x = (int64_t)t[L + j] - (uint32_t)prod + br;
-    v[j] = (uint32_t)x;
-    br = x >> 32;
+    for (int j = 0; j <= L; ++j) {
+      const uint32_t sub = j == 0 ? qh : j == L - 1 ? (uint32_t)qp : j == L ? (uint32_t)(qp >> 32) : 0u;
+      int64_t x = (int64_t)t[L + j] - sub + br;
+      v[j] = (uint32_t)x;
+      br = x >> 32;
+    }
+  } else {
+    uint64_t c = 0;
+    int64_t br = 0;
+#pragma unroll
+    for (int j = 0; j <= L; ++j) {
+      const uint64_t prod = (j < L ? (uint64_t)qh * M.p[j] : 0ull) + c;
+      c = prod >> 32;
+      int64_t x = (int64_t)t[L + j] - (uint32_t)prod + br;
+      v[j] = (uint32_t)x;
+      br = x >> 32;
+    }
   }
   // qh overshoots by at most 1: negative -> add p once
   const bool neg = (int32_t)v[L] < 0;

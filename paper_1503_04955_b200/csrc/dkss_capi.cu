@@ -517,6 +517,12 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
   uint32_t inv = 1;
   for (int i = 0; i < 5; ++i) inv *= 2u - p[0] * inv;
   P->mc.pinv = 0u - inv;
+  {
+    bool pr = L >= 2 && p[0] == 1u;
+    for (int i = 1; i + 1 < L; ++i) pr = pr && p[i] == 0u;
+    const char* np = getenv("DKSS_NO_PROTH");
+    P->mc.proth = (pr && !(np && *np && *np != '0')) ? 1u : 0u;
+  }
   Limbs x(L, 0);
   x[0] = 1;
   for (int i = 0; i < 32 * L; ++i) dbl_mod(x, p);
