@@ -106,6 +106,7 @@ int dkss_mul_device(dkss_plan* plan, int batch, const uint32_t* a_dev, const uin
 #define DKSS_K_INV_PASS 3
 #define DKSS_K_DECODE1 4
 #define DKSS_K_DECODE2 5
+#define DKSS_K_ROWS 7 /* row phase in one cluster kernel (levels >= 1, pointwise, inverse levels >= 1) */
 #define DKSS_K_TRANSPOSE 6
 int dkss_profile_device(dkss_plan* plan, int batch, const uint32_t* a_dev, const uint32_t* b_dev, size_t n_limbs,
                         uint32_t* c_dev, void* stream, int max_launches, int32_t* kinds, float* ms, int64_t* work,

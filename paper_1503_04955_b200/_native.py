@@ -201,7 +201,7 @@ class DevicePlan:
                                          ctypes.c_void_p(c_ptr), nc, ctypes.c_void_p(stream)))
 
     KIND_NAMES = {0: "encode", 1: "fwd_pass", 2: "bottom", 3: "inv_pass", 4: "decode1", 5: "decode2",
-                  6: "transpose"}
+                  6: "transpose", 7: "rows"}
 
     def profile_device(self, batch: int, a_ptr: int, b_ptr: int, n_limbs: int, c_ptr: int, stream: int = 0):
         """Per-launch (kind, ms, limb-products, bytes) of one multiply, timed with CUDA events."""

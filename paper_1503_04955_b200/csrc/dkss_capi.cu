@@ -128,6 +128,8 @@ struct dkss_plan {
   int grid_fw = 0, grid_iw = 0;     // warp-per-column kernels (0 = not used)
   int grid_dft = 0, grid_tw = 0;    // split passes (column DFT kernel + elementwise twiddles)
   int pass_mode = 0;                // 0 auto, 1 CTA-fused, 2 warp-fused, 3 split
+  int rows_cs = 0;                  // >0: row phase in one cluster kernel (k_rows, cluster size)
+  void (*rows_fn)(RowsArgs, ModCtx) = nullptr;
   // workspace
   int cap_batch = 0;
   uint32_t* d_poly = nullptr;  // 2 * cap_batch polynomials
@@ -426,6 +428,36 @@ int launch_decode(dkss_plan* P, const uint32_t* v, uint32_t* out, int npoly, cud
   return 0;
 }
 
+// row phase (levels 1.. of both transforms and the pointwise products) in one cluster kernel
+int launch_rows(dkss_plan* P, uint32_t* a, const uint32_t* b, int batch, bool sq, cudaStream_t s) {
+  RowsArgs R{};
+  R.a = a;
+  R.b = b;
+  R.poly_words = P->poly_words;
+  R.rows = (long long)batch * 2 * P->m;
+  R.log_top_mu = P->log_top_mu;
+  R.twr = P->d_twr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(R.rows * P->rows_cs));
+  cfg.blockDim = dim3(P->kt.nt);
+  cfg.dynamicSmemBytes = P->kt.smem_rows;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = P->rows_cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  CUCHK(cudaLaunchKernelEx(&cfg, P->rows_fn, R, P->mc));
+  const long long lt1 = level_twiddles(P, 1);
+  mark(P, s, DKSS_K_ROWS, rp_work(P, (sq ? 2 : 3) * batch * lt1 + 2LL * P->M * batch),
+       (sq ? 2LL : 3LL) * batch * P->poly_words * 4);
+  return 0;
+}
+
 // whole multiply: operands already encoded-able in device memory
 // b == nullptr: squaring (one forward transform; the pointwise step multiplies each
 // transformed element by itself -- the reference's LL loop squares, bigmul/bench.py:214-215)
@@ -435,6 +467,14 @@ int run_mul(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, long 
   uint32_t* pa = P->d_poly;
   uint32_t* pb = sq ? pa : P->d_poly + (size_t)batch * P->poly_words;
   int rc;
+  if (P->rows_cs) {
+    // level 0 (with the encode) over columns; everything inside a row in one cluster kernel;
+    // level 0 of the inverse with the 1/2M scale
+    if ((rc = launch_fwd_levels(P, P->d_poly, (sq ? 1 : 2) * batch, s, a, b, nl, batch, 0, 1))) return rc;
+    if ((rc = launch_rows(P, pa, pb, batch, sq, s))) return rc;
+    if ((rc = launch_inv_levels(P, pa, batch, true, s, 0, 1))) return rc;
+    return launch_decode(P, pa, prod, batch, s);
+  }
   if (P->levels > 0) {
     // encode fused into the first forward pass
     if ((rc = launch_fwd_levels(P, P->d_poly, (sq ? 1 : 2) * batch, s, a, b, nl, batch))) return rc;
@@ -583,6 +623,41 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
     }
     const char* pm = getenv("DKSS_PASS_MODE");
     if (pm) P->pass_mode = atoi(pm);
+    // row phase in one cluster kernel: two column levels, base length b = cluster size.
+    // Opt-in (DKSS_ROWS=1): measured slower than the three persistent launches it replaces
+    // -- second-level column 0 has no twiddles, so one CTA of every
+    // cluster idles through both level-1 phases, and the cluster barriers keep the CTAs in
+    // lockstep where the persistent kernels overlap tiles
+    const char* nr = getenv("DKSS_ROWS");
+    const int b = P->base_len;
+    const int ri = b == 2 ? 1 : b == 4 ? 2 : b == 8 ? 3 : b == 16 ? 4 : 0;
+    if (P->levels == 2 && ri && kt.rows[ri] && nr && *nr && *nr != '0') {
+      auto fn = kt.rows[ri];
+      bool ok = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kt.smem_rows) ==
+                cudaSuccess;
+      if (ok && b > 8)
+        ok = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+      if (ok) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(b * 2 * m);
+        cfg.blockDim = dim3(kt.nt);
+        cfg.dynamicSmemBytes = kt.smem_rows;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = b;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        ok = cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) == cudaSuccess && ncl > 0;
+      }
+      cudaGetLastError();  // a refused configuration keeps the three-launch row phase
+      if (ok) {
+        P->rows_cs = b;
+        P->rows_fn = fn;
+      }
+    }
   }
   // cbias = -(2^(32L) - 1) * R mod p = (p - ((R mod p) - 1)) * R mod p  (ring_mul bias correction)
   {
@@ -652,7 +727,7 @@ int dkss_plan_get_info(const dkss_plan* P, dkss_plan_info* o) {
   o->product_limbs = P->prod_limbs;
   o->twiddles_per_fft = P->twiddles;
   o->ring_products = 3 * P->twiddles + 2LL * P->M;
-  o->launches_per_mul = (P->levels > 0 ? 0 : 2) + P->levels + 1 + P->levels + 3;
+  o->launches_per_mul = P->rows_cs ? 1 + 1 + 1 + 3 : (P->levels > 0 ? 0 : 2) + P->levels + 1 + P->levels + 3;
   o->workspace_bytes = (int64_t)P->ws_bytes;
   return DKSS_OK;
 }

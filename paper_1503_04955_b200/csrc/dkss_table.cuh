@@ -3,6 +3,7 @@
 #pragma once
 #include "dkss_kernels.cuh"
 #include "dkss_warp.cuh"
+#include "dkss_rows.cuh"
 
 namespace dkss {
 
@@ -25,6 +26,10 @@ struct KTable {
   size_t smem_pass;   // dynamic shared memory bytes: column passes
   size_t smem_bot;    // bottom kernel
   size_t smem_rmul;   // standalone ring product
+  // row phase of two-level plans in one cluster kernel (dkss_rows.cuh), by cluster size
+  // CS = base length b in {2, 4, 8, 16}; null where not instantiated
+  void (*rows[5])(RowsArgs, ModCtx);
+  size_t smem_rows;
 };
 
 template <int MM, int L>
@@ -45,6 +50,13 @@ KTable make_table() {
     t.smem_fwd_w = t.smem_inv_w = 0;
   }
   t.bottom = k_bottom<MM, L>;
+  if constexpr (MM == 16 || MM == 32) {
+    t.rows[1] = k_rows<MM, L, 2>;
+    t.rows[2] = k_rows<MM, L, 4>;
+    t.rows[3] = k_rows<MM, L, 8>;
+    t.rows[4] = k_rows<MM, L, 16>;
+    t.smem_rows = RowsSmem<MM, L>::WORDS * 4;
+  }
   t.rmul = k_rmul<MM, L>;
   t.mscale = k_mont_scale<L>;
   t.build_twr = k_build_twr<L>;

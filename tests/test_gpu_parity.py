@@ -167,7 +167,8 @@ def test_device_api_graph_replay(cuda_ok):
         assert [u32_to_int(row) for row in out] == [a * b for a, b in pairs]
     prof = dp.profile_device(4, A.data_ptr(), B.data_ptr(), nl, C.data_ptr(), s)
     kinds = [k for k, *_ in prof]
-    assert kinds.count("fwd_pass") == pl.levels and kinds.count("inv_pass") == pl.levels
+    levels_in_passes = 1 if "rows" in kinds else pl.levels  # DKSS_ROWS=1: levels >= 1 run in k_rows
+    assert kinds.count("fwd_pass") == levels_in_passes and kinds.count("inv_pass") == levels_in_passes
     assert all(ms > 0 for _, ms, _, _ in prof)
 
 
@@ -280,3 +281,21 @@ def test_dmul_chain_natural_operands(cuda_ok, rng):
     abc = dmul(ab, c)
     assert abc.to_int() == a * b * c and len(abc) == len(ab) + -(-c.bit_length() // 64)
     assert dmul(c, Natural.from_int(a)).to_int() == a * c
+
+
+# --- row phase in one cluster kernel (k_rows): every two-level plan size, multiply and square
+@pytest.mark.parametrize("e", [18, 19, 21, 22, 23])
+def test_dmul_two_level_plans(cuda_ok, e):
+    rng = random.Random(500 + e)
+    N = 1 << e
+    a = rng.getrandbits(N) | 1 << (N - 1)
+    b = rng.getrandbits(N - 3)
+    assert dmul(a, b).to_int() == a * b
+    assert dmul(a, a).to_int() == a * a  # squaring mode (same object -> one forward transform)
+
+
+def test_square_batch_and_all_ones(cuda_ok):
+    rng = random.Random(9)
+    xs = [rng.getrandbits(1 << 18) for _ in range(5)] + [(1 << (1 << 18)) - 1]
+    got = dmul_many([(x, x) for x in xs])
+    assert [g.to_int() for g in got] == [x * x for x in xs]
