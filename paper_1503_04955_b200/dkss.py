@@ -57,8 +57,16 @@ def _plan_for(N: int, w: int) -> DkssPlan:
     return pl
 
 
+_env_device: tuple = (None, 0)
+
+
 def _device() -> int:
-    return int(os.environ.get("DKSS_DEVICE", "0"))
+    """GPU ordinal from DKSS_DEVICE (default 0); the parsed value is cached per env string."""
+    global _env_device
+    raw = os.environ.get("DKSS_DEVICE", "0")
+    if raw != _env_device[0]:
+        _env_device = (raw, int(raw))
+    return _env_device[1]
 
 
 def device_plan(plan: DkssPlan, device: int | None = None) -> DevicePlan:
@@ -182,6 +190,24 @@ def _digits(x, value: int):
     return arr, arr.ctypes.data, arr.size, 32
 
 
+_hot: dict = {}
+
+
+def _hot_plan(N: int, w: int):
+    """(plan, device plan, operand limbs, product limbs, workspace words, r_mul count), cached
+    per (N, w, device) so a multiply does no per-call plan bookkeeping."""
+    key = (N, w, _device())
+    ent = _hot.get(key)
+    if ent is None:
+        plan = _plan_for(N, w)
+        dp = device_plan(plan, key[2])
+        info = dp.info
+        ent = (plan, dp, info["operand_limbs"], info["product_limbs"], 2 * info["poly_bytes"],
+               ring_products_per_multiply(plan))
+        _hot[key] = ent
+    return ent
+
+
 def dmul(a, b, thresholds=None, arena: ScratchArena | None = None) -> Natural:
     """Full product via DKSS on the GPU (bigmul/dkss.py:520-548)."""
     w = word_bits()
@@ -192,23 +218,22 @@ def dmul(a, b, thresholds=None, arena: ScratchArena | None = None) -> Natural:
     if ai == 0 or bi == 0:
         return Natural([0] * outlen)
     n_bits = max(ai.bit_length(), bi.bit_length())
-    N = max(n_bits, _MIN_PLAN_BITS)
-    plan = _plan_for(N, w)
-    dp = device_plan(plan)
-    info = dp.info
-    nl = info["operand_limbs"]
-    nc = max(info["product_limbs"], -(-outlen * w // 32))
-    with arena.frame():
+    plan, dp, nl, npl, poly2_bytes, rp = _hot_plan(max(n_bits, _MIN_PLAN_BITS), w)
+    nc = max(npl, -(-outlen * w // 32))
+    mark = arena.acquire()
+    try:
         # device workspace per multiply: 2 polynomials + operands + product, in words
-        arena.alloc_words((2 * info["poly_bytes"] + 4 * (2 * nl + nc)) * 8 // w)
+        arena.alloc_words((poly2_bytes + 4 * (2 * nl + nc)) * 8 // w)
         ka, pa, na, ba = _digits(a, ai)
-        kb, pb, nb, bb = _digits(b, bi)
+        kb, pb, nb, bb = (ka, pa, na, ba) if b is a else _digits(b, bi)
         if ba == bb:
             c = dp.mul_digits(pa, na, pb, nb, ba, nc)
         else:
             c = dp.mul_limbs(int_to_u32(ai, nl), int_to_u32(bi, nl), nc)
         del ka, kb
-    plan.ks_calls += ring_products_per_multiply(plan)
+    finally:
+        arena.release(mark)
+    plan.ks_calls += rp
     return Natural._from_u32(c, outlen, w)
 
 
