@@ -716,21 +716,25 @@ __device__ __forceinline__ void issue_bottom_tile(const BottomArgs& A, long long
                                                   uint32_t* sb) {
   constexpr int ES = Smem<MM, L>::ES, NE = Cfg<MM>::NE;
   constexpr uint32_t EB = MM * L * 4;
-  const int lane = threadIdx.x & 31;
+  constexpr int NW = kSpreadIssue ? Cfg<MM>::NT / 32 : 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool two = A.mode != 0;
   const long long e0 = tile * NE;
   const int bmask = (1 << A.logb) - 1;
-  uint32_t bytes = 0;
-  for (int el = lane; el < NE; el += 32)
-    if (e0 + el < A.total_elems) bytes += two ? 2 * EB : EB;
-  bytes = __reduce_add_sync(0xFFFFFFFFu, bytes);
-  if (lane == 0) mbar_expect_tx(bar, bytes);
-  __syncwarp();
-  for (int el = lane; el < NE; el += 32) {
-    if (e0 + el >= A.total_elems) continue;
+  if (warp == 0) {
+    const long long n = A.total_elems - e0 < NE ? A.total_elems - e0 : NE;
+    if (lane == 0) mbar_expect_tx(bar, (uint32_t)n * (two ? 2 * EB : EB));
+    __syncwarp();
+  }
+  // copies spread over the calling warps (see issue_pass_tile)
+  for (int q = warp + NW * lane; q < 2 * NE; q += NW * 32) {
+    const int el = q % NE;
+    if (e0 + el >= A.total_elems || (q >= NE && !two)) continue;
     const int slot = (el & ~bmask) | bitrev_n(el & bmask, A.logb);
-    bulk_g2s(sa + slot * ES, A.a + (e0 + el) * (MM * L), EB, bar);
-    if (two) bulk_g2s(sb + slot * ES, A.b + (e0 + el) * (MM * L), EB, bar);
+    if (q < NE)
+      bulk_g2s(sa + slot * ES, A.a + (e0 + el) * (MM * L), EB, bar);
+    else
+      bulk_g2s(sb + slot * ES, A.b + (e0 + el) * (MM * L), EB, bar);
   }
 }
 
@@ -756,13 +760,14 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_bottom(BottomArg
   }
   __syncthreads();
   long long tile = blockIdx.x;
-  if (tile < ntiles && threadIdx.x < 32) issue_bottom_tile<MM, L>(A, tile, &bar[0], smem, smem + NE * ES);
+  if (tile < ntiles && (kSpreadIssue || threadIdx.x < 32))
+    issue_bottom_tile<MM, L>(A, tile, &bar[0], smem, smem + NE * ES);
   for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
     const int st = NS == 2 ? (k & 1) : 0;
     uint32_t* sa = smem + st * STAGE;
     uint32_t* sb = sa + NE * ES;
     const long long nxt = tile + gridDim.x;
-    if (NS == 2 && nxt < ntiles && threadIdx.x < 32)
+    if (NS == 2 && nxt < ntiles && (kSpreadIssue || threadIdx.x < 32))
       issue_bottom_tile<MM, L>(A, nxt, &bar[st ^ 1], smem + (st ^ 1) * STAGE, smem + (st ^ 1) * STAGE + NE * ES);
     mbar_wait(&bar[st], NS == 2 ? ((k >> 1) & 1) : (k & 1));
     const long long e0 = tile * NE;
@@ -812,7 +817,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_bottom(BottomArg
     }
     fence_proxy_async();
     __syncthreads();
-    if (NS == 1 && nxt < ntiles && threadIdx.x < 32) issue_bottom_tile<MM, L>(A, nxt, &bar[0], smem, smem + NE * ES);
+    if (NS == 1 && nxt < ntiles && (kSpreadIssue || threadIdx.x < 32)) issue_bottom_tile<MM, L>(A, nxt, &bar[0], smem, smem + NE * ES);
   }
 }
 
