@@ -41,10 +41,10 @@ KTable make_table() {
   if constexpr (MM <= 16) {
     t.fwd_w = k_fwd_warp<MM, L>;
     t.inv_w = k_inv_warp<MM, L>;
-    t.smem_fwd_w = (size_t)kWarpsPerCta * 2 * (2 * MM) * Smem<MM, L>::ES * 4;  // double-buffered
-    t.smem_inv_w = t.smem_fwd_w;
+    t.smem_fwd_w = (size_t)kWarpsPerCta * 2 * MM * Smem<MM, L>::ES * 4;
+    t.smem_inv_w = 2 * t.smem_fwd_w;
     t.dft = k_dft_cols<MM, L>;
-    t.smem_dft = t.smem_fwd_w / 2;
+    t.smem_dft = t.smem_fwd_w;
   } else {
     t.fwd_w = t.inv_w = nullptr;
     t.smem_fwd_w = t.smem_inv_w = 0;

@@ -16,6 +16,14 @@
 namespace dkss {
 
 constexpr int kWarpsPerCta = 4;
+// resident CTAs per SM the warp-per-column kernels are register-capped for: the forward
+// kernel (one column slice per warp) fits 4 per SM, the inverse (two slices) 3
+#ifndef DKSS_WARP_MINB_FWD
+#define DKSS_WARP_MINB_FWD 4
+#endif
+#ifndef DKSS_WARP_MINB_INV
+#define DKSS_WARP_MINB_INV 3
+#endif
 
 template <int MM>
 struct WG {
@@ -131,40 +139,33 @@ __device__ __forceinline__ void encode_coef(const PassArgs& A, long long cg, int
 
 // forward column pass, warp per column (A.wpc warps per column)
 template <int MM, int L>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_fwd_warp(PassArgs A, ModCtx mc) {
+__global__ void __launch_bounds__(kWarpsPerCta * 32, DKSS_WARP_MINB_FWD) k_fwd_warp(PassArgs A, ModCtx mc) {
   griddep_wait();  // PDL: predecessor grid complete, its writes visible
   griddep_launch();
   constexpr int kT = Cfg<MM>::T;
   constexpr int ES = Smem<MM, L>::ES, E = 2 * MM, EPT = WG<MM>::EPT, TPE = MM / kT;
   extern __shared__ __align__(16) uint32_t smem[];
-  __shared__ __align__(8) uint64_t bars[2 * kWarpsPerCta];
+  __shared__ __align__(8) uint64_t bars[kWarpsPerCta];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = lane & (MM - 1), g = lane / MM;
-  uint32_t* bufs = smem + warp * 2 * E * ES;  // two column slices: load k+1 while k computes
-  uint64_t* bar = &bars[2 * warp];
-  if (lane == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-  }
+  uint32_t* buf = smem + warp * E * ES;
+  uint64_t* bar = &bars[warp];
+  if (lane == 0) mbar_init(bar, 1);
   __syncwarp();
   const long long gw = (long long)blockIdx.x * kWarpsPerCta + warp;
   const long long nw = (long long)gridDim.x * kWarpsPerCta;
   const int wpc = A.wpc, part = (int)(gw % wpc);
   const bool enc = A.ops_a != nullptr;
-  const long long step = nw / wpc;
-  if (!enc && gw / wpc < A.total_cols) warp_issue_column<MM, L, true>(A, gw / wpc, &bar[0], bufs);
-  int k = 0;
-  for (long long cg = gw / wpc; cg < A.total_cols; cg += step, ++k) {
+  uint32_t phase = 0;
+  for (long long cg = gw / wpc; cg < A.total_cols; cg += nw / wpc) {
     uint32_t X[EPT][L];
-    uint32_t* buf = bufs + (k & 1) * E * ES;
     if (enc) {
 #pragma unroll
       for (int i = 0; i < EPT; ++i) encode_coef<MM, L>(A, cg, bitrev_n(g * EPT + i, WG<MM>::LOGE), c, X[i]);
     } else {
-      // the other slice finished with column k-1 (fence + syncwarp at the end of the loop)
-      if (cg + step < A.total_cols)
-        warp_issue_column<MM, L, true>(A, cg + step, &bar[(k & 1) ^ 1], bufs + ((k & 1) ^ 1) * E * ES);
-      mbar_wait(&bar[k & 1], (k >> 1) & 1);
+      warp_issue_column<MM, L, true>(A, cg, bar, buf);
+      mbar_wait(bar, phase);
+      phase ^= 1;
 #pragma unroll
       for (int i = 0; i < EPT; ++i) ld_res<L>(X[i], buf + (g * EPT + i) * ES + c * L);
     }
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_fwd_warp(PassArgs A, M
 // inverse (transposed) column pass, warp per column: twiddle products into a result slice at
 // bit-reversed slots, then the register DFT, then the store (optionally scaled by kscale)
 template <int MM, int L>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_inv_warp(PassArgs A, ModCtx mc) {
+__global__ void __launch_bounds__(kWarpsPerCta * 32, DKSS_WARP_MINB_INV) k_inv_warp(PassArgs A, ModCtx mc) {
   griddep_wait();  // PDL: predecessor grid complete, its writes visible
   griddep_launch();
   constexpr int kT = Cfg<MM>::T;
