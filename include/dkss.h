@@ -79,6 +79,9 @@ int dkss_mul(dkss_plan* plan, const uint32_t* a, size_t na, const uint32_t* b, s
  * is written as nc 32-bit limbs, as dkss_mul. */
 int dkss_mul_digits(dkss_plan* plan, const uint32_t* a, size_t na, const uint32_t* b, size_t nb, int digit_bits,
                     uint32_t* c, size_t nc);
+/* OR into digit_bits when every digit is known to be < 2^digit_bits (e.g. a CPython int's
+ * digits): the library then skips its scan of the digit strings */
+#define DKSS_DIGITS_TRUSTED 0x100
 /* batched form: pair i is a[i] (na[i] digits) x b[i] (nb[i] digits); c is batch x nc limbs */
 int dkss_mul_batch_digits(dkss_plan* plan, int batch, const uint32_t* const* a, const size_t* na,
                           const uint32_t* const* b, const size_t* nb, int digit_bits, uint32_t* c, size_t nc);

@@ -27,6 +27,7 @@ EXPORTS = (
 )
 
 DKSS_OK, DKSS_EINVAL, DKSS_ECUDA, DKSS_ERANGE, DKSS_ENOMEM = 0, -1, -2, -3, -4
+DKSS_DIGITS_TRUSTED = 0x100  # digit_bits flag: digits already known to fit (include/dkss.h)
 
 
 class NativeUnavailable(RuntimeError):

@@ -10,6 +10,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <chrono>
 #include <tuple>
 #include <vector>
 
@@ -146,6 +147,7 @@ struct dkss_plan {
   cudaStream_t stream = nullptr;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   std::map<std::pair<long long, int>, cudaGraphExec_t> ll_graphs;  // (p, iterations per graph)
+  std::map<std::tuple<int, bool, int>, cudaGraphExec_t> dgraphs;   // host digits path: (batch, square, bits)
   std::mutex mu;
   struct Prof {
     static constexpr int kMax = 64;
@@ -172,6 +174,8 @@ void free_ws(dkss_plan* P) {
   P->graphs.clear();
   for (auto& kv : P->ll_graphs) cudaGraphExecDestroy(kv.second);
   P->ll_graphs.clear();
+  for (auto& kv : P->dgraphs) cudaGraphExecDestroy(kv.second);
+  P->dgraphs.clear();
   P->cap_batch = 0;
   P->ws_bytes = 0;
 }
@@ -195,6 +199,8 @@ int ensure_ws(dkss_plan* P, int batch) {
 
 int ensure_pin(dkss_plan* P, size_t words) {
   if (words <= P->h_pin_words) return 0;
+  for (auto& kv : P->dgraphs) cudaGraphExecDestroy(kv.second);  // they copy to/from h_pin
+  P->dgraphs.clear();
   if (P->h_pin) cudaFreeHost(P->h_pin);
   P->h_pin = nullptr;
   CUCHK(cudaMallocHost(&P->h_pin, words * 4));
@@ -852,6 +858,36 @@ int dkss_mul_batch(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b
 }  // extern "C"
 
 namespace {
+// DKSS_HOST_TIMING=1: host-side phase times of the host-buffer multiply, to stderr
+struct HostTimer {
+  bool on;
+  std::chrono::steady_clock::time_point t0, last;
+  char buf[512];
+  int n = 0;
+  HostTimer() {
+    const char* e = getenv("DKSS_HOST_TIMING");
+    on = e && *e && *e != '0';
+    t0 = last = std::chrono::steady_clock::now();
+    buf[0] = 0;
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    n += snprintf(buf + n, sizeof buf - n, " %s=%.1f", what,
+                  std::chrono::duration<double, std::micro>(now - last).count());
+    last = now;
+  }
+  ~HostTimer() {
+    if (on)
+      fprintf(stderr, "dkss host us:%s total=%.1f\n", buf,
+              std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
+thread_local HostTimer* g_ht = nullptr;
+void ht_mark(const char* w) {
+  if (g_ht) g_ht->mark(w);
+}
+
 // fn(i) for i in [0, n), spread over up to 8 host threads when `bytes` of copying is large
 template <class F>
 void host_par(size_t n, size_t bytes, F fn) {
@@ -869,38 +905,76 @@ void host_par(size_t n, size_t bytes, F fn) {
   for (auto& x : th) x.join();
 }
 
-// validate `nops` digit strings, pack them (offsets, then digits) into pinned staging, copy
-// to the device and repack into 32-bit limbs at d_ops (operand q at d_ops + q*op_limbs)
-int stage_digits(dkss_plan* P, int nops, const uint32_t* const* ptrs, const size_t* counts, int digit_bits,
-                 cudaStream_t s) {
-  std::vector<size_t> nd(nops);
-  size_t total = 0;
+}  // namespace
+
+namespace {
+// Host digit strings -> products in ONE graph launch: H2D of the staging buffer (offsets +
+// digits, sized for the largest operands the plan admits), radix repack, the multiply,
+// D2H of the products; the host only validates, packs and unpacks.
+int run_digits_graph(dkss_plan* P, int batch, bool sq, int nops, const uint32_t* const* ptrs, const size_t* counts,
+                     int digit_bits, bool trusted, uint32_t* c, size_t nc) {
+  std::vector<size_t> nd((size_t)nops);
   for (int q = 0; q < nops; ++q) {
     const uint32_t* d = ptrs[q];
     size_t n = counts[q];
     if (n && !d) return fail(DKSS_EINVAL, "null digit pointer");
     while (n > 0 && d[n - 1] == 0) --n;
-    if (digit_bits < 32) {
+    if (digit_bits < 32 && !trusted) {
       uint32_t any = 0;
       for (size_t i = 0; i < n; ++i) any |= d[i];
       if (any >> digit_bits) return fail(DKSS_EINVAL, "a digit exceeds %d bits", digit_bits);
     }
     if (n) {  // value < 2^N (bigmul/dkss.py:389-390)
-      const long long bits = (long long)(n - 1) * digit_bits + (32 - __builtin_clz(d[n - 1]));
+      const uint32_t top = d[n - 1];
+      if (digit_bits < 32 && (top >> digit_bits)) return fail(DKSS_EINVAL, "a digit exceeds %d bits", digit_bits);
+      const long long bits = (long long)(n - 1) * digit_bits + (32 - __builtin_clz(top));
       if (bits > P->N) return fail(DKSS_ERANGE, "operand does not fit the plan (%lld bits > N=%lld)", bits, P->N);
     }
     nd[q] = n;
-    total += n;
   }
-  const size_t head = 2 * (size_t)(nops + 1);  // long long offsets, in u32 words
-  const size_t words = head + total;
+  ht_mark("validate");
+  const size_t head = 2 * ((size_t)nops + 1);  // long long offsets, in u32 words
+  const size_t dmax = (size_t)((P->N + digit_bits - 1) / digit_bits);
+  const size_t cap = head + (size_t)nops * dmax;
+  const size_t prw = (size_t)batch * P->prod_limbs;
   int rc;
-  if ((rc = ensure_pin(P, words))) return rc;
-  if (words > P->stage_words) {
+  if ((rc = ensure_pin(P, std::max(cap, prw)))) return rc;
+  if (cap > P->stage_words) {
+    for (auto& kv : P->dgraphs) cudaGraphExecDestroy(kv.second);
+    P->dgraphs.clear();
     cudaFree(P->d_stage);
     P->d_stage = nullptr;
-    CUCHK(cudaMalloc(&P->d_stage, words * 4));
-    P->stage_words = words;
+    CUCHK(cudaMalloc(&P->d_stage, cap * 4));
+    P->stage_words = cap;
+  }
+  auto key = std::make_tuple(batch, sq, digit_bits);
+  auto it = P->dgraphs.find(key);
+  if (it == P->dgraphs.end()) {
+    cudaStream_t cap_s;
+    CUCHK(cudaStreamCreateWithFlags(&cap_s, cudaStreamNonBlocking));
+    CUCHK(cudaStreamBeginCapture(cap_s, cudaStreamCaptureModeThreadLocal));
+    cudaMemcpyAsync(P->d_stage, P->h_pin, cap * 4, cudaMemcpyHostToDevice, cap_s);
+    RepackArgs R{};
+    R.stage = P->d_stage + head;
+    R.off = reinterpret_cast<const long long*>(P->d_stage);
+    R.dst = P->d_ops;
+    R.ndst = P->op_limbs;
+    R.sbits = digit_bits;
+    const int gx = (int)std::max<long long>(1, std::min<long long>((P->op_limbs + 255) / 256, 1184 / nops + 1));
+    launch_k(k_repack_bits, dim3(gx, nops), dim3(256), 0, cap_s, R);
+    const uint32_t* bo = sq ? nullptr : P->d_ops + (size_t)batch * P->op_limbs;
+    rc = run_mul(P, batch, P->d_ops, bo, P->op_limbs, P->d_prod, cap_s);
+    cudaMemcpyAsync(P->h_pin, P->d_prod, prw * 4, cudaMemcpyDeviceToHost, cap_s);
+    cudaGraph_t g;
+    cudaError_t e = cudaStreamEndCapture(cap_s, &g);
+    cudaStreamDestroy(cap_s);
+    if (rc) return rc;
+    if (e != cudaSuccess) return fail(DKSS_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
+    cudaGraphExec_t ge;
+    e = cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(DKSS_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+    it = P->dgraphs.emplace(key, ge).first;
   }
   long long* off = reinterpret_cast<long long*>(P->h_pin);
   uint32_t* dig = P->h_pin + head;
@@ -910,31 +984,14 @@ int stage_digits(dkss_plan* P, int nops, const uint32_t* const* ptrs, const size
     o += (long long)nd[q];
   }
   off[nops] = o;
-  host_par((size_t)nops, total * 4, [&](size_t q) {
+  host_par((size_t)nops, (size_t)o * 4, [&](size_t q) {
     if (nd[q]) memcpy(dig + off[q], ptrs[q], nd[q] * 4);
   });
-  CUCHK(cudaMemcpyAsync(P->d_stage, P->h_pin, words * 4, cudaMemcpyHostToDevice, s));
-  RepackArgs R{};
-  R.stage = P->d_stage + head;
-  R.off = reinterpret_cast<const long long*>(P->d_stage);
-  R.dst = P->d_ops;
-  R.ndst = P->op_limbs;
-  R.sbits = digit_bits;
-  const int gx = (int)std::max<long long>(1, std::min<long long>((P->op_limbs + 255) / 256, 1184 / nops + 1));
-  launch_k(k_repack_bits, dim3(dim3(gx, nops)), dim3(256), 0, s, R);
-  CUCHK(cudaGetLastError());
-  return 0;
-}
-
-// products of `batch` staged operand pairs (d_ops) -> host c (batch x nc limbs)
-int run_staged(dkss_plan* P, int batch, bool sq, uint32_t* c, size_t nc, cudaStream_t s) {
-  int rc;
-  const size_t prw = (size_t)batch * P->prod_limbs;
-  const uint32_t* b = sq ? nullptr : P->d_ops + (size_t)batch * P->op_limbs;
-  if ((rc = launch_graph(P, batch, P->d_ops, b, (size_t)P->op_limbs, P->d_prod, P->prod_limbs, s))) return rc;
-  if ((rc = ensure_pin(P, prw))) return rc;
-  CUCHK(cudaMemcpyAsync(P->h_pin, P->d_prod, prw * 4, cudaMemcpyDeviceToHost, s));
-  CUCHK(cudaStreamSynchronize(s));
+  ht_mark("stage_copy");
+  CUCHK(cudaGraphLaunch(it->second, P->stream));
+  ht_mark("graph_launch");
+  CUCHK(cudaStreamSynchronize(P->stream));
+  ht_mark("sync");
   const size_t ncopy = std::min<size_t>(nc, P->prod_limbs);
   std::vector<char> over((size_t)batch, 0);
   host_par((size_t)batch, prw * 4, [&](size_t i) {
@@ -945,6 +1002,7 @@ int run_staged(dkss_plan* P, int batch, bool sq, uint32_t* c, size_t nc, cudaStr
       if (src[k]) over[i] = 1;
     if (nc > ncopy) memset(dst + ncopy, 0, (nc - ncopy) * 4);
   });
+  ht_mark("copy_out");
   for (int i = 0; i < batch; ++i)
     if (over[i]) return fail(DKSS_ERANGE, "product %d does not fit nc=%zu limbs", i, nc);
   return DKSS_OK;
@@ -956,6 +1014,8 @@ extern "C" {
 int dkss_mul_batch_digits(dkss_plan* P, int batch, const uint32_t* const* a, const size_t* na,
                           const uint32_t* const* b, const size_t* nb, int digit_bits, uint32_t* c, size_t nc) {
   if (!P || batch < 1 || !a || !na || !b || !nb || !c) return fail(DKSS_EINVAL, "bad argument");
+  const bool trusted = digit_bits & DKSS_DIGITS_TRUSTED;
+  digit_bits &= ~DKSS_DIGITS_TRUSTED;
   if (digit_bits < 8 || digit_bits > 32) return fail(DKSS_EINVAL, "digit_bits=%d outside [8, 32]", digit_bits);
   if (2LL * batch > 65535) return fail(DKSS_EINVAL, "batch %d too large", batch);
   bool sq = true;  // every pair is (x, x): square (one forward transform)
@@ -979,8 +1039,11 @@ int dkss_mul_batch_digits(dkss_plan* P, int batch, const uint32_t* const* a, con
   if ((rc = ensure_ws(P, batch))) return rc;
   // staging sized once for both directions: it must not be reallocated while a copy is in flight
   if ((rc = ensure_pin(P, std::max<size_t>(total, (size_t)batch * (size_t)P->prod_limbs)))) return rc;
-  if ((rc = stage_digits(P, nops, ptrs.data(), counts.data(), digit_bits, P->stream))) return rc;
-  return run_staged(P, batch, sq, c, nc, P->stream);
+  HostTimer ht;
+  g_ht = &ht;
+  rc = run_digits_graph(P, batch, sq, nops, ptrs.data(), counts.data(), digit_bits, trusted, c, nc);
+  g_ht = nullptr;
+  return rc;
 }
 
 int dkss_mul_digits(dkss_plan* P, const uint32_t* a, size_t na, const uint32_t* b, size_t nb, int digit_bits,

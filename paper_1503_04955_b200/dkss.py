@@ -24,7 +24,7 @@ import threading
 
 import numpy as np
 
-from ._native import DevicePlan
+from ._native import DKSS_DIGITS_TRUSTED, DevicePlan
 from .plan import DkssPlan, dkss_select_params, ring_products_per_multiply, twiddle_count
 from .words import (Natural, ScratchArena, as_natural, current_arena, int_to_u32, pylong_digits, u32_to_int,
                     word_bits, PYLONG_DIGIT_BITS)
@@ -184,8 +184,8 @@ def _digits(x, value: int):
         arr = np.ascontiguousarray(x._limbs, dtype=np.uint32)
         return arr, arr.ctypes.data, arr.size, 32
     d = pylong_digits(value)
-    if d is not None:
-        return value, d[0], d[1], PYLONG_DIGIT_BITS
+    if d is not None:  # CPython keeps every digit below 2^30: no scan needed
+        return value, d[0], d[1], PYLONG_DIGIT_BITS | DKSS_DIGITS_TRUSTED
     arr = int_to_u32(value, max(1, -(-value.bit_length() // 32)))
     return arr, arr.ctypes.data, arr.size, 32
 
