@@ -130,6 +130,8 @@ struct dkss_plan {
   int grid_dft = 0, grid_tw = 0;    // split passes (column DFT kernel + elementwise twiddles)
   int pass_mode = 0;                // 0 auto, 1 CTA-fused, 2 warp-fused, 3 split
   int rows_cs = 0;                  // >0: row phase in one cluster kernel (k_rows, cluster size)
+  int dyn_grid = 0;                 // >0: row phase as one persistent dependency-driven kernel
+  unsigned* d_dyn = nullptr;        // its ticket + per-row counters (cap_batch rows)
   void (*rows_fn)(RowsArgs, ModCtx) = nullptr;
   // workspace
   int cap_batch = 0;
@@ -169,6 +171,8 @@ void free_ws(dkss_plan* P) {
   cudaFree(P->d_gmask);
   cudaFree(P->d_pmask);
   cudaFree(P->d_bstat);
+  cudaFree(P->d_dyn);
+  P->d_dyn = nullptr;
   P->d_poly = P->d_ops = P->d_prod = P->d_gmask = P->d_pmask = P->d_bstat = nullptr;
   for (auto& kv : P->graphs) cudaGraphExecDestroy(kv.second);
   P->graphs.clear();
@@ -191,6 +195,8 @@ int ensure_ws(dkss_plan* P, int batch) {
   CUCHK(cudaMalloc(&P->d_gmask, (size_t)batch * nwarps * 4));
   CUCHK(cudaMalloc(&P->d_pmask, (size_t)batch * nwarps * 4));
   CUCHK(cudaMalloc(&P->d_bstat, (size_t)batch * dec_blocks(P) * 4));
+  CUCHK(cudaMalloc(&P->d_dyn, (4 + 2 * (size_t)batch * 2 * P->m) * 4));
+  CUCHK(cudaMemset(P->d_dyn, 0, (4 + 2 * (size_t)batch * 2 * P->m) * 4));
   P->cap_batch = batch;
   P->ws_bytes = 2 * (size_t)batch * poly_b + 2 * (size_t)batch * P->op_limbs * 4 + (size_t)batch * P->prod_limbs * 4 +
                 (size_t)batch * nwarps * 8 + (size_t)batch * dec_blocks(P) * 4;
@@ -464,6 +470,37 @@ int launch_rows(dkss_plan* P, uint32_t* a, const uint32_t* b, int batch, bool sq
   return 0;
 }
 
+// row phase (levels 1.. of both transforms, pointwise, inverse levels 1..) as one persistent
+// kernel with per-row dependency counters (dkss_dyn.cuh)
+int launch_dyn(dkss_plan* P, uint32_t* a, const uint32_t* b, int batch, bool sq, cudaStream_t s) {
+  const int E = 2 * P->m;
+  DynArgs R{};
+  R.a = a;
+  R.b = b;
+  R.poly_words = P->poly_words;
+  R.batch = batch;
+  R.npolys_fwd = sq ? 1 : 2;
+  R.log_mu0 = P->log_top_mu;
+  R.log_mu1 = P->log_top_mu - P->logE;
+  R.log_top_mu = P->log_top_mu;
+  R.logb = P->logb;
+  R.twr = P->d_twr;
+  R.ticket = P->d_dyn;
+  R.fwd_done = P->d_dyn + 4;
+  R.bot_done = P->d_dyn + 4 + (size_t)batch * E;
+  const unsigned rows = (unsigned)batch * E, mu1 = 1u << R.log_mu1;
+  R.n_f = rows * R.npolys_fwd * mu1;
+  R.n_b = rows * (unsigned)((1LL << R.log_mu0) / P->kt.ne);
+  R.n_i = rows * mu1;
+  R.rows = rows;  // counters start at zero (ensure_ws) and the kernel's last CTA re-zeroes them
+  launch_k(P->kt.dyn, dim3(P->dyn_grid), dim3(P->kt.nt), P->kt.smem_dyn, s, R, P->mc);
+  CUCHK(cudaGetLastError());
+  const long long lt1 = level_twiddles(P, 1);
+  mark(P, s, DKSS_K_ROWS, rp_work(P, (sq ? 2 : 3) * batch * lt1 + 2LL * P->M * batch),
+       (sq ? 6LL : 9LL) * batch * P->poly_words * 4);
+  return 0;
+}
+
 // whole multiply: operands already encoded-able in device memory
 // b == nullptr: squaring (one forward transform; the pointwise step multiplies each
 // transformed element by itself -- the reference's LL loop squares, bigmul/bench.py:214-215)
@@ -473,11 +510,11 @@ int run_mul(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, long 
   uint32_t* pa = P->d_poly;
   uint32_t* pb = sq ? pa : P->d_poly + (size_t)batch * P->poly_words;
   int rc;
-  if (P->rows_cs) {
-    // level 0 (with the encode) over columns; everything inside a row in one cluster kernel;
-    // level 0 of the inverse with the 1/2M scale
+  if (P->rows_cs || P->dyn_grid) {
+    // level 0 (with the encode) over columns; everything inside a row in one kernel (cluster
+    // or persistent dependency-driven); level 0 of the inverse with the 1/2M scale
     if ((rc = launch_fwd_levels(P, P->d_poly, (sq ? 1 : 2) * batch, s, a, b, nl, batch, 0, 1))) return rc;
-    if ((rc = launch_rows(P, pa, pb, batch, sq, s))) return rc;
+    if ((rc = P->rows_cs ? launch_rows(P, pa, pb, batch, sq, s) : launch_dyn(P, pa, pb, batch, sq, s))) return rc;
     if ((rc = launch_inv_levels(P, pa, batch, true, s, 0, 1))) return rc;
     return launch_decode(P, pa, prod, batch, s);
   }
@@ -664,6 +701,19 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
         P->rows_fn = fn;
       }
     }
+    // row phase as one persistent dependency-driven kernel: default for m = 32 two-level plans
+    // (2^21..2^26: 1.5-4% faster than three launches); for m = 16 the three pipelined
+    // launches measured faster.  DKSS_DYN=1 forces it on, DKSS_NO_DYN=1 off.
+    const char* nd = getenv("DKSS_NO_DYN");
+    const char* fd = getenv("DKSS_DYN");
+    const bool want_dyn = (fd && *fd && *fd != '0') || m == 32;
+    if (!P->rows_cs && P->levels == 2 && kt.dyn && want_dyn && !(nd && *nd && *nd != '0') &&
+        (1LL << P->log_top_mu) % kt.ne == 0) {
+      CUCHK(cudaFuncSetAttribute((const void*)kt.dyn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kt.smem_dyn));
+      int od = 0;
+      CUCHK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&od, kt.dyn, kt.nt, kt.smem_dyn));
+      P->dyn_grid = od > 0 ? sms * od : 0;
+    }
   }
   // cbias = -(2^(32L) - 1) * R mod p = (p - ((R mod p) - 1)) * R mod p  (ring_mul bias correction)
   {
@@ -733,7 +783,8 @@ int dkss_plan_get_info(const dkss_plan* P, dkss_plan_info* o) {
   o->product_limbs = P->prod_limbs;
   o->twiddles_per_fft = P->twiddles;
   o->ring_products = 3 * P->twiddles + 2LL * P->M;
-  o->launches_per_mul = P->rows_cs ? 1 + 1 + 1 + 3 : (P->levels > 0 ? 0 : 2) + P->levels + 1 + P->levels + 3;
+  o->launches_per_mul =
+      (P->rows_cs || P->dyn_grid) ? 1 + 1 + 1 + 3 : (P->levels > 0 ? 0 : 2) + P->levels + 1 + P->levels + 3;
   o->workspace_bytes = (int64_t)P->ws_bytes;
   return DKSS_OK;
 }

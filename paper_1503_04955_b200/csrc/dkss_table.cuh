@@ -4,6 +4,7 @@
 #include "dkss_kernels.cuh"
 #include "dkss_warp.cuh"
 #include "dkss_rows.cuh"
+#include "dkss_dyn.cuh"
 
 namespace dkss {
 
@@ -30,6 +31,10 @@ struct KTable {
   // CS = base length b in {2, 4, 8, 16}; null where not instantiated
   void (*rows[5])(RowsArgs, ModCtx);
   size_t smem_rows;
+  // row phase of two-level plans as one persistent kernel with dependency-driven items
+  // (dkss_dyn.cuh); null for m = 8
+  void (*dyn)(DynArgs, ModCtx);
+  size_t smem_dyn;
 };
 
 template <int MM, int L>
@@ -56,6 +61,8 @@ KTable make_table() {
     t.rows[3] = k_rows<MM, L, 8>;
     t.rows[4] = k_rows<MM, L, 16>;
     t.smem_rows = RowsSmem<MM, L>::WORDS * 4;
+    t.dyn = k_rows_dyn<MM, L>;
+    t.smem_dyn = DynSmem<MM, L>::WORDS * 4;
   }
   t.rmul = k_rmul<MM, L>;
   t.mscale = k_mont_scale<L>;

@@ -299,3 +299,29 @@ def test_square_batch_and_all_ones(cuda_ok):
     xs = [rng.getrandbits(1 << 18) for _ in range(5)] + [(1 << (1 << 18)) - 1]
     got = dmul_many([(x, x) for x in xs])
     assert [g.to_int() for g in got] == [x * x for x in xs]
+
+
+@pytest.mark.parametrize("env", ["DKSS_DYN=1", "DKSS_NO_DYN=1", "DKSS_ROWS=1"])
+def test_row_phase_variants_subprocess(cuda_ok, env):
+    # the row-phase implementation is chosen at plan creation from the environment: run the
+    # two-level sizes of both inner lengths in a fresh process per variant
+    import subprocess
+    import sys
+
+    code = (
+        "import random\n"
+        "from paper_1503_04955_b200 import dmul, dmul_many\n"
+        "r = random.Random(11)\n"
+        "for e in (18, 20, 21, 23):\n"
+        "    N = 1 << e\n"
+        "    a, b = r.getrandbits(N), r.getrandbits(N)\n"
+        "    assert dmul(a, b).to_int() == a * b, e\n"
+        "    assert dmul(a, a).to_int() == a * a, e\n"
+        "ps = [(r.getrandbits(1 << 18), r.getrandbits(1 << 18)) for _ in range(6)]\n"
+        "assert [c.to_int() for c in dmul_many(ps)] == [x * y for x, y in ps]\n"
+        "print('ok')\n")
+    k, v = env.split("=")
+    envd = dict(os.environ, **{k: v})
+    out = subprocess.run([sys.executable, "-c", code], env=envd, capture_output=True, text=True, timeout=600,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
