@@ -395,11 +395,13 @@ def main():
     rp = ring_products_per_multiply(plan)
     w_mul = rp * plan.m * plan.m * info["L"] * info["L"]
     prof_total_ms = sum(d["ms_per_mul"] for d in per_kind.values())
-    traffic = None
+    traffic, pipe_pct = None, None
     tpath = os.path.join(HERE, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get(args.config, {}).get(dom)
+            nt = json.load(f).get(args.config, {})
+        traffic = nt.get(dom)
+        pipe_pct = nt.get("fmaheavy_pct", {}).get(dom)
 
     # end to end through the public API (Python ints in, Natural / ints out; H2D + D2H inside):
     # dmul for one product, dmul_many for the batched workload (one device call per step)
@@ -437,6 +439,7 @@ def main():
             "roofline": {"bound": "imad", "achieved": round(achieved / 1e12, 4), "peak": round(peak / 1e12, 4),
                          "unit": "T limb-products/s (32x32->64)", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "kernel": dom, "peak_source": peak_src,
+                         "ncu_fmaheavy_pct": pipe_pct,  # IMAD.WIDE pipe busy, from the committed ncu capture
                          "work_per_launch": dk["work"] // max(1, dk["launches"]),
                          "whole_multiply_frac": round(w_mul / (ms_per_step * 1e-3 / batch) / peak, 4) if batch == 1
                          else round(w_mul * batch / (ms_per_step * 1e-3) / peak, 4)},

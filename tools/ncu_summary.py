@@ -48,6 +48,7 @@ def full(rep, workload=None, traffic=None):
     scale = {"usecond": 1e3, "us": 1e3, "nsecond": 1.0, "ns": 1.0, "msecond": 1e6, "ms": 1e6, "byte": 1, "Kbyte": 1e3,
              "Mbyte": 1e6, "Gbyte": 1e9}
     per_kind = defaultdict(list)
+    pipe = defaultdict(list)
     print(f"# {os.path.basename(rep)}" + (f" ({workload})" if workload else ""))
     print("kernel | " + " | ".join(k for _, k in keys) + " | top stalls")
     for row in r[2:]:
@@ -78,6 +79,9 @@ def full(rep, workload=None, traffic=None):
         print(f"{name.split('(')[0][:34]} | " + " | ".join(cells) + f" | {stalls}")
         if vals[1] is not None and vals[2] is not None:
             per_kind[kind_of(name)].append(vals[1] + vals[2])
+        fh = vals[[k for _, k in keys].index("fmaheavy%")]
+        if fh is not None:
+            pipe[kind_of(name)].append(fh)
     if traffic and workload:
         data = {}
         if os.path.exists(traffic):
@@ -86,7 +90,9 @@ def full(rep, workload=None, traffic=None):
         w = data.setdefault(workload, {})
         for k, v in per_kind.items():
             w[k] = int(sum(v) / len(v))
-        w["_source"] = f"{os.path.basename(rep)}: dram__bytes_read.sum + dram__bytes_write.sum per launch (avg)"
+        w["fmaheavy_pct"] = {k: round(sum(v) / len(v), 1) for k, v in pipe.items()}
+        w["_source"] = (f"{os.path.basename(rep)}: dram__bytes_read.sum + dram__bytes_write.sum per launch (avg); "
+                        "fmaheavy_pct = sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed (avg)")
         with open(traffic, "w") as f:
             json.dump(data, f, indent=1, sort_keys=True)
         print(f"# merged per-launch DRAM bytes into {traffic}: {dict((k, w[k]) for k in per_kind)}")
