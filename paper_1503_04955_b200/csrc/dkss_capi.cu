@@ -472,9 +472,10 @@ int launch_rows(dkss_plan* P, uint32_t* a, const uint32_t* b, int batch, bool sq
 
 // row phase (levels 1.. of both transforms, pointwise, inverse levels 1..) as one persistent
 // kernel with per-row dependency counters (dkss_dyn.cuh)
-int launch_dyn(dkss_plan* P, uint32_t* a, const uint32_t* b, int batch, bool sq, cudaStream_t s) {
-  const int E = 2 * P->m;
+int launch_dyn(dkss_plan* P, uint32_t* a, const uint32_t* b, int batch, bool sq, cudaStream_t s, int rows_pp = 0) {
+  const int E = rows_pp ? rows_pp : 2 * P->m;
   DynArgs R{};
+  R.rows_pp = E;
   R.a = a;
   R.b = b;
   R.poly_words = P->poly_words;
@@ -1172,6 +1173,14 @@ int dkss_fs_rows(dkss_plan* P, int world, uint32_t* z, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const int rows = 2 * P->m / world;
   const long long row_words = P->poly_words / (2LL * P->m);
+  const long long f_items = 2LL * rows << (P->log_top_mu - P->logE);
+  if (P->dyn_grid && f_items >= 2LL * P->dyn_grid) {
+    // the persistent row-phase kernel on this rank's R rows of a and b when there are enough
+    // column items to keep its grid busy (2^26 on 8 ranks: 0.43 vs 0.50 ms; 2^24 on 8 ranks,
+    // 256 items: the three launches win); its counters live in the plan workspace
+    if ((rc = ensure_ws(P, 1))) return rc;
+    return launch_dyn(P, z, z + (size_t)rows * row_words, 1, false, s, rows);
+  }
   const Geom g{row_words, P->log_top_mu - P->logE, 0, -1};
   if ((rc = launch_fwd_levels(P, z, 2 * rows, s, nullptr, nullptr, 0, 0, 1, P->levels, &g))) return rc;
   BottomArgs A{};

@@ -28,6 +28,7 @@ struct DynArgs {
   const uint32_t* b;       // b polynomials (== a when squaring)
   long long poly_words;    // 2M * MM * L
   int batch;               // pairs
+  int rows_pp;             // rows per pair (E; E/G for a four-step row shard)
   int npolys_fwd;          // 1 (squaring) or 2 polynomials transformed per pair
   int log_mu0, log_mu1;    // row length, level-1 columns per row
   int log_top_mu;          // twiddle split (log2 M/m)
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_rows_dyn(DynArgs
       const unsigned l = item & (unsigned)(mu1 - 1);
       const unsigned rest = item >> R.log_mu1;
       const unsigned w = rest % R.npolys_fwd, prow = rest / R.npolys_fwd;  // prow = pair * E + row
-      const unsigned pair = prow / E, row = prow % E;
+      const unsigned pair = prow / R.rows_pp, row = prow % R.rows_pp;
       uint32_t* poly = (w ? const_cast<uint32_t*>(R.b) : R.a) + pair * R.poly_words + row * mu0 * EW;
       // twiddle rows first (TMA, independent), then the column (plain loads)
       if constexpr (Cfg<MM>::TWS) {
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_rows_dyn(DynArgs
       const unsigned bi = item - R.n_f;
       const unsigned tpr = (unsigned)(mu0 / NE);  // tiles per row
       const unsigned prow = bi / tpr, t = bi % tpr;
-      const unsigned pair = prow / E, row = prow % E;
+      const unsigned pair = prow / R.rows_pp, row = prow % R.rows_pp;
       wait_count(R.fwd_done + prow, (unsigned)(R.npolys_fwd * mu1));
       const long long base = pair * R.poly_words + (row * mu0 + (long long)t * NE) * EW;
       uint32_t* pa = R.a + base;
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_rows_dyn(DynArgs
       // ---- I: inverse level-1 column l of the product row: twiddles, then the column DFT
       const unsigned ii = item - R.n_f - R.n_b;
       const unsigned l = ii & (unsigned)(mu1 - 1), prow = ii >> R.log_mu1;
-      const unsigned pair = prow / E, row = prow % E;
+      const unsigned pair = prow / R.rows_pp, row = prow % R.rows_pp;
       uint32_t* poly = R.a + pair * R.poly_words + row * mu0 * EW;
       if constexpr (Cfg<MM>::TWS) {
         if (threadIdx.x == 0) {
