@@ -325,3 +325,25 @@ def test_row_phase_variants_subprocess(cuda_ok, env):
     out = subprocess.run([sys.executable, "-c", code], env=envd, capture_output=True, text=True, timeout=600,
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("e", [27, 28])
+def test_dmul_beyond_the_configs_residues(cuda_ok, e):
+    # SURVEY.md 8(f) "general plans": N >= 2^27 selects d = 192 (L = 6 limbs) and u = 64;
+    # 2^28 needs three column levels.  Checked by residues modulo 32 seeded 62-bit primes.
+    rng = random.Random(e)
+    N = 1 << e
+    a = rng.getrandbits(N) | 1 << (N - 1)
+    b = rng.getrandbits(N) | 1 << (N - 1)
+    pl = P.dkss_select_params(N)
+    assert -(-pl.p.bit_length() // 32) == 6 and pl.u == 64
+    c = dmul(a, b).to_int()
+    assert c.bit_length() in (2 * N - 1, 2 * N)
+    pr = random.Random(777)
+    primes = []
+    while len(primes) < 32:
+        q = pr.getrandbits(62) | 1 << 61 | 1
+        if all(pow(w, q - 1, q) == 1 for w in (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37)):
+            primes.append(q)
+    for q in primes:
+        assert c % q == (a % q) * (b % q) % q
