@@ -538,9 +538,14 @@ int run_mul(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, long 
     if ((rc = launch_encode(P, a, nl, pa, batch, s))) return rc;
     if (!sq && (rc = launch_encode(P, b, nl, pb, batch, s))) return rc;
   }
-  if ((rc = launch_bottom(P, pa, pb, batch, 1, P->levels == 0, s))) return rc;
-  if ((rc = launch_inv_levels(P, pa, batch, true, s))) return rc;
-  if ((rc = launch_decode(P, pa, prod, batch, s))) return rc;
+  // DKSS_EXP_SKIP (timing experiments only, wrong products): bit 0 bottom, 1 inverse, 2 decode
+  static const int skip = [] {
+    const char* e = getenv("DKSS_EXP_SKIP");
+    return e ? atoi(e) : 0;
+  }();
+  if (!(skip & 1) && (rc = launch_bottom(P, pa, pb, batch, 1, P->levels == 0, s))) return rc;
+  if (!(skip & 2) && (rc = launch_inv_levels(P, pa, batch, true, s))) return rc;
+  if (!(skip & 4) && (rc = launch_decode(P, pa, prod, batch, s))) return rc;
   return 0;
 }
 

@@ -82,12 +82,12 @@ int main() {
   mc.pinv = 0xFFFFFFFFu;
   mc.pf_inv = 1.0f / (float)(81.0 * 33554432.0);
 
+  mc.proth = 1;
   run<16, 4, 2, 256, 2>("m16 T2 NT256 minb2", seed, out, mc);
   run<16, 4, 2, 256, 3>("m16 T2 NT256 minb3", seed, out, mc);
-  run<16, 4, 1, 256, 3>("m16 T1 NT256 minb3", seed, out, mc);
-  run<16, 4, 1, 256, 4>("m16 T1 NT256 minb4", seed, out, mc);
+  run<16, 4, 2, 128, 5>("m16 T2 NT128 minb5", seed, out, mc);
+  run<16, 4, 2, 384, 2>("m16 T2 NT384 minb2", seed, out, mc);
   run<32, 4, 2, 256, 2>("m32 T2 NT256 minb2", seed, out, mc);
-  run<32, 4, 1, 256, 3>("m32 T1 NT256 minb3", seed, out, mc);
-  run<32, 4, 1, 256, 4>("m32 T1 NT256 minb4", seed, out, mc);
+  run<32, 4, 2, 256, 3>("m32 T2 NT256 minb3", seed, out, mc);
   return 0;
 }
