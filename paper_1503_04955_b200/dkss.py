@@ -53,7 +53,8 @@ def _plan_for(N: int, w: int) -> DkssPlan:
     if pl is None:
         pl = dkss_select_params(N, w)
         with _dev_lock:
-            _host_plans.setdefault(key, pl)
+            if key not in _host_plans:
+                _cache_put(_host_plans, key, pl)
     return pl
 
 
@@ -69,20 +70,40 @@ def _device() -> int:
     return _env_device[1]
 
 
+_MAX_PLANS = 32  # cached plans per kind; older entries are dropped (and freed when unreferenced)
+
+
+def _cache_put(cache: dict, key, value):
+    cache[key] = value
+    while len(cache) > _MAX_PLANS:
+        cache.pop(next(iter(cache)))
+
+
+def plan_capacity(plan: DkssPlan) -> int:
+    """Largest operand bit length the plan's geometry encodes: M coefficients of m/2 u-bit
+    pieces (bigmul/dkss.py:381-398).  Every N the planner maps to (M, m, u) is at most this."""
+    return plan.M * (plan.m // 2) * plan.u
+
+
 def device_plan(plan: DkssPlan, device: int | None = None) -> DevicePlan:
-    """Upload (once) and return the device plan for a host plan."""
+    """Upload (once) and return the device plan for a host plan.
+
+    Device plans are shared by every N with the same geometry (M, m, u, p): they are built for
+    the geometry's capacity, so multiplying operands of many different sizes does not create
+    a device plan (twiddle table + workspace) per size."""
     device = _device() if device is None else device
-    key = (plan.N, plan.M, plan.m, plan.u, plan.p, device)
+    key = (plan.M, plan.m, plan.u, plan.p, device)
     with _dev_lock:
         dp = _dev_plans.get(key)
         if dp is None:
-            dp = DevicePlan(plan.N, plan.M, plan.m, plan.u, plan.p, plan.rho_powers, device)
-            _dev_plans[key] = dp
+            dp = DevicePlan(plan_capacity(plan), plan.M, plan.m, plan.u, plan.p, plan.rho_powers, device)
+            _cache_put(_dev_plans, key, dp)
         return dp
 
 
 def clear_device_plans() -> None:
     with _dev_lock:
+        _hot.clear()
         for dp in _dev_plans.values():
             dp.close()
         _dev_plans.clear()
@@ -204,7 +225,8 @@ def _hot_plan(N: int, w: int):
         info = dp.info
         ent = (plan, dp, info["operand_limbs"], info["product_limbs"], 2 * info["poly_bytes"],
                ring_products_per_multiply(plan))
-        _hot[key] = ent
+        with _dev_lock:
+            _cache_put(_hot, key, ent)
     return ent
 
 
