@@ -128,6 +128,8 @@ typedef struct {
   int64_t rows;        /* R, rows per rank after the exchange */
   int64_t elem_words;  /* m*L */
   int64_t block_words; /* one polynomial's share per rank: poly_words / world */
+  int64_t decode_seg;  /* distributed decode (u = 32): limbs per run segment; a rank writes
+                          (2m + 1) segments of 64-bit window sums; 0 when u != 32 */
 } dkss_fs_layout;
 int dkss_fs_layout_get(const dkss_plan* plan, int world, dkss_fs_layout* out);
 /* encode (bigmul/dkss.py:381-398) fused with the first forward level (column DFTs + twiddles,
@@ -141,6 +143,15 @@ int dkss_fs_rows(dkss_plan* plan, int world, uint32_t* z_dev, void* stream);
 /* last inverse level (columns) of the product with the 1/2M scaling (bigmul/dkss.py:507):
  * x = [E][C] elements of this rank's columns */
 int dkss_fs_columns_inv(dkss_plan* plan, int rank, int world, uint32_t* x_dev, void* stream);
+/* distributed decode (u = 32): after dkss_fs_columns_inv, every rank turns its columns into
+ * the per-limb window sums of its logical runs, s_out = uint64[2m + 1][decode_seg]
+ * (bigmul/dkss.py:498-513 restricted to the rank's coefficients); rank 0 gathers the world's
+ * segments, parts = uint64[world][2m + 1][decode_seg], adds the overlapping runs and
+ * resolves the carries into nc >= product_limbs limbs */
+int dkss_fs_decode_partial(dkss_plan* plan, int rank, int world, const uint32_t* x_dev, uint64_t* s_out_dev,
+                           void* stream);
+int dkss_fs_decode_finish(dkss_plan* plan, int world, const uint64_t* parts_dev, uint32_t* out_dev, size_t nc,
+                          void* stream);
 /* exchange re-layout: src [n][A][B][run_words] -> dst [n][B][A][run_words] (16-byte aligned,
  * run_words a multiple of 4, n*A*B <= 65535) */
 int dkss_block_transpose(dkss_plan* plan, const uint32_t* src_dev, uint32_t* dst_dev, int n, int A, int B,

@@ -23,7 +23,8 @@ EXPORTS = (
     "dkss_mul", "dkss_mul_digits", "dkss_mul_batch_digits", "dkss_mul_batch", "dkss_mul_device", "dkss_profile_device",
     "dkss_encode_host", "dkss_fft_host", "dkss_rmul_host", "dkss_decode_host",
     "dkss_fs_layout_get", "dkss_fs_columns_fwd", "dkss_fs_rows", "dkss_fs_columns_inv",
-    "dkss_block_transpose", "dkss_decode_device", "dkss_lucas_lehmer",
+    "dkss_block_transpose", "dkss_decode_device", "dkss_lucas_lehmer", "dkss_fs_decode_partial",
+    "dkss_fs_decode_finish",
 )
 
 DKSS_OK, DKSS_EINVAL, DKSS_ECUDA, DKSS_ERANGE, DKSS_ENOMEM = 0, -1, -2, -3, -4
@@ -57,7 +58,7 @@ class PlanInfo(ctypes.Structure):
 
 class FsLayout(ctypes.Structure):
     _fields_ = [("cols", ctypes.c_int64), ("rows", ctypes.c_int64), ("elem_words", ctypes.c_int64),
-                ("block_words", ctypes.c_int64)]
+                ("block_words", ctypes.c_int64), ("decode_seg", ctypes.c_int64)]
 
 
 _u32p = ctypes.POINTER(ctypes.c_uint32)
@@ -105,6 +106,8 @@ def load(path: str = LIB_PATH):
         L.dkss_fs_columns_inv.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp]
         L.dkss_block_transpose.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, vp]
         L.dkss_decode_device.argtypes = [vp, vp, vp, ctypes.c_size_t, vp]
+        L.dkss_fs_decode_partial.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp, vp]
+        L.dkss_fs_decode_finish.argtypes = [vp, ctypes.c_int, vp, vp, ctypes.c_size_t, vp]
         L.dkss_lucas_lehmer.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, _u32p, ctypes.c_size_t]
         for name in EXPORTS:
             if not hasattr(L, name):
@@ -262,6 +265,14 @@ class DevicePlan:
     def block_transpose(self, src_ptr: int, dst_ptr: int, n: int, a: int, b: int, run_words: int, stream: int = 0):
         _check(self._lib.dkss_block_transpose(self._h, ctypes.c_void_p(src_ptr), ctypes.c_void_p(dst_ptr), n, a, b,
                                               run_words, ctypes.c_void_p(stream)))
+
+    def fs_decode_partial(self, rank: int, world: int, x_ptr: int, s_ptr: int, stream: int = 0):
+        _check(self._lib.dkss_fs_decode_partial(self._h, rank, world, ctypes.c_void_p(x_ptr), ctypes.c_void_p(s_ptr),
+                                                ctypes.c_void_p(stream)))
+
+    def fs_decode_finish(self, world: int, parts_ptr: int, out_ptr: int, nc: int, stream: int = 0):
+        _check(self._lib.dkss_fs_decode_finish(self._h, world, ctypes.c_void_p(parts_ptr), ctypes.c_void_p(out_ptr), nc,
+                                               ctypes.c_void_p(stream)))
 
     def decode_device(self, v_ptr: int, out_ptr: int, nc: int, stream: int = 0):
         _check(self._lib.dkss_decode_device(self._h, ctypes.c_void_p(v_ptr), ctypes.c_void_p(out_ptr), nc,

@@ -132,6 +132,7 @@ struct dkss_plan {
   int rows_cs = 0;                  // >0: row phase in one cluster kernel (k_rows, cluster size)
   int dyn_grid = 0;                 // >0: row phase as one persistent dependency-driven kernel
   unsigned* d_dyn = nullptr;        // its ticket + per-row counters (cap_batch rows)
+  unsigned long long* d_sglob = nullptr;  // per-limb window sums of a distributed decode
   void (*rows_fn)(RowsArgs, ModCtx) = nullptr;
   // workspace
   int cap_batch = 0;
@@ -426,9 +427,11 @@ int launch_bottom(dkss_plan* P, uint32_t* a, const uint32_t* b, int npoly, int m
   return 0;
 }
 
-int launch_decode(dkss_plan* P, const uint32_t* v, uint32_t* out, int npoly, cudaStream_t s) {
+int launch_decode(dkss_plan* P, const uint32_t* v, uint32_t* out, int npoly, cudaStream_t s,
+                  const unsigned long long* sglob = nullptr) {
   DecodeArgs A{};
   A.v = v;
+  A.sglob = sglob;
   A.poly_words = P->poly_words;
   A.out = out;
   A.nout = P->prod_limbs;
@@ -783,6 +786,7 @@ void dkss_plan_destroy(dkss_plan* P) {
   cudaFree(P->d_twr);
   if (P->h_pin) cudaFreeHost(P->h_pin);
   cudaFree(P->d_stage);
+  cudaFree(P->d_sglob);
   if (P->stream) cudaStreamDestroy(P->stream);
   delete P;
 }
@@ -1165,6 +1169,65 @@ int dkss_fs_layout_get(const dkss_plan* P, int world, dkss_fs_layout* o) {
   o->rows = 2LL * P->m / world;
   o->elem_words = (long long)P->m * P->L;
   o->block_words = P->poly_words / world;
+  o->decode_seg = P->u == 32 ? o->cols * (P->m / 2) + P->m / 2 + P->L - 1 : 0;
+  return DKSS_OK;
+}
+
+int dkss_fs_decode_partial(dkss_plan* P, int rank, int world, const uint32_t* x, uint64_t* s_out, void* stream) {
+  int rc;
+  if ((rc = fs_check(P, rank, world))) return rc;
+  if (!x || !s_out) return fail(DKSS_EINVAL, "bad argument");
+  if (P->u != 32) return fail(DKSS_EINVAL, "distributed decode needs u = 32 (plan has u = %d)", P->u);
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  PartialArgs A{};
+  A.x = x;
+  A.s_out = reinterpret_cast<unsigned long long*>(s_out);
+  A.C = (1LL << P->log_top_mu) / world;
+  A.seg = A.C * (P->m / 2) + P->m / 2 + P->L - 1;
+  A.mu0 = 1LL << P->log_top_mu;
+  A.twoM = 2LL * P->M;
+  A.rank = rank;
+  A.E = 2 * P->m;
+  A.MM = P->m;
+  A.L = P->L;
+  const long long total = (long long)(A.E + 1) * A.seg;
+  const int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  launch_k(k_decode_partial, dim3(grid), dim3(256), 0, (cudaStream_t)stream, A);
+  CUCHK(cudaGetLastError());
+  return DKSS_OK;
+}
+
+int dkss_fs_decode_finish(dkss_plan* P, int world, const uint64_t* parts, uint32_t* out, size_t nc, void* stream) {
+  int rc;
+  if ((rc = fs_check(P, 0, world))) return rc;
+  if (!parts || !out) return fail(DKSS_EINVAL, "bad argument");
+  if (P->u != 32) return fail(DKSS_EINVAL, "distributed decode needs u = 32 (plan has u = %d)", P->u);
+  if ((long long)nc < P->prod_limbs) return fail(DKSS_EINVAL, "nc=%zu below product limbs %lld", nc, P->prod_limbs);
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  if ((rc = ensure_ws(P, 1))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!P->d_sglob) CUCHK(cudaMalloc(&P->d_sglob, (size_t)P->prod_limbs * 8));
+  CUCHK(cudaMemsetAsync(P->d_sglob, 0, (size_t)P->prod_limbs * 8, s));
+  AssembleArgs A{};
+  A.parts = reinterpret_cast<const unsigned long long*>(parts);
+  A.sglob = P->d_sglob;
+  A.C = (1LL << P->log_top_mu) / world;
+  A.seg = A.C * (P->m / 2) + P->m / 2 + P->L - 1;
+  A.nout = P->prod_limbs;
+  A.mu0 = 1LL << P->log_top_mu;
+  A.twoM = 2LL * P->M;
+  A.world = world;
+  A.E = 2 * P->m;
+  A.half = P->m / 2;
+  const long long total = (long long)world * (A.E + 1) * A.seg;
+  const int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  launch_k(k_decode_assemble, dim3(grid), dim3(256), 0, s, A);
+  CUCHK(cudaGetLastError());
+  if ((rc = launch_decode(P, nullptr, out, 1, s, P->d_sglob))) return rc;
+  if ((long long)nc > P->prod_limbs)
+    CUCHK(cudaMemsetAsync(out + P->prod_limbs, 0, ((long long)nc - P->prod_limbs) * 4, s));
   return DKSS_OK;
 }
 

@@ -1015,6 +1015,7 @@ struct DecodeArgs {
   uint32_t* bstat;     // per block: bit0 = cout(cin=0), bit1 = cout(cin=1)
   int blocks_per_poly;
   int M, MM, L, u;
+  const unsigned long long* sglob;  // non-null: per-limb window sums precomputed (distributed decode)
 };
 
 __device__ __forceinline__ unsigned long long window_sum(const DecodeArgs& A, const uint32_t* v, long long t) {
@@ -1079,9 +1080,10 @@ __global__ void __launch_bounds__(kDecThreads) k_decode1(DecodeArgs A) {
   const uint32_t* v = A.v + (long long)pidx * A.poly_words;
   __shared__ unsigned long long sS[kDecThreads + 1];
   __shared__ uint32_t wg[kDecWarps], wp[kDecWarps];
-  unsigned long long S = t < A.nout ? window_sum(A, v, t) : 0ull;
+  unsigned long long S = t < A.nout ? (A.sglob ? A.sglob[t] : window_sum(A, v, t)) : 0ull;
   sS[threadIdx.x + 1] = S;
-  if (threadIdx.x == 0) sS[0] = (t < A.nout && t > 0) ? window_sum(A, v, t - 1) : 0ull;
+  if (threadIdx.x == 0)
+    sS[0] = (t < A.nout && t > 0) ? (A.sglob ? A.sglob[t - 1] : window_sum(A, v, t - 1)) : 0ull;
   __syncthreads();
   unsigned long long w = (S & 0xFFFFFFFFull) + (sS[threadIdx.x] >> 32);
   if (t >= A.nout) w = 0;
@@ -1187,6 +1189,91 @@ __global__ void __launch_bounds__(kDecThreads) k_decode2(DecodeArgs A) {
   const unsigned long long carries = (a + b + s_wcin[warp]) ^ a ^ b;
   const unsigned c = (unsigned)((carries >> lane) & 1ull);
   A.out[(long long)pidx * A.nout + t] += c;
+}
+
+// ---------------------------------------------------------------------------
+// distributed decode of a four-step split (u = 32).  Rank r holds the product coefficients of
+// physical elements g = j*mu0 + r*C + c (its columns of every row j); the decode reads
+// logical element l at physical (2M - l) mod 2M, so row j of rank r is the logical run
+// [2M - j*mu0 - r*C - C + 1, 2M - j*mu0 - r*C] (rank 0 / row 0: [2M - C + 1, 2M) plus the lone
+// element 0, run E).  For every run, k_decode_partial writes the window sums of the output
+// limbs [l_a*half, l_b*half + half + L - 1) using only this rank's coefficients; runs of
+// different ranks overlap by half + L - 1 limbs, and k_decode_assemble adds the gathered runs
+// into the global per-limb sums that k_decode1 then turns into limbs and carries.
+struct PartialArgs {
+  const uint32_t* x;          // [E][C] local elements (m*L words each)
+  unsigned long long* s_out;  // [E + 1][seg] window sums
+  long long seg;              // limbs per run segment: C*half + half + L - 1
+  long long C, mu0, twoM;
+  int rank, E, MM, L;
+};
+
+__device__ __forceinline__ void run_bounds(long long r, long long j, long long C, long long mu0, long long twoM, int E,
+                                           long long* la, long long* lb) {
+  if (j == E) {  // the lone element 0 (rank 0 only)
+    *la = 0;
+    *lb = r == 0 ? 1 : 0;
+    return;
+  }
+  const long long hi = twoM - j * mu0 - r * C;  // logical index of physical column r*C (row j)
+  *la = hi - C + 1;
+  *lb = (hi == twoM) ? twoM : hi + 1;  // physical element 0 is the lone run
+}
+
+__global__ void k_decode_partial(PartialArgs A) {
+  griddep_wait();
+  griddep_launch();
+  const int half = A.MM / 2;
+  const long long total = (long long)(A.E + 1) * A.seg;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long j = idx / A.seg, tl = idx % A.seg;
+    long long la, lb;
+    run_bounds(A.rank, j, A.C, A.mu0, A.twoM, A.E, &la, &lb);
+    unsigned long long S = 0;
+    if (lb > la) {
+      const long long t = la * half + tl;
+      for (int q = 0; q < A.L; ++q) {
+        const long long sl = t - q;
+        if (sl < 0) break;
+        const long long lq = sl / half;
+        const int kk = (int)(sl % half);
+        for (int h = 0; h < 2; ++h) {
+          const long long l = lq - h;
+          if (l < la || l >= lb) continue;
+          const long long g = (A.twoM - l) % A.twoM;  // physical element
+          const long long jj = g / A.mu0, cc = g % A.mu0 - (long long)A.rank * A.C;
+          const int k = kk + h * half;
+          S += __ldg(A.x + ((jj * A.C + cc) * A.MM + k) * A.L + q);
+        }
+      }
+    }
+    A.s_out[idx] = S;
+  }
+}
+
+struct AssembleArgs {
+  const unsigned long long* parts;  // [G][E + 1][seg] gathered window sums
+  unsigned long long* sglob;        // [nout] zeroed
+  long long seg, nout, C, mu0, twoM;
+  int world, E, half;
+};
+
+__global__ void k_decode_assemble(AssembleArgs A) {
+  griddep_wait();
+  griddep_launch();
+  const long long total = (long long)A.world * (A.E + 1) * A.seg;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long v = A.parts[idx];
+    if (!v) continue;
+    const long long tl = idx % A.seg, rj = idx / A.seg;
+    const long long r = rj / (A.E + 1), j = rj % (A.E + 1);
+    long long la, lb;
+    run_bounds(r, j, A.C, A.mu0, A.twoM, A.E, &la, &lb);
+    const long long t = la * A.half + tl;
+    if (lb > la && t < A.nout) atomicAdd(A.sglob + t, v);
+  }
 }
 
 // ---------------------------------------------------------------------------

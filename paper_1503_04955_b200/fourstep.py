@@ -14,8 +14,11 @@ every deeper level and the base case act inside one of the E rows (:493-495).  S
            (dkss_fs_rows);
   exchange the transpose back (one polynomial);
   phase C  last inverse level on the own columns with the 1/2M scale (dkss_fs_columns_inv);
-  decode   the product columns are gathered to rank 0, re-laid to [E][mu0] and decoded
-           (dkss_decode_device) -- the survey's "first cut" decode.
+  decode   distributed (u = 32): every rank turns its columns into the per-limb window sums of
+           its logical runs (dkss_fs_decode_partial, 8 bytes per output limb it touches), rank 0
+           gathers them, adds the overlapping run ends and resolves the carries
+           (dkss_fs_decode_finish); otherwise the product columns are gathered to rank 0,
+           re-laid to [E][mu0] and decoded there (dkss_decode_device).
 
 Each rank moves P*(G-1)/G^2 bytes per polynomial per exchange (P = one polynomial),
 three polynomial exchanges per multiply, plus the final gather.  The exchange is NCCL
@@ -64,6 +67,12 @@ class DeviceStages:
     def decode(self, v, out):
         self.dp.decode_device(v.data_ptr(), out.data_ptr(), out.numel(), self._s())
 
+    def decode_partial(self, rank, world, x, s_out):
+        self.dp.fs_decode_partial(rank, world, x.data_ptr(), s_out.data_ptr(), self._s())
+
+    def decode_finish(self, world, parts, out):
+        self.dp.fs_decode_finish(world, parts.data_ptr(), out.data_ptr(), out.numel(), self._s())
+
 
 class DistExchange:
     """all-to-all / gather over a torch.distributed process group (NCCL on GPUs, gloo on CPU)."""
@@ -90,18 +99,27 @@ class DistExchange:
 class FourStepRank:
     """Buffers and phases of one rank (all limb buffers are int32 tensors on `device`)."""
 
-    def __init__(self, stages, rank: int, world: int, M: int, m: int, device, product_limbs: int):
+    def __init__(self, stages, rank: int, world: int, M: int, m: int, device, product_limbs: int,
+                 distributed_decode: bool | None = None):
         lay = stages.layout(world)
         self.stages, self.rank, self.world = stages, rank, world
         self.E = 2 * m
         self.C, self.R, self.ew, self.bw = lay["cols"], lay["rows"], lay["elem_words"], lay["block_words"]
         self.mu0 = 2 * M // self.E
+        seg = lay.get("decode_seg", 0)
+        self.dist_decode = bool(seg) if distributed_decode is None else (distributed_decode and bool(seg))
         kw = dict(dtype=torch.int32, device=device)
         self.x = torch.empty(2 * self.bw, **kw)  # [2][E][C] columns (phase A/C)
         self.y = torch.empty(2 * self.bw, **kw)  # exchange staging
         self.z = torch.empty(2 * self.bw, **kw)  # [2][R][mu0] rows (phase B)
-        self.full = torch.empty(world * self.bw if rank == 0 else 1, **kw)
-        self.gath = torch.empty(world * self.bw if rank == 0 else 1, **kw)
+        if self.dist_decode:
+            n_part = (self.E + 1) * seg  # 64-bit window sums of this rank's runs
+            self.part = torch.empty(n_part, dtype=torch.int64, device=device)
+            self.gath = torch.empty(world * n_part if rank == 0 else 1, dtype=torch.int64, device=device)
+            self.full = None
+        else:
+            self.full = torch.empty(world * self.bw if rank == 0 else 1, **kw)
+            self.gath = torch.empty(world * self.bw if rank == 0 else 1, **kw)
         self.prod = torch.empty(product_limbs if rank == 0 else 1, **kw)
 
     # one polynomial's share split by destination rank (rows [h*R, (h+1)*R) x C columns)
@@ -122,11 +140,19 @@ class FourStepRank:
         return [self._poly(self.y, 0)], [self._poly(self.x, 0)]
 
     def phase_finish(self):
-        # x[0] = [G src][R][C] = [E][C]: last inverse level of the own columns
+        """Last inverse level of the own columns (x[0] = [G src][R][C] = [E][C]); returns what
+        this rank sends to rank 0: its run window sums (distributed decode) or its columns."""
         self.stages.columns_inv(self.rank, self.world, self._poly(self.x, 0))
+        if self.dist_decode:
+            self.stages.decode_partial(self.rank, self.world, self._poly(self.x, 0), self.part)
+            return self.part
         return self._poly(self.x, 0)
 
     def decode(self):
+        if self.dist_decode:
+            # rank 0: gath = [G][E+1][seg] window sums -> product limbs
+            self.stages.decode_finish(self.world, self.gath, self.prod)
+            return self.prod
         # rank 0: gath = [G][E][C] -> full = [E][G][C] = [E][mu0], then decode
         self.stages.block_transpose(self.gath, self.full, 1, self.world, self.E, self.C * self.ew)
         self.stages.decode(self.full, self.prod)
@@ -181,10 +207,11 @@ def _plan_and_limbs(a: int, b: int):
     return plan
 
 
-def make_rank(plan, rank: int, world: int, device=None) -> FourStepRank:
+def make_rank(plan, rank: int, world: int, device=None, distributed_decode: bool | None = None) -> FourStepRank:
     device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     dp = device_plan(plan, device.index or 0)
-    return FourStepRank(DeviceStages(dp), rank, world, plan.M, plan.m, device, dp.info["product_limbs"])
+    return FourStepRank(DeviceStages(dp), rank, world, plan.M, plan.m, device, dp.info["product_limbs"],
+                        distributed_decode)
 
 
 def _operands(plan, a: int, b: int, device):
@@ -215,10 +242,10 @@ def dmul_fourstep(a: int, b: int, group=None) -> int | None:
     return _to_int(prod) if rank == 0 else None
 
 
-def dmul_fourstep_virtual(a: int, b: int, world: int, device=None) -> int:
+def dmul_fourstep_virtual(a: int, b: int, world: int, device=None, distributed_decode: bool | None = None) -> int:
     """a*b through the four-step split with `world` ranks emulated on one GPU (tests)."""
     plan = _plan_and_limbs(a, b)
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-    ranks = [make_rank(plan, r, world, dev) for r in range(world)]
+    ranks = [make_rank(plan, r, world, dev, distributed_decode) for r in range(world)]
     A, B = _operands(plan, a, b, dev)
     return _to_int(run_virtual(ranks, A, B))

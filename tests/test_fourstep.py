@@ -21,12 +21,38 @@ E, MU0, EW = 2 * MM, 2 * M // (2 * MM), MM * LL
 A_TAG, B_TAG, PROD_TAG, SCALED_TAG = 1, 2, 7, 9
 
 
+SEG = 5  # stand-in segment length of the distributed decode
+
+
 class TagStages:
-    def __init__(self):
+    def __init__(self, dist=False):
         self.calls = []
+        self.dist = dist
 
     def layout(self, world):
-        return {"cols": MU0 // world, "rows": E // world, "elem_words": EW, "block_words": 2 * M * EW // world}
+        return {"cols": MU0 // world, "rows": E // world, "elem_words": EW, "block_words": 2 * M * EW // world,
+                "decode_seg": SEG if self.dist else 0}
+
+    def decode_partial(self, rank, world, x, s_out):
+        # the columns must be the scaled product of exactly this rank's columns
+        self.columns_seen(rank, world, x)
+        v = s_out.view(E + 1, SEG)
+        v[:, 0] = rank
+        v[:, 1] = torch.arange(E + 1)
+        self.calls.append("decode_partial")
+
+    def columns_seen(self, rank, world, x):
+        C = MU0 // world
+        v = x.view(E, C, EW)
+        want = torch.arange(E).view(E, 1) * MU0 + rank * C + torch.arange(C).view(1, C)
+        assert bool((v[:, :, 0] == SCALED_TAG).all()) and torch.equal(v[:, :, 1], want.to(torch.int32))
+
+    def decode_finish(self, world, parts, out):
+        v = parts.view(world, E + 1, SEG)
+        assert torch.equal(v[:, :, 0], torch.arange(world).view(world, 1).expand(world, E + 1).to(v.dtype))
+        assert torch.equal(v[:, :, 1], torch.arange(E + 1).view(1, E + 1).expand(world, E + 1).to(v.dtype))
+        out.fill_(1)
+        self.calls.append("decode")
 
     def columns_fwd(self, rank, world, a, b, x):
         C = MU0 // world
@@ -69,14 +95,15 @@ class TagStages:
         self.calls.append("decode")
 
 
-def _ranks(world):
-    st = TagStages()
+def _ranks(world, dist=False):
+    st = TagStages(dist)
     return st, [FourStepRank(st, r, world, M, MM, torch.device("cpu"), 4) for r in range(world)]
 
 
+@pytest.mark.parametrize("dist", [False, True])
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
-def test_virtual_ranks_move_every_element(world):
-    st, ranks = _ranks(world)
+def test_virtual_ranks_move_every_element(world, dist):
+    st, ranks = _ranks(world, dist)
     a = torch.zeros(4, dtype=torch.int32)
     out = run_virtual(ranks, a, a)
     assert out.tolist() == [1, 1, 1, 1]
@@ -92,14 +119,14 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, distd=False):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        st = TagStages()
+        st = TagStages(distd)
         fs = FourStepRank(st, rank, world, M, MM, torch.device("cpu"), 4)
         a = torch.zeros(4, dtype=torch.int32)
         out = run_rank(fs, DistExchange(), a, a)
@@ -111,11 +138,12 @@ def _worker(rank, world, port, q):
 
 
 @pytest.mark.timeout(180)
-def test_two_rank_gloo_fourstep_exchange():
+@pytest.mark.parametrize("distd", [False, True])
+def test_two_rank_gloo_fourstep_exchange(distd):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, distd)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted(q.get(timeout=150) for _ in procs)

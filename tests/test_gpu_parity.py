@@ -215,15 +215,16 @@ def test_dmul_2_26_residues(cuda_ok):
 
 
 # --- four-step split of one multiply, G ranks emulated on one GPU ---------
+@pytest.mark.parametrize("dist_decode", [True, False])
 @pytest.mark.parametrize("e,world", [(16, 2), (16, 16), (18, 4), (20, 2), (20, 8), (20, 32)])
-def test_fourstep_virtual_ranks(cuda_ok, e, world):
+def test_fourstep_virtual_ranks(cuda_ok, e, world, dist_decode):
     from paper_1503_04955_b200.fourstep import dmul_fourstep_virtual
 
     rng = random.Random(100 + e + world)
     N = 1 << e
     a = rng.getrandbits(N) | 1 << (N - 1)
     b = rng.getrandbits(N) | 1 << (N - 1)
-    assert dmul_fourstep_virtual(a, b, world) == a * b
+    assert dmul_fourstep_virtual(a, b, world, distributed_decode=dist_decode) == a * b
 
 
 def test_fourstep_virtual_all_ones(cuda_ok):
