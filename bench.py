@@ -197,6 +197,7 @@ def run_split(args):
     import torch
     import torch.distributed as dist
 
+    from paper_1503_04955_b200.dkss import set_device
     from paper_1503_04955_b200.fourstep import DistExchange, _operands, dmul_fourstep, make_rank, run_rank
     from paper_1503_04955_b200.plan import dkss_select_params, ring_products_per_multiply
 
@@ -209,6 +210,7 @@ def run_split(args):
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     os.environ["DKSS_DEVICE"] = str(local)
+    set_device(local)
     N, batch, seed, ones = CONFIGS[args.config]
     if batch != 1:
         raise SystemExit("--split applies to single-multiply configs")
@@ -310,7 +312,8 @@ def main():
     torch.cuda.set_device(dev)
     os.environ["DKSS_DEVICE"] = str(local)
 
-    from paper_1503_04955_b200.dkss import device_plan, dmul, dmul_many
+    from paper_1503_04955_b200.dkss import device_plan, dmul, dmul_many, set_device
+    set_device(local)
     from paper_1503_04955_b200.plan import dkss_select_params, ring_products_per_multiply
     from paper_1503_04955_b200.words import int_to_u32, u32_to_int
 

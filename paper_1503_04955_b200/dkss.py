@@ -58,16 +58,21 @@ def _plan_for(N: int, w: int) -> DkssPlan:
     return pl
 
 
-_env_device: tuple = (None, 0)
+_device_ordinal: int | None = None
 
 
 def _device() -> int:
-    """GPU ordinal from DKSS_DEVICE (default 0); the parsed value is cached per env string."""
-    global _env_device
-    raw = os.environ.get("DKSS_DEVICE", "0")
-    if raw != _env_device[0]:
-        _env_device = (raw, int(raw))
-    return _env_device[1]
+    """GPU ordinal: set_device(), else DKSS_DEVICE read at the first call (default 0)."""
+    global _device_ordinal
+    if _device_ordinal is None:
+        _device_ordinal = int(os.environ.get("DKSS_DEVICE", "0"))
+    return _device_ordinal
+
+
+def set_device(ordinal: int) -> None:
+    """Select the GPU later multiplies of this process run on."""
+    global _device_ordinal
+    _device_ordinal = int(ordinal)
 
 
 _MAX_PLANS = 32  # cached plans per kind; older entries are dropped (and freed when unreferenced)

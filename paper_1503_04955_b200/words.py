@@ -307,10 +307,10 @@ _PYLONG_OK = _layout_ok()
 def pylong_digits(x: int):
     """(address, digit count) of the 30-bit digits of a nonnegative int, or None when the
     interpreter's int layout is not the one checked above.  The int must stay alive while
-    the address is used."""
+    the address is used.  (The count of a normalised int is ceil(bit_length / 30); the
+    digits start at a fixed offset -- both checked against the object header at import.)"""
     if not _PYLONG_OK or type(x) is not int:
         return None
-    addr, nd, sign = _raw_digits(x)
-    if sign == 2:
+    if x < 0:
         raise ValueError("Natural is nonnegative")
-    return addr, (0 if sign == 1 else nd)
+    return id(x) + 24, (x.bit_length() + 29) // 30
