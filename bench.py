@@ -206,8 +206,14 @@ def run_split(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world < 2:
         raise SystemExit("--split needs torchrun with >= 2 ranks (tests emulate ranks on one GPU)")
+    gloo = os.environ.get("DKSS_BENCH_GLOO", "0") not in ("", "0")  # see main()
+    if gloo:
+        local %= max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if gloo:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     os.environ["DKSS_DEVICE"] = str(local)
     set_device(local)
@@ -305,9 +311,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # DKSS_BENCH_GLOO=1: run the multi-rank path with gloo and ranks sharing the visible GPUs
+    # (checks the orchestration on a 1-GPU box; NCCL needs one GPU per rank)
+    gloo = os.environ.get("DKSS_BENCH_GLOO", "0") not in ("", "0")
+    if gloo:
+        local %= max(1, torch.cuda.device_count())
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     os.environ["DKSS_DEVICE"] = str(local)

@@ -82,13 +82,27 @@ class DistExchange:
 
         self.dist = dist
         self.group = group
+        # gloo has no all-to-all / gather on CUDA tensors: stage through host memory (tests on a
+        # one-GPU box; NCCL takes device tensors directly)
+        self.host = dist.get_backend(group) == "gloo"
 
     def all_to_all(self, out, inp):
+        if self.host and out.is_cuda:
+            o = torch.empty_like(out, device="cpu")
+            self.dist.all_to_all_single(o, inp.cpu(), group=self.group)
+            out.copy_(o)
+            return
         self.dist.all_to_all_single(out, inp, group=self.group)
 
     def gather(self, out, inp, rank):
         # out: [G * n] on rank 0 (ignored elsewhere)
         world = self.dist.get_world_size(self.group)
+        if self.host and inp.is_cuda:
+            o = torch.empty(out.shape, dtype=out.dtype) if rank == 0 else None
+            self.gather(o, inp.cpu(), rank)
+            if rank == 0:
+                out.copy_(o)
+            return
         if rank == 0:
             parts = list(out.view(world, -1).unbind(0))
             self.dist.gather(inp, parts, dst=0, group=self.group)
