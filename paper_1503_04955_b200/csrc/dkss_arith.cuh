@@ -29,6 +29,7 @@ struct ModCtx {
   uint32_t cbias[DKSS_MAXL];   // -(2^(32L) - 1) * R mod p  (ring_mul bias correction)
   uint32_t proth;              // p = 1 + ptop * 2^(32(L-1)): p[0] = 1, middle limbs 0 (every
                                // table prime at the configs, 81 * 2^121 + 1); REDC specialises
+  uint32_t qbias[2 * DKSS_MAXL + 1];  // p * 2^(32L + 5): keeps the pointwise bias removal >= 0
 };
 
 // r = (a + b) mod p and r = (a - b) mod p for canonical a, b (PTX carry chains, dkss_carry.cuh)

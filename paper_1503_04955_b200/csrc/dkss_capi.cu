@@ -627,6 +627,17 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
     const char* np = getenv("DKSS_NO_PROTH");
     P->mc.proth = (pr && !(np && *np && *np != '0')) ? 1u : 0u;
   }
+  {
+    // qbias = p * 2^(32L + 5) in 2L+1 limbs (pointwise bias removal, ring_mul BiasFromY)
+    uint64_t carry = 0;
+    for (int i = 0; i < 2 * L + 1; ++i) P->mc.qbias[i] = 0;
+    for (int i = 0; i < L; ++i) {
+      const uint64_t v = ((uint64_t)p[i] << 5) | carry;
+      P->mc.qbias[L + i] = (uint32_t)v;
+      carry = v >> 32;
+    }
+    P->mc.qbias[2 * L] = (uint32_t)carry;
+  }
   Limbs x(L, 0);
   x[0] = 1;
   for (int i = 0; i < 32 * L; ++i) dbl_mod(x, p);

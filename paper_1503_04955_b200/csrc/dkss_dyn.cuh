@@ -193,8 +193,6 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_rows_dyn(DynArgs
       __syncthreads();
       uint32_t* ra = dft_pingpong<MM, L, NE>(s0, s2, R.logb, mc);
       uint32_t* rb = dft_pingpong<MM, L, NE>(s1, ra == s0 ? s2 : s0, R.logb, mc);
-      uint32_t* wb = (ra != s0 && rb != s0) ? s0 : (ra != s1 && rb != s1) ? s1 : s2;
-      cta_w_rows<MM, L, NE>(rb, wb, mc);
       __syncthreads();
       uint32_t res[PER][kT][L];
       int dsts[PER];
@@ -204,7 +202,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_rows_dyn(DynArgs
         dsts[q] = -1;
         if (it < NE * TPE) {
           const int el = it / TPE, k0 = (it % TPE) * kT;
-          ring_mul<MM, L>(ResS<L>{rb + el * ES}, ResS<L>{ra + el * ES}, ResS<L>{wb + el * ES}, k0, mc, res[q]);
+          ring_mul<MM, L>(ResS<L>{rb + el * ES}, ResS<L>{ra + el * ES}, BiasFromY{}, k0, mc, res[q]);
           dsts[q] = slot(el) * ES + k0 * L;
         }
       }

@@ -22,6 +22,7 @@
 // twiddle rows into shared memory while tile k is transformed and multiplied.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #ifdef DKSS_EXP_TRACE
 #include <cstdio>
 #endif
@@ -206,6 +207,12 @@ __device__ __forceinline__ void mac_limb(uint32_t& lo, uint32_t& hi, uint32_t& c
 #ifndef DKSS_R32_UNROLL
 #define DKSS_R32_UNROLL 4
 #endif
+
+// wl argument of ring_mul for products where y is not a table twiddle (the pointwise
+// products): the bias B * sum_{i>k} y_i is removed exactly instead of through a W residue --
+// value = acc + S_k + Q - S_k 2^(32L) with S_k = sum_{i>k} y_i as an integer and
+// Q = p 2^(32L+5) (a multiple of p keeping the value non-negative), then REDC as usual
+struct BiasFromY {};
 template <int MM, int L, class YL, class XL, class WL, int kT = Cfg<MM>::T>
 __device__ __forceinline__ void ring_mul(YL yl, XL xl, WL wl, int k0, const ModCtx& mc, uint32_t (&out)[kT][L]) {
   constexpr int NCOL = 2 * L - 1;
@@ -239,23 +246,72 @@ __device__ __forceinline__ void ring_mul(YL yl, XL xl, WL wl, int k0, const ModC
             mac_limb(lo[t][a + b], hi[t][a + b], cy[t][a + b], yg[a], win[(t - s + kT) % kT][b]);
     }
   }
+  if constexpr (std::is_same_v<WL, BiasFromY>) {
+    // S = sum_{i > k0+kT-1} y_i, then walk t down adding y_{k0+t+1}
+    uint32_t S[L + 1];
 #pragma unroll
-  for (int t = 0; t < kT; ++t) {
-    // value = sum_c (lo_c + hi_c 2^32 + cy_c 2^64) 2^(32c) + W_k  ->  2L+1 limbs
-    uint32_t wv[L];
-    wl(k0 + t, wv);
-    uint32_t tl[2 * L + 1];
-    uint64_t acc = 0;
+    for (int q = 0; q <= L; ++q) S[q] = 0;
+    for (int i = MM - 1; i > k0 + kT - 1; --i) {
+      uint32_t yg[L];
+      yl(i, yg);
+      uint64_t c = 0;
 #pragma unroll
-    for (int q = 0; q < 2 * L + 1; ++q) {
-      if (q < NCOL) acc += lo[t][q];
-      if (q >= 1 && q - 1 < NCOL) acc += hi[t][q - 1];
-      if (q >= 2 && q - 2 < NCOL) acc += cy[t][q - 2];
-      if (q < L) acc += wv[q];
-      tl[q] = (uint32_t)acc;
-      acc >>= 32;
+      for (int q = 0; q < L; ++q) {
+        c += (uint64_t)S[q] + yg[q];
+        S[q] = (uint32_t)c;
+        c >>= 32;
+      }
+      S[L] += (uint32_t)c;
     }
-    redc<L>(out[t], tl, mc);
+#pragma unroll
+    for (int t = kT - 1; t >= 0; --t) {
+      uint32_t tl[2 * L + 1];
+      int64_t acc = 0;
+#pragma unroll
+      for (int q = 0; q < 2 * L + 1; ++q) {
+        uint64_t col = 0;
+        if (q < NCOL) col += lo[t][q];
+        if (q >= 1 && q - 1 < NCOL) col += hi[t][q - 1];
+        if (q >= 2 && q - 2 < NCOL) col += cy[t][q - 2];
+        acc += (int64_t)col + mc.qbias[q];
+        if (q <= L) acc += S[q];
+        if (q >= L) acc -= S[q - L];
+        tl[q] = (uint32_t)acc;
+        acc >>= 32;  // arithmetic: carries and borrows
+      }
+      redc<L>(out[t], tl, mc);
+      if (t > 0) {
+        uint32_t yg[L];
+        yl(k0 + t, yg);
+        uint64_t c = 0;
+#pragma unroll
+        for (int q = 0; q < L; ++q) {
+          c += (uint64_t)S[q] + yg[q];
+          S[q] = (uint32_t)c;
+          c >>= 32;
+        }
+        S[L] += (uint32_t)c;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < kT; ++t) {
+      // value = sum_c (lo_c + hi_c 2^32 + cy_c 2^64) 2^(32c) + W_k  ->  2L+1 limbs
+      uint32_t wv[L];
+      wl(k0 + t, wv);
+      uint32_t tl[2 * L + 1];
+      uint64_t acc = 0;
+#pragma unroll
+      for (int q = 0; q < 2 * L + 1; ++q) {
+        if (q < NCOL) acc += lo[t][q];
+        if (q >= 1 && q - 1 < NCOL) acc += hi[t][q - 1];
+        if (q >= 2 && q - 2 < NCOL) acc += cy[t][q - 2];
+        if (q < L) acc += wv[q];
+        tl[q] = (uint32_t)acc;
+        acc >>= 32;
+      }
+      redc<L>(out[t], tl, mc);
+    }
   }
 }
 
@@ -278,35 +334,6 @@ __device__ __forceinline__ void store_rot(uint32_t* dst, const uint32_t (&w)[kT]
   }
 }
 
-// W rows of NE elements y (stride ES) -> dst (stride ESW):
-//   W_k = -(2^(32L) - 1) * sum_{i>k} y_i  mod p   (mc.cbias = -(2^(32L)-1) * R mod p)
-// One thread per element runs the suffix sum (MM-1 modular adds), then all threads scale.
-template <int MM, int L, int NE>
-__device__ __forceinline__ void cta_w_rows(const uint32_t* src, uint32_t* dst, const ModCtx& mc) {
-  constexpr int ES = Smem<MM, L>::ES, ESW = Smem<MM, L>::ESW, NT = Cfg<MM>::NT;
-  for (int el = threadIdx.x; el < NE; el += NT) {
-    uint32_t s[L];
-#pragma unroll
-    for (int q = 0; q < L; ++q) s[q] = 0;
-    st_res<L>(dst + el * ESW + (MM - 1) * L, s);
-    for (int k = MM - 2; k >= 0; --k) {
-      uint32_t y[L];
-      ld_res<L>(y, src + el * ES + (k + 1) * L);
-      add_mod<L>(s, s, y, mc);
-      st_res<L>(dst + el * ESW + k * L, s);
-    }
-  }
-  __syncthreads();
-  for (int it = threadIdx.x; it < NE * MM; it += NT) {
-    const int el = it / MM, k = it % MM;
-    uint32_t s[L], c[L];
-    ld_res<L>(s, dst + el * ESW + k * L);
-#pragma unroll
-    for (int q = 0; q < L; ++q) c[q] = mc.cbias[q];
-    mont_mul<L>(s, s, c, mc);
-    st_res<L>(dst + el * ESW + k * L, s);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // radix-2 DIT over NE elements in shared memory, split into groups of n = 2^logn
@@ -771,13 +798,11 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_bottom(BottomArg
       issue_bottom_tile<MM, L>(A, nxt, &bar[st ^ 1], smem + (st ^ 1) * STAGE, smem + (st ^ 1) * STAGE + NE * ES);
     mbar_wait(&bar[st], NS == 2 ? ((k >> 1) & 1) : (k & 1));
     const long long e0 = tile * NE;
-    // three NE-element buffers {sa, sb, wr} serve as DFT ping-pong space, W rows and results
+    // three NE-element buffers {sa, sb, wr} serve as DFT ping-pong space and results
     uint32_t* ra = dft_pingpong<MM, L, NE>(sa, wr, A.logb, mc);
     uint32_t* out = ra;
     if (two) {
       uint32_t* rb = dft_pingpong<MM, L, NE>(sb, ra == sa ? wr : sa, A.logb, mc);
-      uint32_t* wb = (ra != sa && rb != sa) ? sa : (ra != sb && rb != sb) ? sb : wr;
-      cta_w_rows<MM, L, NE>(rb, wb, mc);
       __syncthreads();
       uint32_t res[PER][kT][L];
       int dsts[PER];
@@ -787,7 +812,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_bottom(BottomArg
         dsts[q] = -1;
         if (it < NE * TPE) {
           const int el = it / TPE, k0 = (it % TPE) * kT;
-          ring_mul<MM, L>(ResS<L>{rb + el * ES}, ResS<L>{ra + el * ES}, ResS<L>{wb + el * ES}, k0, mc, res[q]);
+          ring_mul<MM, L>(ResS<L>{rb + el * ES}, ResS<L>{ra + el * ES}, BiasFromY{}, k0, mc, res[q]);
           const int slot = (el & ~bmask) | bitrev_n(el & bmask, A.logb);
           dsts[q] = slot * ES + k0 * L;
         }
@@ -835,7 +860,6 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_rmul(const uint3
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t* sx = smem;
   uint32_t* sy = smem + NE * ES;
-  uint32_t* wr = smem + 2 * NE * ES;
   const long long e0 = (long long)blockIdx.x * NE;
   constexpr int V4 = MM * L / 4;
   for (int it = threadIdx.x; it < NE * V4; it += NT) {
@@ -850,13 +874,13 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_rmul(const uint3
     *reinterpret_cast<uint4*>(sy + el * ES + w4 * 4) = vy;
   }
   __syncthreads();
-  cta_w_rows<MM, L, NE>(sy, wr, mc);
+
   __syncthreads();
   for (int it = threadIdx.x; it < NE * TPE; it += NT) {
     const int el = it / TPE, k0 = (it % TPE) * kT;
     if (e0 + el >= count) continue;
     uint32_t w[kT][L];
-    ring_mul<MM, L>(ResS<L>{sy + el * ES}, ResS<L>{sx + el * ES}, ResS<L>{wr + el * ESW}, k0, mc, w);
+    ring_mul<MM, L>(ResS<L>{sy + el * ES}, ResS<L>{sx + el * ES}, BiasFromY{}, k0, mc, w);
     uint32_t r2[L];
 #pragma unroll
     for (int q = 0; q < L; ++q) r2[q] = mc.r2[q];

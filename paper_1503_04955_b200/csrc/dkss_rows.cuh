@@ -147,8 +147,6 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_rows(RowsArgs R,
   {
     uint32_t* ra = dft_pingpong<MM, L, E>(sA, sT, LOGB, mc);
     uint32_t* rb = dft_pingpong<MM, L, E>(sB, ra == sA ? sT : sA, LOGB, mc);
-    uint32_t* wb = (ra != sA && rb != sA) ? sA : (ra != sB && rb != sB) ? sB : sT;
-    cta_w_rows<MM, L, E>(rb, wb, mc);
     __syncthreads();
     uint32_t res[PER][kT][L];
     int dsts[PER];
@@ -158,7 +156,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_rows(RowsArgs R,
       dsts[qq] = -1;
       if (it < E * TPE) {
         const int el = it / TPE, k0 = (it % TPE) * kT;
-        ring_mul<MM, L>(ResS<L>{rb + el * ES}, ResS<L>{ra + el * ES}, ResS<L>{wb + el * ES}, k0, mc, res[qq]);
+        ring_mul<MM, L>(ResS<L>{rb + el * ES}, ResS<L>{ra + el * ES}, BiasFromY{}, k0, mc, res[qq]);
         const int slot = (el & ~(CS - 1)) | bitrev_n(el & (CS - 1), LOGB);
         dsts[qq] = slot * ES + k0 * L;
       }
