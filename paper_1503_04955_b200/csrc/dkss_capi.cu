@@ -125,6 +125,7 @@ struct dkss_plan {
   KTable kt{};
   uint32_t* d_tw = nullptr;   // Montgomery-form rho table [M/m][m][L]
   uint32_t* d_twr = nullptr;  // twiddle rows [M/m][2m][L]: Montgomery-form rho^s, then W_s
+  uint32_t* d_twr_s = nullptr;  // the same rows times (2M)^-1 R: the last inverse level scales for free
   int grid_pass = 0, grid_bot = 0;  // persistent grid sizes (SMs x resident CTAs)
   int grid_fw = 0, grid_iw = 0;     // warp-per-column kernels (0 = not used)
   int grid_dft = 0, grid_tw = 0;    // split passes (column DFT kernel + elementwise twiddles)
@@ -388,6 +389,12 @@ int launch_inv_levels(dkss_plan* P, uint32_t* poly, int npoly, bool scale_last, 
     // the inverse pass keeps the CTA-wide kernel in auto mode: the warp-per-column inverse needs
     // two column slices per warp (3 CTAs/SM) and measured slower (batch 1024 x 2^18: 4.22 vs 3.89 ms)
     const int kind = P->pass_mode ? pass_kind(P, cols) : 1;
+    if (kind == 1 && A.scale) {
+      // CTA-wide kernel: the twiddle products use the scaled rows, only untwiddled elements
+      // take an explicit multiply (scale mode 2)
+      A.scale = 2;
+      A.twr = P->d_twr_s;
+    }
     if (kind == 3) {
       PassArgs B = A;
       B.scale = 0;
@@ -780,7 +787,24 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
         P->d_tw, P->d_twr, (long long)(M / m), m, P->mc);
     e = cudaGetLastError();
   }
+  // scaled rows for the last inverse level: rho^s R * kscale R^-1 = rho^s (2M)^-1 R^2, so a
+  // twiddle product also applies the final 1/2M (and undoes the pointwise R^-1)
+  uint32_t* tw_s = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc(&tw_s, tw_words * 4);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(tw_s, P->d_tw, tw_words * 4, cudaMemcpyDeviceToDevice, P->stream);
+  if (e == cudaSuccess) {
+    kt.mscale<<<(int)std::min<size_t>((tw_words / L + 255) / 256, 4096), 256, 0, P->stream>>>(tw_s, tw_words / L, 2,
+                                                                                               P->mc);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_twr_s, (size_t)(M / m) * 2 * m * L * 4);
+  if (e == cudaSuccess) {
+    kt.build_twr<<<(int)std::min<size_t>(((size_t)(M / m) * m + 255) / 256, 4096), 256, 0, P->stream>>>(
+        tw_s, P->d_twr_s, (long long)(M / m), m, P->mc);
+    e = cudaGetLastError();
+  }
   if (e == cudaSuccess) e = cudaStreamSynchronize(P->stream);
+  cudaFree(tw_s);
   if (e != cudaSuccess) {
     dkss_plan_destroy(P);
     return fail(DKSS_ECUDA, "plan upload failed: %s", cudaGetErrorString(e));
@@ -795,6 +819,7 @@ void dkss_plan_destroy(dkss_plan* P) {
   free_ws(P);
   cudaFree(P->d_tw);
   cudaFree(P->d_twr);
+  cudaFree(P->d_twr_s);
   if (P->h_pin) cudaFreeHost(P->h_pin);
   cudaFree(P->d_stage);
   cudaFree(P->d_sglob);

@@ -426,7 +426,8 @@ struct PassArgs {
   int log_mu_enc;        // fused encode: log2 of the global column count mu_0 (operand position stride)
   long long base_pow;    // (2m)^level
   const uint32_t* twr;   // [M/m][2MM][L]: rho~_s = rho^s R mod p, then W_s (see ring_mul)
-  int scale;             // inverse pass: multiply outputs by mc.kscale
+  int scale;             // inverse pass: 1 multiply outputs by mc.kscale; 2 the twiddle rows are
+                         // pre-scaled, untwiddled elements are multiplied before the DFT
   long long total_cols;  // columns in the launch (npoly * M/m)
   // fused encode (first forward level): elements are sliced from the operands instead of
   // loaded -- poly q < enc_split takes operand q of ops_a, others operand q-enc_split of ops_b
@@ -685,6 +686,13 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArg
       if (s == 0) {
 #pragma unroll
         for (int t = 0; t < kT; ++t) ld_res<L>(res[q][t], buf + el * ES + (k0 + t) * L);
+        if (A.scale == 2) {
+          uint32_t ks[L];
+#pragma unroll
+          for (int qq = 0; qq < L; ++qq) ks[qq] = mc.kscale[qq];
+#pragma unroll
+          for (int t = 0; t < kT; ++t) mont_mul<L>(res[q][t], res[q][t], ks, mc);
+        }
       } else {
         twiddle_mul<MM, L, kT>(A, buf + el * ES, tws + el * EST, s, k0, mc, res[q]);
       }
@@ -706,7 +714,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArg
       const long long off = col_elem(A, cg, vv, LOGE, MM * L, &l);
       uint32_t v[L];
       ld_res<L>(v, ov + el * ES + kk * L);
-      if (A.scale) {
+      if (A.scale == 1) {
         uint32_t ks[L];
 #pragma unroll
         for (int q = 0; q < L; ++q) ks[q] = mc.kscale[q];
