@@ -134,6 +134,9 @@ struct dkss_plan {
   int dyn_grid = 0;                 // >0: row phase as one persistent dependency-driven kernel
   unsigned* d_dyn = nullptr;        // its ticket + per-row counters (cap_batch rows)
   unsigned long long* d_sglob = nullptr;  // per-limb window sums of a distributed decode
+  unsigned* d_tick = nullptr;       // per-launch tile tickets of the CTA kernels, kTickSlots x 2
+  int tick_next = 0;
+  bool dyn_tiles = true;            // DKSS_NO_DYNTILES=1: static round-robin tiles
   void (*rows_fn)(RowsArgs, ModCtx) = nullptr;
   // workspace
   int cap_batch = 0;
@@ -263,6 +266,19 @@ void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStrea
 }
 
 // --- launch helpers (all stream-ordered) ---------------------------------------------
+// ticket counter pair for the next CTA-kernel launch (consecutive launches get different
+// slots, so a PDL-overlapped successor never shares one; each launch re-zeroes its own)
+constexpr int kTickSlots = 64;
+// Only worth it with several tiles per resident CTA: below that the ticket round trip before
+// each prefetch costs more than the balance gains (2^20, 1.7 tiles per CTA: +4%; batch
+// 1024 x 2^18: -9%; the 2^24 inverse, 3.5 tiles per CTA: -1.5%)
+unsigned* next_tick(dkss_plan* P, long long tiles = 1LL << 62, int grid = 1) {
+  if (!P->dyn_tiles || !P->d_tick || tiles < 3LL * grid) return nullptr;
+  unsigned* c = P->d_tick + 2 * (P->tick_next % kTickSlots);
+  ++P->tick_next;
+  return c;
+}
+
 int launch_encode(dkss_plan* P, const uint32_t* ops, long long na, uint32_t* poly, int npoly, cudaStream_t s) {
   EncodeArgs A{ops, na, poly, P->poly_words, npoly, P->M, P->m, P->L, P->u};
   const long long total = 2LL * P->M * P->m * npoly;
@@ -276,7 +292,9 @@ int launch_encode(dkss_plan* P, const uint32_t* ops, long long na, uint32_t* pol
 // pass implementation for a launch over `cols` columns: 1 CTA-fused, 2 warp-fused, 3 split
 int pass_kind(const dkss_plan* P, long long cols) {
   if (P->pass_mode) return (P->pass_mode == 3 && !P->grid_dft) ? 1 : (P->pass_mode == 2 && !P->grid_fw) ? 1 : P->pass_mode;
-  if (P->grid_fw && cols >= 4LL * P->grid_fw * kWarpsPerCta) return 2;
+  // with ticketed tiles the CTA-wide kernel is at least as fast as warp-per-column everywhere
+  // (batch 1024 x 2^18 forward: 5.76 vs 5.81 ms); without them large launches prefer warps
+  if (!P->dyn_tiles && P->grid_fw && cols >= 4LL * P->grid_fw * kWarpsPerCta) return 2;
   return 1;
 }
 
@@ -367,6 +385,7 @@ int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s, c
       const int gw = (int)std::min<long long>(P->grid_fw, (cols * wpc + kWarpsPerCta - 1) / kWarpsPerCta);
       launch_k(P->kt.fwd_w, dim3(gw), dim3(kWarpsPerCta * 32), P->kt.smem_fwd_w, s, A, P->mc);
     } else {
+      A.ctr = next_tick(P, (cols + P->kt.cols - 1) / P->kt.cols, grid);
       launch_k(P->kt.fwd, dim3(grid), dim3(P->kt.nt), smem_pass(P), s, A, P->mc);
     }
     CUCHK(cudaGetLastError());
@@ -406,6 +425,7 @@ int launch_inv_levels(dkss_plan* P, uint32_t* poly, int npoly, bool scale_last, 
       const int gw = (int)std::min<long long>(P->grid_iw, (cols + kWarpsPerCta - 1) / kWarpsPerCta);
       launch_k(P->kt.inv_w, dim3(gw), dim3(kWarpsPerCta * 32), P->kt.smem_inv_w, s, A, P->mc);
     } else {
+      A.ctr = next_tick(P, (cols + P->kt.cols - 1) / P->kt.cols, grid);
       launch_k(P->kt.inv, dim3(grid), dim3(P->kt.nt), smem_pass(P), s, A, P->mc);
     }
     CUCHK(cudaGetLastError());
@@ -427,6 +447,7 @@ int launch_bottom(dkss_plan* P, uint32_t* a, const uint32_t* b, int npoly, int m
   const long long elems = 2LL * P->M * npoly;
   const int grid = (int)std::min<long long>((elems + P->kt.ne - 1) / P->kt.ne, P->grid_bot);
   A.total_elems = elems;
+  A.ctr = next_tick(P, (elems + P->kt.ne - 1) / P->kt.ne, grid);
   launch_k(P->kt.bottom, dim3(grid), dim3(P->kt.nt), smem_two(P), s, A, P->mc);
   CUCHK(cudaGetLastError());
   mark(P, s, DKSS_K_BOTTOM, mode ? rp_work(P, 2LL * P->M * npoly) : 0,
@@ -772,6 +793,12 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
     memcpy(P->mc.cbias, nb.data(), 4 * L);
   }
   CUCHK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+  {
+    const char* nt = getenv("DKSS_NO_DYNTILES");
+    P->dyn_tiles = !(nt && *nt && *nt != '0');
+    CUCHK(cudaMalloc(&P->d_tick, 2 * kTickSlots * sizeof(unsigned)));
+    CUCHK(cudaMemset(P->d_tick, 0, 2 * kTickSlots * sizeof(unsigned)));
+  }
   // twiddle table -> Montgomery form
   const size_t tw_words = (size_t)(M / m) * m * L;
   cudaError_t e = cudaMalloc(&P->d_tw, tw_words * 4);
@@ -820,6 +847,7 @@ void dkss_plan_destroy(dkss_plan* P) {
   cudaFree(P->d_tw);
   cudaFree(P->d_twr);
   cudaFree(P->d_twr_s);
+  cudaFree(P->d_tick);
   if (P->h_pin) cudaFreeHost(P->h_pin);
   cudaFree(P->d_stage);
   cudaFree(P->d_sglob);
@@ -1309,6 +1337,7 @@ int dkss_fs_rows(dkss_plan* P, int world, uint32_t* z, void* stream) {
   A.scale = 0;
   A.total_elems = (long long)rows << P->log_top_mu;
   const int grid = (int)std::min<long long>((A.total_elems + P->kt.ne - 1) / P->kt.ne, P->grid_bot);
+  A.ctr = next_tick(P, (A.total_elems + P->kt.ne - 1) / P->kt.ne, grid);
   launch_k(P->kt.bottom, dim3(grid), dim3(P->kt.nt), smem_two(P), s, A, P->mc);
   CUCHK(cudaGetLastError());
   mark(P, s, DKSS_K_BOTTOM, rp_work(P, A.total_elems), 3LL * A.total_elems * P->m * P->L * 4);

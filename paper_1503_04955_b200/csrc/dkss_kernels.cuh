@@ -98,6 +98,26 @@ struct SmemPlan {
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
+// Tiles of a persistent CTA kernel: handed out from a per-launch counter (ctr[0]) when one
+// is given, so CTAs that finish early take more tiles and the SMs run out of work together
+// (static round-robin leaves one CTA per SM working alone at the end); ctr[1] counts CTAs
+// that ran dry, and the last of them re-zeroes both for the next launch.
+__device__ __forceinline__ long long grab_tile(unsigned* ctr, long long prev, long long* s_slot) {
+  if (!ctr) return prev < 0 ? (long long)blockIdx.x : prev + gridDim.x;
+  __syncthreads();
+  if (threadIdx.x == 0) *s_slot = atomicAdd(ctr, 1u);
+  __syncthreads();
+  return *s_slot;
+}
+__device__ __forceinline__ void release_tiles(unsigned* ctr) {
+  if (!ctr) return;
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+    ctr[0] = 0u;
+    ctr[1] = 0u;
+  }
+}
+
 __device__ __forceinline__ int bitrev_n(int x, int bits) { return bits ? (int)(__brev((unsigned)x) >> (32 - bits)) : 0; }
 
 // ---------------------------------------------------------------------------
@@ -438,6 +458,7 @@ struct PassArgs {
   int u;                 // bits per inner coefficient
   int M;                 // outer length (elements e >= M are zero)
   int wpc;               // warp-per-column kernels: warps sharing one column (power of 2)
+  unsigned* ctr;         // CTA kernels: tile tickets of this launch (null: static round-robin)
 };
 
 template <int MM>
@@ -583,7 +604,8 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArg
     mbar_init(&bar[1], 1);
   }
   __syncthreads();
-  long long tile = blockIdx.x;
+  __shared__ long long s_tile;
+  long long tile = grab_tile(A.ctr, -1, &s_tile);
   const bool enc = A.ops_a != nullptr;
   // PDL: the twiddle rows do not depend on the previous kernel; the elements (and, for the
   // fused encode, the operands) do
@@ -592,11 +614,11 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArg
   griddep_wait();
   if (tile < ntiles && (kSpreadIssue || threadIdx.x < 32))
     issue_pass_tile<MM, L, true>(A, tile, &bar[0], smem, smem + NE * ES, !enc, 2);
-  for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
+  for (int k = 0; tile < ntiles; ++k) {
     const int st = k & 1;
     uint32_t* buf = smem + st * STAGE;
     uint32_t* tws = buf + NE * ES;
-    const long long nxt = tile + gridDim.x;
+    const long long nxt = grab_tile(A.ctr, tile, &s_tile);
     if (nxt < ntiles && (kSpreadIssue || threadIdx.x < 32))
       issue_pass_tile<MM, L, true>(A, nxt, &bar[st ^ 1], smem + (st ^ 1) * STAGE, smem + (st ^ 1) * STAGE + NE * ES,
                                    !enc);
@@ -630,7 +652,9 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArg
     fence_proxy_async();
     __syncthreads();
     TRACE_MARK
+    tile = nxt;
   }
+  release_tiles(A.ctr);
   TRACE_DUMP(enc ? "fwd0" : "fwd")
 }
 
@@ -653,17 +677,18 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArg
     mbar_init(&bar[1], 1);
   }
   __syncthreads();
-  long long tile = blockIdx.x;
+  __shared__ long long s_tile;
+  long long tile = grab_tile(A.ctr, -1, &s_tile);
   if (tile < ntiles && (kSpreadIssue || threadIdx.x < 32))
     issue_pass_tile<MM, L, false>(A, tile, &bar[0], smem, smem + NE * ES, true, 1);
   griddep_wait();  // PDL: twiddle rows above are independent of the previous kernel
   if (tile < ntiles && (kSpreadIssue || threadIdx.x < 32))
     issue_pass_tile<MM, L, false>(A, tile, &bar[0], smem, smem + NE * ES, true, 2);
-  for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
+  for (int k = 0; tile < ntiles; ++k) {
     const int st = k & 1;
     uint32_t* buf = smem + st * STAGE;
     uint32_t* tws = buf + NE * ES;
-    const long long nxt = tile + gridDim.x;
+    const long long nxt = grab_tile(A.ctr, tile, &s_tile);
     if (nxt < ntiles && (kSpreadIssue || threadIdx.x < 32))
       issue_pass_tile<MM, L, false>(A, nxt, &bar[st ^ 1], smem + (st ^ 1) * STAGE, smem + (st ^ 1) * STAGE + NE * ES);
     TRACE_MARK
@@ -725,7 +750,9 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArg
     fence_proxy_async();
     __syncthreads();
     TRACE_MARK
+    tile = nxt;
   }
+  release_tiles(A.ctr);
   TRACE_DUMP("inv")
 }
 
@@ -744,6 +771,7 @@ struct BottomArgs {
   int mode;
   int scale;
   long long total_elems;  // elements in the launch (npoly * 2M)
+  unsigned* ctr;          // tile tickets of this launch (null: static round-robin)
 };
 
 template <int MM, int L>
@@ -794,14 +822,15 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_bottom(BottomArg
     mbar_init(&bar[1], 1);
   }
   __syncthreads();
-  long long tile = blockIdx.x;
+  __shared__ long long s_tile;
+  long long tile = grab_tile(A.ctr, -1, &s_tile);
   if (tile < ntiles && (kSpreadIssue || threadIdx.x < 32))
     issue_bottom_tile<MM, L>(A, tile, &bar[0], smem, smem + NE * ES);
-  for (int k = 0; tile < ntiles; ++k, tile += gridDim.x) {
+  for (int k = 0; tile < ntiles; ++k) {
     const int st = NS == 2 ? (k & 1) : 0;
     uint32_t* sa = smem + st * STAGE;
     uint32_t* sb = sa + NE * ES;
-    const long long nxt = tile + gridDim.x;
+    const long long nxt = grab_tile(A.ctr, tile, &s_tile);
     if (NS == 2 && nxt < ntiles && (kSpreadIssue || threadIdx.x < 32))
       issue_bottom_tile<MM, L>(A, nxt, &bar[st ^ 1], smem + (st ^ 1) * STAGE, smem + (st ^ 1) * STAGE + NE * ES);
     mbar_wait(&bar[st], NS == 2 ? ((k >> 1) & 1) : (k & 1));
@@ -851,7 +880,9 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_bottom(BottomArg
     fence_proxy_async();
     __syncthreads();
     if (NS == 1 && nxt < ntiles && (kSpreadIssue || threadIdx.x < 32)) issue_bottom_tile<MM, L>(A, nxt, &bar[0], smem, smem + NE * ES);
+    tile = nxt;
   }
+  release_tiles(A.ctr);
 }
 
 // standalone batched ring product (stage API r_mul / pointwise): out = y*x (exact)
