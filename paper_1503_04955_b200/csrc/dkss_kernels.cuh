@@ -64,8 +64,12 @@ struct Cfg<8> {
 #define DKSS_CFG16_T 2
 #endif
 template <>
+#ifndef DKSS_CFG16_COLS
+#define DKSS_CFG16_COLS 1
+#endif
 struct Cfg<16> {
-  static constexpr int NT = DKSS_CFG16_NT, COLS = 1, NE = 32, MINB = DKSS_CFG16_MINB, T = DKSS_CFG16_T;
+  static constexpr int NT = DKSS_CFG16_NT, COLS = DKSS_CFG16_COLS, NE = 32 * DKSS_CFG16_COLS, MINB = DKSS_CFG16_MINB,
+                       T = DKSS_CFG16_T;
 #ifdef DKSS_EXP_NOTWS
   static constexpr bool TWS = false;
 #else

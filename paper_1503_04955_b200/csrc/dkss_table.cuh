@@ -61,8 +61,10 @@ KTable make_table() {
     t.rows[3] = k_rows<MM, L, 8>;
     t.rows[4] = k_rows<MM, L, 16>;
     t.smem_rows = RowsSmem<MM, L>::WORDS * 4;
-    t.dyn = k_rows_dyn<MM, L>;
-    t.smem_dyn = DynSmem<MM, L>::WORDS * 4;
+    if constexpr (Cfg<MM>::NE == 2 * MM) {  // one column per work item
+      t.dyn = k_rows_dyn<MM, L>;
+      t.smem_dyn = DynSmem<MM, L>::WORDS * 4;
+    }
   }
   t.rmul = k_rmul<MM, L>;
   t.mscale = k_mont_scale<L>;
