@@ -25,6 +25,8 @@ EXPORTS = (
     "dkss_fs_layout_get", "dkss_fs_columns_fwd", "dkss_fs_rows", "dkss_fs_columns_inv",
     "dkss_block_transpose", "dkss_decode_device", "dkss_lucas_lehmer", "dkss_fs_decode_partial",
     "dkss_fs_decode_finish",
+    # include/smul.h
+    "smul_plan_create", "smul_plan_destroy", "smul_product_limbs", "smul_mul", "smul_mul_device", "smul_fft_host",
 )
 
 DKSS_OK, DKSS_EINVAL, DKSS_ECUDA, DKSS_ERANGE, DKSS_ENOMEM = 0, -1, -2, -3, -4
@@ -59,6 +61,11 @@ class PlanInfo(ctypes.Structure):
 class FsLayout(ctypes.Structure):
     _fields_ = [("cols", ctypes.c_int64), ("rows", ctypes.c_int64), ("elem_words", ctypes.c_int64),
                 ("block_words", ctypes.c_int64), ("decode_seg", ctypes.c_int64)]
+
+
+class SmulPlanDesc(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int64), ("m", ctypes.c_int32), ("s", ctypes.c_int64), ("K", ctypes.c_int32),
+                ("omega_exp", ctypes.c_int32)]
 
 
 _u32p = ctypes.POINTER(ctypes.c_uint32)
@@ -109,6 +116,14 @@ def load(path: str = LIB_PATH):
         L.dkss_fs_decode_partial.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp, vp]
         L.dkss_fs_decode_finish.argtypes = [vp, ctypes.c_int, vp, vp, ctypes.c_size_t, vp]
         L.dkss_lucas_lehmer.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, _u32p, ctypes.c_size_t]
+        L.smul_plan_create.argtypes = [ctypes.POINTER(SmulPlanDesc), ctypes.c_int, ctypes.POINTER(vp)]
+        L.smul_plan_destroy.argtypes = [vp]
+        L.smul_plan_destroy.restype = None
+        L.smul_product_limbs.argtypes = [vp]
+        L.smul_product_limbs.restype = ctypes.c_int64
+        L.smul_mul.argtypes = [vp, _u32p, ctypes.c_size_t, _u32p, ctypes.c_size_t, _u32p, ctypes.c_size_t]
+        L.smul_mul_device.argtypes = [vp, ctypes.c_int, vp, vp, ctypes.c_size_t, vp, ctypes.c_size_t, vp]
+        L.smul_fft_host.argtypes = [vp, _u32p, _u32p, ctypes.c_int]
         for name in EXPORTS:
             if not hasattr(L, name):
                 raise NativeUnavailable(f"{path} lacks symbol {name}")
@@ -283,3 +298,39 @@ class DevicePlan:
         s = np.ascontiguousarray(s, dtype=np.uint32).copy()
         _check(self._lib.dkss_lucas_lehmer(self._h, p, iters, _ptr(s), s.size))
         return s
+
+
+class SmulDevicePlan:
+    """An outermost Schoenhage-Strassen plan (bigmul/smul.py:20-30) on one GPU (include/smul.h)."""
+
+    def __init__(self, N: int, m: int, s: int, K: int, omega_exp: int, device: int = 0):
+        lib = load()
+        self.N, self.m, self.s, self.K, self.omega_exp, self.device = N, m, s, K, omega_exp, device
+        desc = SmulPlanDesc(N, m, s, K, omega_exp)
+        h = ctypes.c_void_p()
+        _check(lib.smul_plan_create(ctypes.byref(desc), device, ctypes.byref(h)))
+        self._h = h
+        self._lib = lib
+        self.product_limbs = int(lib.smul_product_limbs(h))
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.smul_plan_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def mul_limbs(self, a: np.ndarray, b: np.ndarray, nc: int) -> np.ndarray:
+        out = np.zeros(max(nc, 1), dtype=np.uint32)
+        if b is a:
+            _check(self._lib.smul_mul(self._h, _ptr(a), a.size, _ptr(a), a.size, _ptr(out), nc))
+        else:
+            _check(self._lib.smul_mul(self._h, _ptr(a), a.size, _ptr(b), b.size, _ptr(out), nc))
+        return out[:nc]
+
+    def mul_device(self, batch: int, a_ptr: int, b_ptr: int, n_limbs: int, c_ptr: int, nc: int, stream: int = 0):
+        _check(self._lib.smul_mul_device(self._h, batch, a_ptr, b_ptr, n_limbs, c_ptr, nc, stream))
+
+    def fft(self, x: np.ndarray, top: np.ndarray, inverse: bool = False):
+        """fft_eval in place: x uint32[n][K/32], top uint32[n]; shuffled in, natural out."""
+        _check(self._lib.smul_fft_host(self._h, _ptr(x), _ptr(top), 1 if inverse else 0))

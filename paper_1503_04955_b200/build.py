@@ -34,7 +34,7 @@ INSTANCES = [(m, L) for m in (8, 16, 32) for L in (2, 3, 4, 5, 6)]
 
 
 def _headers():
-    return glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(INCLUDE, "dkss.h")]
+    return glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INCLUDE, "*.h"))
 
 
 def _stale(target: str, deps) -> bool:

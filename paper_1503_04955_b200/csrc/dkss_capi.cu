@@ -1533,3 +1533,6 @@ int dkss_decode_host(dkss_plan* P, const uint32_t* v, uint32_t* out, size_t nout
 }
 
 }  // extern "C"
+
+// Schoenhage-Strassen multiply (include/smul.h)
+#include "smul_capi.cuh"

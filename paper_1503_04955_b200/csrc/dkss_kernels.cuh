@@ -1137,20 +1137,19 @@ __device__ __forceinline__ unsigned long long window_sum(const DecodeArgs& A, co
   return S;
 }
 
-// phase 1: per-limb sums, per-warp (generate, propagate) masks, per-block carry function
-__global__ void __launch_bounds__(kDecThreads) k_decode1(DecodeArgs A) {
-  griddep_wait();  // PDL: predecessor grid complete, its writes visible
-  griddep_launch();
+// phase 1: per-limb sums, per-warp (generate, propagate) masks, per-block carry function.
+// `sum(pidx, t)` is the 64-bit sum of the 32-bit windows that land on limb t (every
+// window sum is < 2^35, so limb t = low(S_t) + high(S_(t-1)) carries at most one bit).
+template <class SumFn>
+__device__ __forceinline__ void decode1_body(const DecodeArgs& A, SumFn sum) {
   const int pidx = blockIdx.x / A.blocks_per_poly;
   const int blk = blockIdx.x % A.blocks_per_poly;
   const long long t = (long long)blk * kDecThreads + threadIdx.x;
-  const uint32_t* v = A.v + (long long)pidx * A.poly_words;
   __shared__ unsigned long long sS[kDecThreads + 1];
   __shared__ uint32_t wg[kDecWarps], wp[kDecWarps];
-  unsigned long long S = t < A.nout ? (A.sglob ? A.sglob[t] : window_sum(A, v, t)) : 0ull;
+  unsigned long long S = t < A.nout ? sum(pidx, t) : 0ull;
   sS[threadIdx.x + 1] = S;
-  if (threadIdx.x == 0)
-    sS[0] = (t < A.nout && t > 0) ? (A.sglob ? A.sglob[t - 1] : window_sum(A, v, t - 1)) : 0ull;
+  if (threadIdx.x == 0) sS[0] = (t < A.nout && t > 0) ? sum(pidx, t - 1) : 0ull;
   __syncthreads();
   unsigned long long w = (S & 0xFFFFFFFFull) + (sS[threadIdx.x] >> 32);
   if (t >= A.nout) w = 0;
@@ -1178,6 +1177,14 @@ __global__ void __launch_bounds__(kDecThreads) k_decode1(DecodeArgs A) {
       A.bstat[(long long)pidx * A.blocks_per_poly + blk] = co0 | (co1 << 1);
     }
   }
+}
+
+__global__ void __launch_bounds__(kDecThreads) k_decode1(DecodeArgs A) {
+  griddep_wait();  // PDL: predecessor grid complete, its writes visible
+  griddep_launch();
+  decode1_body(A, [&](int pidx, long long t) {
+    return A.sglob ? A.sglob[t] : window_sum(A, A.v + (long long)pidx * A.poly_words, t);
+  });
 }
 
 // phase 2: one CTA per product turns the block carry functions into block carry-ins

@@ -1,0 +1,313 @@
+// smul_capi.cuh -- host side of the SMUL multiply (include/smul.h); included at the end of
+// dkss_capi.cu so it shares the launch helper, the error channel and the carry-scan kernels.
+#pragma once
+#include <algorithm>
+#include "../../include/smul.h"
+#include "smul_kernels.cuh"
+
+struct smul_plan {
+  int device = 0;
+  long long N = 0, s = 0, n = 0;
+  int m = 0, K = 0, KW = 0, Q = 1, omega_exp = 0;
+  long long prod_limbs = 0;
+  std::vector<std::pair<int, int>> passes;  // (lv0, nlv) per FFT pass
+  size_t smem_fft = 0, smem_pw = 0;
+  cudaStream_t stream = nullptr;
+  int cap = 0;  // operands the workspace holds (a's and b's)
+  long long cap_nc = 0;
+  uint32_t *d_x = nullptr, *d_xt = nullptr, *d_o = nullptr, *d_ot = nullptr;
+  uint32_t *d_ops = nullptr, *d_prod = nullptr, *d_gmask = nullptr, *d_pmask = nullptr, *d_bstat = nullptr;
+  std::mutex mu;
+};
+
+namespace {
+
+constexpr int kSmulPwWarps = 4;
+constexpr size_t kSmulFftSmemMax = 96 * 1024;
+
+template <int Q>
+int smul_set_attrs(smul_plan* P) {
+  CUCHK(cudaFuncSetAttribute(k_smul_fft<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmulFftSmemMax));
+  // the attribute is per kernel, not per plan: allow the largest plan this Q serves
+  const int pw_max = kSmulPwWarps * 10 * 32 * Q * 4;
+  CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, pw_max));
+  return 0;
+}
+
+int smul_attrs(smul_plan* P) {
+  switch (P->Q) {
+    case 1: return smul_set_attrs<1>(P);
+    case 2: return smul_set_attrs<2>(P);
+    case 4: return smul_set_attrs<4>(P);
+    case 8: return smul_set_attrs<8>(P);
+    case 16: return smul_set_attrs<16>(P);
+    case 32: return smul_set_attrs<32>(P);
+  }
+  return fail(DKSS_EINVAL, "unsupported limb count per lane %d", P->Q);
+}
+
+template <int Q>
+void smul_fft_q(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool inverse, bool normalise, cudaStream_t s) {
+  SmulFftArgs A{};
+  A.x = x;
+  A.top = top;
+  A.log_n = P->m;
+  A.KW = P->KW;
+  A.K = P->K;
+  A.omega_exp = inverse ? (2 * P->K - P->omega_exp) % (2 * P->K) : P->omega_exp;
+  for (size_t i = 0; i < P->passes.size(); ++i) {
+    A.lv0 = P->passes[i].first;
+    A.nlv = P->passes[i].second;
+    A.post_e = (normalise && i + 1 == P->passes.size()) ? (2 * P->K - P->m) % (2 * P->K) : -1;
+    const int G = 1 << A.nlv;
+    const size_t smem = (size_t)G * P->KW * 4 + (size_t)G * 4;
+    const int nt = std::min(kSmulThreads, std::max(32, G / 2 * 32));
+    launch_k(k_smul_fft<Q>, dim3((unsigned)(P->n >> A.nlv), npoly), dim3(nt), smem, s, A);
+  }
+}
+
+void smul_fft(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool inverse, bool normalise, cudaStream_t s) {
+  switch (P->Q) {
+    case 1: return smul_fft_q<1>(P, x, top, npoly, inverse, normalise, s);
+    case 2: return smul_fft_q<2>(P, x, top, npoly, inverse, normalise, s);
+    case 4: return smul_fft_q<4>(P, x, top, npoly, inverse, normalise, s);
+    case 8: return smul_fft_q<8>(P, x, top, npoly, inverse, normalise, s);
+    case 16: return smul_fft_q<16>(P, x, top, npoly, inverse, normalise, s);
+    case 32: return smul_fft_q<32>(P, x, top, npoly, inverse, normalise, s);
+  }
+}
+
+template <int Q>
+void smul_pw_q(smul_plan* P, const SmulPwArgs& A, cudaStream_t s) {
+  const long long blocks = (A.count + kSmulPwWarps - 1) / kSmulPwWarps;
+  launch_k(k_smul_pointwise<Q>, dim3((unsigned)std::min<long long>(blocks, 148LL * 16)), dim3(32 * kSmulPwWarps),
+           P->smem_pw, s, A);
+}
+
+void smul_pointwise(smul_plan* P, const SmulPwArgs& A, cudaStream_t s) {
+  switch (P->Q) {
+    case 1: return smul_pw_q<1>(P, A, s);
+    case 2: return smul_pw_q<2>(P, A, s);
+    case 4: return smul_pw_q<4>(P, A, s);
+    case 8: return smul_pw_q<8>(P, A, s);
+    case 16: return smul_pw_q<16>(P, A, s);
+    case 32: return smul_pw_q<32>(P, A, s);
+  }
+}
+
+void smul_free(smul_plan* P) {
+  for (uint32_t** p : {&P->d_x, &P->d_xt, &P->d_o, &P->d_ot, &P->d_ops, &P->d_prod, &P->d_gmask, &P->d_pmask,
+                       &P->d_bstat}) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+  }
+  P->cap = 0;
+  P->cap_nc = 0;
+}
+
+// workspace for `ops` transforms (a's and b's) and products of nc limbs
+int smul_ensure(smul_plan* P, int ops, long long nc) {
+  if (ops <= P->cap && nc <= P->cap_nc) return 0;
+  ops = std::max(ops, P->cap);
+  nc = std::max(nc, P->cap_nc);
+  smul_free(P);
+  const size_t vec = (size_t)P->n * P->KW;
+  const int prods = ops;  // products never outnumber the transforms
+  const long long blocks = (nc + kDecThreads - 1) / kDecThreads;
+  CUCHK(cudaMalloc(&P->d_x, (size_t)ops * vec * 4));
+  CUCHK(cudaMalloc(&P->d_xt, (size_t)ops * P->n * 4));
+  CUCHK(cudaMalloc(&P->d_o, (size_t)prods * vec * 4));
+  CUCHK(cudaMalloc(&P->d_ot, (size_t)prods * P->n * 4));
+  CUCHK(cudaMalloc(&P->d_ops, (size_t)ops * P->prod_limbs * 4));
+  CUCHK(cudaMalloc(&P->d_prod, (size_t)prods * nc * 4));
+  CUCHK(cudaMalloc(&P->d_gmask, (size_t)prods * blocks * kDecWarps * 4));
+  CUCHK(cudaMalloc(&P->d_pmask, (size_t)prods * blocks * kDecWarps * 4));
+  CUCHK(cudaMalloc(&P->d_bstat, (size_t)prods * blocks * 4));
+  P->cap = ops;
+  P->cap_nc = nc;
+  return 0;
+}
+
+// the whole multiply, stream-ordered: encode, forward FFTs, pointwise, inverse FFT (+2^-m),
+// overlap-add with carry resolution (bigmul/smul.py:238-249, 256-271)
+int run_smul(smul_plan* P, int batch, const uint32_t* a, const uint32_t* b, long long na, uint32_t* c, long long nc,
+             cudaStream_t s) {
+  const bool sq = b == nullptr;
+  const int ops = (sq ? 1 : 2) * batch;
+  int rc;
+  if ((rc = smul_ensure(P, ops, nc))) return rc;
+  const long long vec = P->n * P->KW;
+  SmulEncodeArgs E{};
+  E.na = na;
+  E.log_n = P->m;
+  E.KW = P->KW;
+  E.s = P->s;
+  const int gx = (int)std::max<long long>(1, std::min<long long>((vec + 255) / 256, 1184 / std::max(1, batch) + 1));
+  for (int q = 0; q < (sq ? 1 : 2); ++q) {
+    E.a = q ? b : a;
+    E.x = P->d_x + (size_t)q * batch * vec;
+    E.top = P->d_xt + (size_t)q * batch * P->n;
+    launch_k(k_smul_encode, dim3(gx, batch), dim3(256), 0, s, E);
+  }
+  smul_fft(P, P->d_x, P->d_xt, ops, false, false, s);
+  SmulPwArgs W{};
+  W.x = P->d_x;
+  W.xtop = P->d_xt;
+  W.y = sq ? P->d_x : P->d_x + (size_t)batch * vec;
+  W.ytop = sq ? P->d_xt : P->d_xt + (size_t)batch * P->n;
+  W.out = P->d_o;
+  W.otop = P->d_ot;
+  W.log_n = P->m;
+  W.KW = P->KW;
+  W.count = (long long)batch * P->n;
+  smul_pointwise(P, W, s);
+  smul_fft(P, P->d_o, P->d_ot, batch, true, true, s);
+  DecodeArgs A{};
+  A.out = c;
+  A.nout = nc;
+  A.gmask = P->d_gmask;
+  A.pmask = P->d_pmask;
+  A.bstat = P->d_bstat;
+  A.blocks_per_poly = (int)((nc + kDecThreads - 1) / kDecThreads);
+  SmulDecodeArgs D{};
+  D.x = P->d_o;
+  D.log_n = P->m;
+  D.KW = P->KW;
+  D.s = P->s;
+  launch_k(k_smul_decode1, dim3(A.blocks_per_poly * batch), dim3(kDecThreads), 0, s, A, D);
+  launch_k(k_decode_scan, dim3(batch), dim3(kScanThreads), 0, s, A);
+  launch_k(k_decode2, dim3(A.blocks_per_poly * batch), dim3(kDecThreads), 0, s, A);
+  CUCHK(cudaGetLastError());
+  return 0;
+}
+
+long long bitlen_limbs(const uint32_t* a, size_t na) {
+  while (na > 0 && a[na - 1] == 0) --na;
+  return na ? (long long)(na - 1) * 32 + (32 - __builtin_clz(a[na - 1])) : 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int smul_plan_create(const smul_plan_desc* d, int device, smul_plan** out) {
+  if (!d || !out) return fail(DKSS_EINVAL, "bad argument");
+  *out = nullptr;
+  if (d->m < 1 || d->m > 26) return fail(DKSS_EINVAL, "FFT depth m=%d outside [1, 26]", d->m);
+  const long long n = 1LL << d->m;
+  if (d->s < 1 || d->s * n != d->N) return fail(DKSS_EINVAL, "N must equal s * 2^m");  // bigmul/smul.py:37-38
+  if (d->K % 32) return fail(DKSS_EINVAL, "K=%d not a multiple of 32 (device limbs)", d->K);
+  if ((long long)d->K < d->m + 2 * d->s + 1) return fail(DKSS_EINVAL, "K below the convolution bound m + 2s + 1");
+  if ((2LL * d->K) % n) return fail(DKSS_EINVAL, "outermost level needs n | 2K");  // bigmul/smul.py:43-45
+  if ((long long)d->omega_exp * n != 2LL * d->K) return fail(DKSS_EINVAL, "omega_exp must be 2K/n");
+  if (d->K > 32 * 1024) return fail(DKSS_EINVAL, "K=%d above the device limit 32768", d->K);
+  auto* P = new smul_plan();
+  P->device = device;
+  P->N = d->N;
+  P->m = d->m;
+  P->n = n;
+  P->s = d->s;
+  P->K = d->K;
+  P->KW = d->K / 32;
+  P->omega_exp = d->omega_exp;
+  P->prod_limbs = (d->N + 31) / 32;
+  int q = (P->KW + 31) / 32, Q = 1;
+  while (Q < q) Q <<= 1;
+  P->Q = Q;
+  // FFT passes: as many levels per CTA as kSmulFftSmemMax holds, split evenly
+  int nlv_max = 1;
+  while (nlv_max < 12 && ((size_t)P->KW * 4 + 4) << (nlv_max + 1) <= kSmulFftSmemMax) ++nlv_max;
+  const int npass = (P->m + nlv_max - 1) / nlv_max;
+  for (int i = 0, lv = 0; i < npass; ++i) {
+    const int nl = (P->m - lv + (npass - i) - 1) / (npass - i);
+    P->passes.emplace_back(lv, nl);
+    lv += nl;
+  }
+  P->smem_pw = (size_t)kSmulPwWarps * 10 * P->KW * 4;
+  int rc;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete P;
+    return fail(DKSS_ECUDA, "smul_plan_create: %s", cudaGetErrorString(e));
+  }
+  if ((rc = smul_attrs(P))) {
+    cudaStreamDestroy(P->stream);
+    delete P;
+    return rc;
+  }
+  *out = P;
+  return DKSS_OK;
+}
+
+void smul_plan_destroy(smul_plan* P) {
+  if (!P) return;
+  cudaSetDevice(P->device);
+  smul_free(P);
+  if (P->stream) cudaStreamDestroy(P->stream);
+  delete P;
+}
+
+int64_t smul_product_limbs(const smul_plan* P) { return P ? P->prod_limbs : -1; }
+
+int smul_mul_device(smul_plan* P, int batch, const uint32_t* a_dev, const uint32_t* b_dev, size_t n_limbs,
+                    uint32_t* c_dev, size_t nc, void* stream) {
+  if (!P || batch < 1 || !a_dev || !c_dev) return fail(DKSS_EINVAL, "bad argument");
+  if ((long long)nc < P->prod_limbs) return fail(DKSS_EINVAL, "nc=%zu below the plan's %lld product limbs", nc, P->prod_limbs);
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  return run_smul(P, batch, a_dev, b_dev, (long long)n_limbs, c_dev, (long long)nc, (cudaStream_t)stream);
+}
+
+int smul_mul(smul_plan* P, const uint32_t* a, size_t na, const uint32_t* b, size_t nb, uint32_t* c, size_t nc) {
+  if (!P || (!a && na) || (!b && nb) || (!c && nc)) return fail(DKSS_EINVAL, "bad argument");
+  const long long ba = bitlen_limbs(a, na), bb = bitlen_limbs(b, nb);
+  if (ba + bb > P->N) return fail(DKSS_ERANGE, "product of %lld + %lld bits exceeds N=%lld", ba, bb, P->N);
+  const bool sq = a == b && na == nb;
+  const size_t la = (size_t)(ba + 31) / 32, lb = (size_t)(bb + 31) / 32;
+  const size_t nl = std::max<size_t>(1, std::max(la, lb));
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  int rc;
+  if ((rc = smul_ensure(P, 2, P->prod_limbs))) return rc;
+  cudaStream_t s = P->stream;
+  if (nl > (size_t)P->prod_limbs) return fail(DKSS_ERANGE, "operand does not fit the plan");
+  uint32_t* da = P->d_ops;
+  uint32_t* db = P->d_ops + nl;
+  CUCHK(cudaMemsetAsync(P->d_ops, 0, 2 * nl * 4, s));
+  if (la) CUCHK(cudaMemcpyAsync(da, a, la * 4, cudaMemcpyHostToDevice, s));
+  if (!sq && lb) CUCHK(cudaMemcpyAsync(db, b, lb * 4, cudaMemcpyHostToDevice, s));
+  if ((rc = run_smul(P, 1, da, sq ? nullptr : db, (long long)nl, P->d_prod, P->prod_limbs, s))) return rc;
+  std::vector<uint32_t> full((size_t)P->prod_limbs);
+  CUCHK(cudaMemcpyAsync(full.data(), P->d_prod, full.size() * 4, cudaMemcpyDeviceToHost, s));
+  CUCHK(cudaStreamSynchronize(s));
+  const size_t ncopy = std::min<size_t>(nc, full.size());
+  for (size_t k = ncopy; k < full.size(); ++k)
+    if (full[k]) return fail(DKSS_ERANGE, "product does not fit nc=%zu limbs", nc);
+  if (ncopy) memcpy(c, full.data(), ncopy * 4);
+  if (nc > ncopy) memset(c + ncopy, 0, (nc - ncopy) * 4);
+  return DKSS_OK;
+}
+
+int smul_fft_host(smul_plan* P, uint32_t* x, uint32_t* top, int inverse) {
+  if (!P || !x || !top) return fail(DKSS_EINVAL, "bad argument");
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  int rc;
+  if ((rc = smul_ensure(P, 1, P->prod_limbs))) return rc;
+  cudaStream_t s = P->stream;
+  const size_t vec = (size_t)P->n * P->KW;
+  for (long long i = 0; i < P->n; ++i)
+    if (top[i] > 1 || (top[i] && std::any_of(x + i * P->KW, x + (i + 1) * P->KW, [](uint32_t w) { return w != 0; })))
+      return fail(DKSS_EINVAL, "element %lld is not canonical in [0, 2^K]", i);
+  CUCHK(cudaMemcpyAsync(P->d_x, x, vec * 4, cudaMemcpyHostToDevice, s));
+  CUCHK(cudaMemcpyAsync(P->d_xt, top, P->n * 4, cudaMemcpyHostToDevice, s));
+  smul_fft(P, P->d_x, P->d_xt, 1, inverse != 0, false, s);
+  CUCHK(cudaGetLastError());
+  CUCHK(cudaMemcpyAsync(x, P->d_x, vec * 4, cudaMemcpyDeviceToHost, s));
+  CUCHK(cudaMemcpyAsync(top, P->d_xt, P->n * 4, cudaMemcpyDeviceToHost, s));
+  CUCHK(cudaStreamSynchronize(s));
+  return DKSS_OK;
+}
+
+}  // extern "C"

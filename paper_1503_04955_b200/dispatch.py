@@ -1,9 +1,10 @@
 """``mul`` and the ``ALGORITHMS`` plugin table (bigmul/dispatch.py:11-46).
 
-Only the DKSS rung is provided (this build is the drop-in for the reference's
-dmul path); the other rungs of the reference ladder (omul,
-kmul, t3mul, qmul, smul) are out of scope and raise ``NotImplementedError``
-naming the rung, rather than silently computing the product some other way.
+The DKSS rung (this build is the drop-in for the reference's dmul path, SURVEY.md
+§8(b)) and the Schoenhage-Strassen rung (its comparison baseline, §8(f) rank 3) run on
+the GPU; the other rungs of the reference ladder (omul, kmul, t3mul, qmul) are out of
+scope and raise ``NotImplementedError`` naming the rung, rather than silently computing
+the product some other way.
 INTEGRATION.md shows how the reference registers this dmul in its own table.
 """
 
@@ -48,6 +49,12 @@ def set_default_thresholds(table: ThresholdTable) -> None:
     _default = table.validate()
 
 
+def _smul(a, b, table, arena):
+    from .smul import smul
+
+    return smul(a, b, table, arena)
+
+
 def _out_of_scope(name):
     def fn(a, b, table, arena):
         raise NotImplementedError(f"algorithm {name!r} is not part of the B200 DKSS build; "
@@ -60,7 +67,7 @@ ALGORITHMS = {
     "kmul": _out_of_scope("kmul"),
     "t3mul": _out_of_scope("t3mul"),
     "qmul": _out_of_scope("qmul"),
-    "smul": _out_of_scope("smul"),
+    "smul": lambda a, b, table, arena: _smul(a, b, table, arena),
     "dmul": lambda a, b, table, arena: dmul(a, b, table, arena),
 }
 

@@ -15,7 +15,7 @@ def test_unknown_algorithm():
 
 def test_out_of_scope_rungs_raise():
     with pytest.raises(NotImplementedError):
-        mul(3, 5, algorithm="smul")
+        mul(3, 5, algorithm="t3mul")
     with pytest.raises(NotImplementedError):
         mul(3, 5)  # default ladder would pick omul
 
@@ -31,6 +31,11 @@ def test_dmul_zero_shortcut_needs_no_device():
     assert r.to_int() == 0 and len(r) == 3     # bigmul/dkss.py:529-531
     r = mul(0, a, algorithm="dmul")
     assert r.to_int() == 0
+
+
+def test_smul_zero_shortcut_needs_no_device():
+    r = mul(Natural.from_int(7, length=3), 0, algorithm="smul")  # bigmul/smul.py:290-292
+    assert r.to_int() == 0 and len(r) == 4
 
 
 def test_dmul_argument_types():

@@ -1,5 +1,5 @@
-"""The C-ABI library loads and exports every symbol include/dkss.h declares (no compute:
-runs on CPU-only machines)."""
+"""The C-ABI library loads and exports every symbol include/dkss.h and include/smul.h
+declare (no compute: runs on CPU-only machines)."""
 import os
 import re
 
@@ -9,9 +9,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _declared():
-    with open(os.path.join(ROOT, "include", "dkss.h")) as f:
-        src = f.read()
-    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(dkss_\w+)\s*\(", src, re.M)))
+    names = set()
+    for h in ("dkss.h", "smul.h"):
+        with open(os.path.join(ROOT, "include", h)) as f:
+            src = f.read()
+        names |= set(re.findall(r"^\s*(?:int|int64_t|void|const char\*)\s+((?:dkss|smul)_\w+)\s*\(", src, re.M))
+    return sorted(names)
 
 
 def test_header_declares_expected_entry_points():
@@ -31,3 +34,4 @@ def test_structs_match_header_layout():
 
     assert ctypes.sizeof(_native.PlanDesc) == 8 + 4 * 4 + 2 * 8
     assert ctypes.sizeof(_native.PlanInfo) >= 8 * 7 + 4 * 7
+    assert ctypes.sizeof(_native.SmulPlanDesc) == 8 + 4 + 4 + 8 + 4 + 4  # include/smul.h, padded

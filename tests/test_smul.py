@@ -1,0 +1,176 @@
+"""SMUL, the reference's comparison baseline: plan selection pinned
+field for field to the reference's smul_select_params (tests/golden/smul_plans.json, made
+by tools/make_golden_smul.py from the reference itself); on the GPU, fft_eval over the
+Fermat ring against the reference's transform vectors (tests/golden/smul_stages.npz) and
+the full product against a*b."""
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+from paper_1503_04955_b200 import Natural, mul
+from paper_1503_04955_b200.dispatch import ThresholdTable
+from paper_1503_04955_b200.smul import (SmulPlan, device_select_params, fft_eval_fermat, smul,
+                                        smul_plan_candidates, smul_select_params)
+from paper_1503_04955_b200.words import int_to_u32, using_word_bits
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _load(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def _fields(p: SmulPlan):
+    return {"N": p.N, "m": p.m, "n": p.n, "s": p.s, "K": p.K, "omega_exp": p.omega_exp,
+            "theta_exp": p.theta_exp, "outermost": p.outermost, "w": p.w}
+
+
+def test_plans_match_reference():
+    g = _load("smul_plans.json")
+    assert len(g["plans"]) > 100
+    for e in g["plans"]:
+        with using_word_bits(e["w"]):
+            assert _fields(smul_select_params(e["n0"], True, e["w"])) == e["plan"], e
+            assert len(smul_plan_candidates(e["n0"], True, e["w"])) == e["candidates"], e
+
+
+def test_forced_depth_matches_reference():
+    for e in _load("smul_plans.json")["forced"]:
+        t = ThresholdTable()
+        t.smul_fft_m[max(0, (e["n0"] // 64).bit_length() - 1)] = e["m"]
+        p = smul_select_params(e["n0"], True, 64, t)
+        assert _fields(p) == e["plan"]  # a depth with no candidate falls back to the cost model
+
+
+def test_plan_validation_errors():
+    with pytest.raises(ValueError):
+        SmulPlan(1001, 3, 8, 125, 1024, 256, 0, True, 64).validate()  # N != s * n
+    with pytest.raises(ValueError):
+        SmulPlan(1024, 3, 8, 128, 192, 48, 0, True, 64).validate()    # K below m + 2s + 1
+
+
+@pytest.mark.parametrize("e", range(9, 30, 2))
+def test_device_plans_are_valid_candidates(e):
+    p = device_select_params(1 << e, 64)
+    assert p.K % 32 == 0 and p.K <= 32768 and p.N >= 1 << e
+    assert p in smul_plan_candidates(1 << e, True, 64)
+
+
+# ---- GPU ------------------------------------------------------------------------------
+
+def _elems(x, top, K):
+    return [int.from_bytes(x[i].tobytes(), "little") | (int(top[i]) << K) for i in range(len(top))]
+
+
+def _stage_sets():
+    return _load("smul_stages_index.json")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("idx", range(3))
+def test_fft_matches_reference(cuda_ok, idx):
+    e = _stage_sets()[idx]
+    p = SmulPlan(**e["plan"])
+    z = np.load(os.path.join(GOLD, "smul_stages.npz"))
+    t = e["tag"]
+    v = _elems(z[f"{t}_a_shuffled"], z[f"{t}_a_shuffled_top"], p.K)
+    fft_eval_fermat(v, p)
+    assert v == _elems(z[f"{t}_a_fft"], z[f"{t}_a_fft_top"], p.K)
+    v = _elems(z[f"{t}_v"], z[f"{t}_v_top"], p.K)  # holds 0 and 2^K
+    fft_eval_fermat(v, p, inverse=True)
+    assert v == _elems(z[f"{t}_v_inv"], z[f"{t}_v_inv_top"], p.K)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("idx", range(3))
+def test_product_on_reference_plan(cuda_ok, idx):
+    from paper_1503_04955_b200._native import SmulDevicePlan
+
+    e = _stage_sets()[idx]
+    p = e["plan"]
+    z = np.load(os.path.join(GOLD, "smul_stages.npz"))
+    t = e["tag"]
+    dp = SmulDevicePlan(p["N"], p["m"], p["s"], p["K"], p["omega_exp"])
+    prod = z[f"{t}_prod"]
+    c = dp.mul_limbs(z[f"{t}_a"].copy(), z[f"{t}_b"].copy(), prod.size)
+    assert np.array_equal(c, prod)
+
+
+@pytest.mark.gpu
+def test_smul_equals_product(cuda_ok):
+    rng = random.Random(7)
+    for bits in (1, 31, 32, 33, 100, 511, 512, 4096, 20000, 65537, 1 << 18, 1 << 20):
+        a = rng.getrandbits(bits) | 1 << (bits - 1)
+        b = rng.getrandbits(bits) | 1 << (bits - 1)
+        assert smul(a, b).to_int() == a * b, bits
+        c = rng.getrandbits(max(1, bits // 5)) | 1
+        assert smul(a, c).to_int() == a * c, bits  # unbalanced
+        assert smul(a, a).to_int() == a * a, bits  # square
+
+
+@pytest.mark.gpu
+def test_smul_edge_values(cuda_ok):
+    for bits in (64, 3000, 1 << 16, 1 << 21):
+        ones = (1 << bits) - 1                       # longest carry chains
+        assert smul(ones, ones).to_int() == ones * ones
+        assert smul(1 << (bits - 1), 1 << (bits - 1)).to_int() == 1 << (2 * bits - 2)
+        assert smul(ones, 1).to_int() == ones
+    r = smul(Natural.from_int(0, length=4), 12345)
+    assert r.to_int() == 0 and len(r) == 5
+
+
+@pytest.mark.gpu
+def test_smul_result_length_and_routing(cuda_ok):
+    rng = random.Random(11)
+    a = Natural.from_int(rng.getrandbits(6400), length=120)
+    b = Natural.from_int(rng.getrandbits(6400), length=101)
+    r = mul(a, b, algorithm="smul")
+    assert len(r) == 221 and r.to_int() == a.to_int() * b.to_int()
+    for w in (8, 32):
+        with using_word_bits(w):
+            x = rng.getrandbits(5000 * w // 8) | 1
+            y = rng.getrandbits(4000 * w // 8) | 1
+            assert smul(x, y).to_int() == x * y
+
+
+@pytest.mark.gpu
+def test_smul_device_batch(cuda_ok):
+    import torch
+
+    from paper_1503_04955_b200.smul import device_plan_for
+
+    rng = random.Random(3)
+    bits, batch = 1 << 16, 8
+    p, dp = device_plan_for(2 * bits, 64)
+    nl = bits // 32
+    A = [rng.getrandbits(bits) for _ in range(batch)]
+    B = [rng.getrandbits(bits) for _ in range(batch)]
+    da = torch.from_numpy(np.stack([int_to_u32(x, nl) for x in A]).view(np.int32)).cuda()
+    db = torch.from_numpy(np.stack([int_to_u32(x, nl) for x in B]).view(np.int32)).cuda()
+    nc = dp.product_limbs
+    dc = torch.zeros(batch, nc, dtype=torch.int32, device="cuda")
+    dp.mul_device(batch, da.data_ptr(), db.data_ptr(), nl, dc.data_ptr(), nc, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    C = dc.cpu().numpy().view(np.uint32)
+    for i in range(batch):
+        assert int.from_bytes(C[i].tobytes(), "little") == A[i] * B[i]
+    dp.mul_device(batch, da.data_ptr(), 0, nl, dc.data_ptr(), nc, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    C = dc.cpu().numpy().view(np.uint32)
+    assert all(int.from_bytes(C[i].tobytes(), "little") == A[i] * A[i] for i in range(batch))
+
+
+@pytest.mark.gpu
+def test_smul_range_errors(cuda_ok):
+    from paper_1503_04955_b200._native import SmulDevicePlan
+
+    dp = SmulDevicePlan(4096, 3, 512, 1088, 272)
+    a = int_to_u32((1 << 3000) - 1, 94)
+    with pytest.raises(ValueError):
+        dp.mul_limbs(a, a, 200)  # 6000-bit product does not fit N = 4096
+    with pytest.raises(ValueError):
+        SmulDevicePlan(4096, 3, 512, 1080, 270)  # K not a multiple of 32
