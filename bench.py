@@ -440,6 +440,38 @@ def main():
     e2e_times.sort()
     e2e_s = e2e_times[len(e2e_times) // 2]
 
+    # the thesis's comparison baseline on the same operands: SMUL device time and T_DMUL / T_SMUL
+    # (bigmul/bench.py:80-91), L2 flushed before every call
+    smul_line = None
+    try:
+        from paper_1503_04955_b200.smul import device_plan_for
+        splan, sdp = device_plan_for(2 * N, 64)
+        snc = sdp.product_limbs
+        dS = torch.zeros((batch, snc), dtype=torch.int32, device=dev)
+
+        def sstep():
+            sdp.mul_device(batch, dA.data_ptr(), dB.data_ptr(), nl, dS.data_ptr(), snc, sp)
+
+        sstep()
+        torch.cuda.synchronize(dev)
+        S0 = dS[0].cpu().numpy().view(np.uint32)
+        sts = []
+        for i in range(8):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sstep()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            if i >= 2:
+                sts.append(e0.elapsed_time(e1))
+        s_ms = float(np.median(sts))
+        smul_line = {"ms_per_step": round(s_ms, 5), "gbit_s": round(2 * N * batch / (s_ms * 1e-3) / 1e9, 4),
+                     "dmul_over_smul": round(ms_per_step / s_ms, 3), "exact": u32_to_int(S0) == pairs[0][0] * pairs[0][1],
+                     "plan": {"m": splan.m, "K": splan.K, "s": splan.s}}
+    except Exception as e:  # the headline does not depend on it; say why it is missing
+        smul_line = {"unavailable": repr(e)[:200]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(N, pairs[:4], args.cpu_budget)
@@ -474,6 +506,7 @@ def main():
                     "api": "paper_1503_04955_b200.dmul(int, int) -> Natural" if batch == 1 else
                            "paper_1503_04955_b200.dmul_many([(int, int)] * batch) -> [Natural]"},
             "clocks": clocks.summary(),
+            "smul": smul_line,
         }
         if cpu:
             line["cpu_baseline"] = {k: v for k, v in cpu.items() if k != "ms_per_mul"}

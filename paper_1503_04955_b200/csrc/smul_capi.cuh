@@ -10,7 +10,7 @@ struct smul_plan {
   long long N = 0, s = 0, n = 0;
   int m = 0, K = 0, KW = 0, Q = 1, omega_exp = 0;
   long long prod_limbs = 0;
-  std::vector<std::pair<int, int>> passes;  // (lv0, nlv) per FFT pass
+  int nlv_max = 1;  // most DIT levels one FFT pass runs in shared memory
   size_t smem_fft = 0, smem_pw = 0;
   cudaStream_t stream = nullptr;
   int cap = 0;  // operands the workspace holds (a's and b's)
@@ -30,7 +30,8 @@ int smul_set_attrs(smul_plan* P) {
   CUCHK(cudaFuncSetAttribute(k_smul_fft<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmulFftSmemMax));
   // the attribute is per kernel, not per plan: allow the largest plan this Q serves
   const int pw_max = kSmulPwWarps * 10 * 32 * Q * 4;
-  CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, pw_max));
+  CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, pw_max));
+  CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 10 * 32 * Q * 4));
   return 0;
 }
 
@@ -55,13 +56,20 @@ void smul_fft_q(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool invers
   A.KW = P->KW;
   A.K = P->K;
   A.omega_exp = inverse ? (2 * P->K - P->omega_exp) % (2 * P->K) : P->omega_exp;
-  for (size_t i = 0; i < P->passes.size(); ++i) {
-    A.lv0 = P->passes[i].first;
-    A.nlv = P->passes[i].second;
-    A.post_e = (normalise && i + 1 == P->passes.size()) ? (2 * P->K - P->m) % (2 * P->K) : -1;
+  // levels per pass: at most what shared memory and one warp per butterfly (<= 32 warps)
+  // allow, fewer while the launch would not cover the SMs; then split the levels evenly
+  int nlv = P->nlv_max;
+  while (nlv > 3 && (P->n >> nlv) * npoly < 148) --nlv;
+  const int npass = (P->m + nlv - 1) / nlv;
+  for (int i = 0, lv = 0; i < npass; ++i) {
+    const int nl = (P->m - lv + (npass - i) - 1) / (npass - i);
+    A.lv0 = lv;
+    A.nlv = nl;
+    lv += nl;
+    A.post_e = (normalise && i + 1 == npass) ? (2 * P->K - P->m) % (2 * P->K) : -1;
     const int G = 1 << A.nlv;
     const size_t smem = (size_t)G * P->KW * 4 + (size_t)G * 4;
-    const int nt = std::min(kSmulThreads, std::max(32, G / 2 * 32));
+    const int nt = std::max(32, G / 2 * 32);
     launch_k(k_smul_fft<Q>, dim3((unsigned)(P->n >> A.nlv), npoly), dim3(nt), smem, s, A);
   }
 }
@@ -77,10 +85,16 @@ void smul_fft(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool inverse,
   }
 }
 
+// small K: a warp per product (4 per CTA); K >= 4096: a CTA of 8 warps per product
 template <int Q>
 void smul_pw_q(smul_plan* P, const SmulPwArgs& A, cudaStream_t s) {
+  if (Q >= 4) {
+    launch_k(k_smul_pointwise<Q, 8>, dim3((unsigned)std::min<long long>(A.count, 148LL * 8)), dim3(256),
+             (size_t)10 * P->KW * 4, s, A);
+    return;
+  }
   const long long blocks = (A.count + kSmulPwWarps - 1) / kSmulPwWarps;
-  launch_k(k_smul_pointwise<Q>, dim3((unsigned)std::min<long long>(blocks, 148LL * 16)), dim3(32 * kSmulPwWarps),
+  launch_k(k_smul_pointwise<Q, 1>, dim3((unsigned)std::min<long long>(blocks, 148LL * 16)), dim3(32 * kSmulPwWarps),
            P->smem_pw, s, A);
 }
 
@@ -214,15 +228,10 @@ int smul_plan_create(const smul_plan_desc* d, int device, smul_plan** out) {
   int q = (P->KW + 31) / 32, Q = 1;
   while (Q < q) Q <<= 1;
   P->Q = Q;
-  // FFT passes: as many levels per CTA as kSmulFftSmemMax holds, split evenly
+  // FFT passes: up to 64 elements (32 butterfly warps) per CTA, as shared memory allows
   int nlv_max = 1;
-  while (nlv_max < 12 && ((size_t)P->KW * 4 + 4) << (nlv_max + 1) <= kSmulFftSmemMax) ++nlv_max;
-  const int npass = (P->m + nlv_max - 1) / nlv_max;
-  for (int i = 0, lv = 0; i < npass; ++i) {
-    const int nl = (P->m - lv + (npass - i) - 1) / (npass - i);
-    P->passes.emplace_back(lv, nl);
-    lv += nl;
-  }
+  while (nlv_max < 6 && nlv_max < d->m && ((size_t)P->KW * 4 + 4) << (nlv_max + 1) <= kSmulFftSmemMax) ++nlv_max;
+  P->nlv_max = std::min(nlv_max, d->m);
   P->smem_pw = (size_t)kSmulPwWarps * 10 * P->KW * 4;
   int rc;
   cudaError_t e = cudaSetDevice(device);

@@ -209,7 +209,7 @@ __global__ void k_smul_encode(SmulEncodeArgs A) {
 // nlv radix-2 DIT levels of bigmul/fft.py:82-104 on the 2^nlv elements
 // hi | (j << lv0) | lo of one transform, held in shared memory; a warp per butterfly
 template <int Q>
-__global__ void __launch_bounds__(kSmulThreads) k_smul_fft(SmulFftArgs A) {
+__global__ void __launch_bounds__(1024) k_smul_fft(SmulFftArgs A) {
   griddep_wait();
   griddep_launch();
   extern __shared__ uint32_t smem[];
@@ -222,13 +222,13 @@ __global__ void __launch_bounds__(kSmulThreads) k_smul_fft(SmulFftArgs A) {
   const long long g = blockIdx.x;
   const long long lo = g & ((1LL << A.lv0) - 1), hi = (g >> A.lv0) << (A.lv0 + A.nlv);
   auto gidx = [&](int j) { return hi | ((long long)j << A.lv0) | lo; };
-  for (int t = threadIdx.x; t < G * KW; t += blockDim.x) {
-    const int j = t / KW, i = t - j * KW;
-    sx[t] = X[gidx(j) * KW + i];
-  }
-  for (int j = threadIdx.x; j < G; j += blockDim.x) stop[j] = T[gidx(j)];
-  __syncthreads();
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < G; j += nw) {  // a warp per element: contiguous KW-limb rows
+    const uint32_t* src = X + gidx(j) * KW;
+    for (int i = lane; i < KW; i += 32) sx[j * KW + i] = src[i];
+    if (lane == 0) stop[j] = T[gidx(j)];
+  }
+  __syncthreads();
   const long long twoK = 2LL * K;
   for (int l = A.lv0; l < A.lv0 + A.nlv; ++l) {
     const int lb = l - A.lv0;
@@ -269,125 +269,148 @@ __global__ void __launch_bounds__(kSmulThreads) k_smul_fft(SmulFftArgs A) {
     }
     __syncthreads();
   }
-  for (int t = threadIdx.x; t < G * KW; t += blockDim.x) {
-    const int j = t / KW, i = t - j * KW;
-    X[gidx(j) * KW + i] = sx[t];
+  for (int j = warp; j < G; j += nw) {
+    uint32_t* dst = X + gidx(j) * KW;
+    for (int i = lane; i < KW; i += 32) dst[i] = sx[j * KW + i];
+    if (lane == 0) T[gidx(j)] = stop[j];
   }
-  for (int j = threadIdx.x; j < G; j += blockDim.x) T[gidx(j)] = stop[j];
 }
 
 // pointwise products in Z/(2^K+1) (bigmul/smul.py:206-216 at the outermost level; the
 // product is the same residue whichever multiplier computes it): schoolbook column sums,
 // carry resolution, fold hi*2^K == -hi.  One warp per product; smem per warp:
 // x, y (2*KW limbs), column sums (2*KW x 96 bit), product limbs (2*KW).
-template <int Q>
-__global__ void __launch_bounds__(128) k_smul_pointwise(SmulPwArgs A) {
+template <int WPP>
+__device__ __forceinline__ void group_sync() {
+  if (WPP == 1)
+    __syncwarp();
+  else
+    __syncthreads();  // WPP > 1: the group is the whole CTA
+}
+
+template <int Q, int WPP>
+__global__ void __launch_bounds__(WPP == 1 ? 128 : 32 * WPP) k_smul_pointwise(SmulPwArgs A) {
   griddep_wait();
   griddep_launch();
   extern __shared__ uint32_t smem[];
   const int KW = A.KW, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = warp / WPP, gw = warp % WPP, ngrp = (blockDim.x >> 5) / WPP, gt = gw * 32 + lane;
   const int per = 2 * KW + 2 * KW * 3 + 2 * KW;
-  uint32_t* sa = smem + (long long)warp * per;
+  uint32_t* sa = smem + (long long)grp * per;
   uint32_t* sb = sa + KW;
   uint32_t* scol = sb + KW;        // [2KW][3]: low, mid, high words of the column sum
   uint32_t* sp = scol + 6 * KW;    // product limbs
   const long long n = 1LL << A.log_n;
-  for (long long pk = (long long)blockIdx.x * (blockDim.x >> 5) + warp; pk < A.count;
-       pk += (long long)gridDim.x * (blockDim.x >> 5)) {
+  for (long long pk = (long long)blockIdx.x * ngrp + grp; pk < A.count; pk += (long long)gridDim.x * ngrp) {
     const long long bidx = pk >> A.log_n, k = pk & (n - 1);
     const uint32_t* xa = A.x + pk * KW;
     const uint32_t* yb = A.y + pk * KW;
     const int at = (int)A.xtop[pk], bt = (int)A.ytop[pk];
     const long long opos = bidx * n + (__brev((unsigned)k) >> (32 - A.log_n));
-    uint32_t r[Q];
-    int rt;
-    if (at | bt) {  // 2^K == -1
-      uint32_t z[Q], v[Q];
-      const int base = lane * Q;
-#pragma unroll
-      for (int j = 0; j < Q; ++j) {
-        z[j] = 0;
-        v[j] = base + j < KW ? (at ? yb[base + j] : xa[base + j]) : 0u;
-      }
-      if (at && bt) {
-#pragma unroll
-        for (int j = 0; j < Q; ++j) r[j] = (base + j == 0) ? 1u : 0u;
-        rt = 0;
-      } else {
-        rt = w_submod<Q>(r, z, 0, v, at ? bt : at, KW);
-      }
-    } else {
-      for (int i = lane; i < KW; i += 32) {
+    if (!(at | bt)) {
+      for (int i = gt; i < KW; i += 32 * WPP) {
         sa[i] = xa[i];
         sb[i] = yb[i];
       }
-      __syncwarp();
-      for (int c = lane; c < 2 * KW; c += 32) {
-        unsigned long long acc = 0;
-        uint32_t h = 0;
+      group_sync<WPP>();
+      for (int c = gt; c < 2 * KW; c += 32 * WPP) {
+        unsigned long long acc = 0, acc2 = 0;
+        uint32_t h = 0, h2 = 0;
         const int i0 = c - KW + 1 > 0 ? c - KW + 1 : 0, i1 = c < KW - 1 ? c : KW - 1;
-        for (int i = i0; i <= i1; ++i) {
+        int i = i0;
+        for (; i + 1 <= i1; i += 2) {  // two independent chains
+          const unsigned long long p = (unsigned long long)sa[i] * sb[c - i];
+          const unsigned long long p2 = (unsigned long long)sa[i + 1] * sb[c - i - 1];
+          acc += p;
+          h += acc < p;
+          acc2 += p2;
+          h2 += acc2 < p2;
+        }
+        if (i <= i1) {
           const unsigned long long p = (unsigned long long)sa[i] * sb[c - i];
           acc += p;
           h += acc < p;
         }
+        acc += acc2;
+        h += h2 + (acc < acc2);
         scol[3 * c] = (uint32_t)acc;
         scol[3 * c + 1] = (uint32_t)(acc >> 32);
         scol[3 * c + 2] = h;
       }
-      __syncwarp();
-      // limb c = low(C_c) + mid(C_(c-1)) + high(C_(c-2)) + carries; lane owns 2Q limbs
-      const int b2 = lane * 2 * Q;
-      uint32_t w[2 * Q];
-      uint32_t c = 0;
-#pragma unroll
-      for (int j = 0; j < 2 * Q; ++j) {
-        const int i = b2 + j;
-        unsigned long long v = c;
-        if (i < 2 * KW) {
-          v += scol[3 * i];
-          if (i >= 1) v += scol[3 * (i - 1) + 1];
-          if (i >= 2) v += scol[3 * (i - 2) + 2];
-        }
-        w[j] = (uint32_t)v;
-        c = (uint32_t)(v >> 32);
-      }
-      // the lane's small carry-out goes to the next lane's first limb
-      uint32_t cin = __shfl_up_sync(0xFFFFFFFFu, c, 1);
-      if (lane == 0) cin = 0;
-      uint32_t g = 0;
-      bool ones = true;
-#pragma unroll
-      for (int j = 0; j < 2 * Q; ++j) {
-        const unsigned long long v = (unsigned long long)w[j] + cin;
-        w[j] = (uint32_t)v;
-        cin = (uint32_t)(v >> 32);
-        ones &= w[j] == 0xFFFFFFFFu;
-      }
-      g = cin;
-      const unsigned GG = __ballot_sync(0xFFFFFFFFu, g != 0), PP = __ballot_sync(0xFFFFFFFFu, ones && !g);
-      const unsigned long long a2 = (unsigned long long)(GG | PP), bb = GG;
-      uint32_t ci = (uint32_t)((((a2 + bb) ^ a2 ^ bb)) >> lane) & 1u;
-#pragma unroll
-      for (int j = 0; j < 2 * Q; ++j) {
-        const uint32_t t = w[j] + ci;
-        ci = ci && t == 0u;
-        w[j] = t;
-        if (b2 + j < 2 * KW) sp[b2 + j] = w[j];
-      }
-      __syncwarp();
-      uint32_t plo[Q], phi[Q];
-      const int base = lane * Q;
-#pragma unroll
-      for (int j = 0; j < Q; ++j) {
-        plo[j] = base + j < KW ? sp[base + j] : 0u;
-        phi[j] = base + j < KW ? sp[KW + base + j] : 0u;
-      }
-      rt = w_submod<Q>(r, plo, 0, phi, 0, KW);
-      __syncwarp();
+      group_sync<WPP>();
     }
-    w_store<Q>(A.out + opos * KW, r, KW);
-    if (lane == 0) A.otop[opos] = (uint32_t)rt;
+    if (gw == 0) {
+      uint32_t r[Q];
+      int rt;
+      if (at | bt) {  // 2^K == -1
+        uint32_t z[Q], v[Q];
+        const int base = lane * Q;
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+          z[j] = 0;
+          v[j] = base + j < KW ? (at ? yb[base + j] : xa[base + j]) : 0u;
+        }
+        if (at && bt) {
+#pragma unroll
+          for (int j = 0; j < Q; ++j) r[j] = (base + j == 0) ? 1u : 0u;
+          rt = 0;
+        } else {
+          rt = w_submod<Q>(r, z, 0, v, at ? bt : at, KW);
+        }
+      } else {
+        // limb c = low(C_c) + mid(C_(c-1)) + high(C_(c-2)) + carries; lane owns 2Q limbs
+        const int b2 = lane * 2 * Q;
+        uint32_t w[2 * Q];
+        uint32_t c = 0;
+#pragma unroll
+        for (int j = 0; j < 2 * Q; ++j) {
+          const int i = b2 + j;
+          unsigned long long v = c;
+          if (i < 2 * KW) {
+            v += scol[3 * i];
+            if (i >= 1) v += scol[3 * (i - 1) + 1];
+            if (i >= 2) v += scol[3 * (i - 2) + 2];
+          }
+          w[j] = (uint32_t)v;
+          c = (uint32_t)(v >> 32);
+        }
+        // the lane's small carry-out goes to the next lane's first limb
+        uint32_t cin = __shfl_up_sync(0xFFFFFFFFu, c, 1);
+        if (lane == 0) cin = 0;
+        uint32_t g = 0;
+        bool ones = true;
+#pragma unroll
+        for (int j = 0; j < 2 * Q; ++j) {
+          const unsigned long long v = (unsigned long long)w[j] + cin;
+          w[j] = (uint32_t)v;
+          cin = (uint32_t)(v >> 32);
+          ones &= w[j] == 0xFFFFFFFFu;
+        }
+        g = cin;
+        const unsigned GG = __ballot_sync(0xFFFFFFFFu, g != 0), PP = __ballot_sync(0xFFFFFFFFu, ones && !g);
+        const unsigned long long a2 = (unsigned long long)(GG | PP), bb = GG;
+        uint32_t ci = (uint32_t)((((a2 + bb) ^ a2 ^ bb)) >> lane) & 1u;
+#pragma unroll
+        for (int j = 0; j < 2 * Q; ++j) {
+          const uint32_t t = w[j] + ci;
+          ci = ci && t == 0u;
+          w[j] = t;
+          if (b2 + j < 2 * KW) sp[b2 + j] = w[j];
+        }
+        __syncwarp();
+        uint32_t plo[Q], phi[Q];
+        const int base = lane * Q;
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+          plo[j] = base + j < KW ? sp[base + j] : 0u;
+          phi[j] = base + j < KW ? sp[KW + base + j] : 0u;
+        }
+        rt = w_submod<Q>(r, plo, 0, phi, 0, KW);
+      }
+      w_store<Q>(A.out + opos * KW, r, KW);
+      if (lane == 0) A.otop[opos] = (uint32_t)rt;
+    }
+    group_sync<WPP>();  // the group's shared memory is reused by the next product
   }
 }
 

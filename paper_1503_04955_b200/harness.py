@@ -3,9 +3,10 @@
 Restates the reference harness (bigmul/bench.py:16-108): ``run_bench`` times every
 (algorithm, size) pair ``reps`` times, checks every timed product bit-exactly before it is
 reported, and keeps the median; ``write_csv`` / ``quotient_column`` produce the CSV and the
-T_num/T_den column of the thesis's run-time table.  Only the ``"dmul"`` rung exists in this
-build, so the default check is Python's own int product (``reference=None``); naming another
-rung raises NotImplementedError through ALGORITHMS, as ``mul`` does.
+T_num/T_den column of the thesis's run-time table.  The ``"dmul"`` and ``"smul"`` rungs run
+on the GPU, so ``quotient_column(records)`` is the thesis's T_DMUL / T_SMUL; the default
+check is Python's own int product (``reference=None``); naming another rung raises
+NotImplementedError through ALGORITHMS, as ``mul`` does.
 """
 
 from __future__ import annotations

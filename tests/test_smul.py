@@ -174,3 +174,18 @@ def test_smul_range_errors(cuda_ok):
         dp.mul_limbs(a, a, 200)  # 6000-bit product does not fit N = 4096
     with pytest.raises(ValueError):
         SmulDevicePlan(4096, 3, 512, 1080, 270)  # K not a multiple of 32
+
+
+@pytest.mark.gpu
+def test_harness_quotient_dmul_over_smul(cuda_ok):
+    import io
+
+    from paper_1503_04955_b200.harness import quotient_column, run_bench, write_csv
+
+    recs = run_bench(["dmul", "smul"], [64, 1024], reps=3, seed=5)
+    assert {(r.algorithm, r.input_words) for r in recs} == {(a, s) for a in ("dmul", "smul") for s in (64, 1024)}
+    q = quotient_column(recs)  # T_DMUL / T_SMUL (bigmul/bench.py:80-91)
+    assert [s for s, _ in q] == [64, 1024] and all(v > 0 for _, v in q)
+    buf = io.StringIO()
+    write_csv(recs, buf)
+    assert buf.getvalue().count("smul,") == 2
