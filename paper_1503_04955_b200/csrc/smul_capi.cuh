@@ -39,6 +39,8 @@ int smul_attrs(smul_plan* P) {
   switch (P->Q) {
     case 1: return smul_set_attrs<1>(P);
     case 2: return smul_set_attrs<2>(P);
+    case 3: return smul_set_attrs<3>(P);
+    case 6: return smul_set_attrs<6>(P);
     case 4: return smul_set_attrs<4>(P);
     case 8: return smul_set_attrs<8>(P);
     case 16: return smul_set_attrs<16>(P);
@@ -55,7 +57,8 @@ void smul_fft_q(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool invers
   A.log_n = P->m;
   A.KW = P->KW;
   A.K = P->K;
-  A.omega_exp = inverse ? (2 * P->K - P->omega_exp) % (2 * P->K) : P->omega_exp;
+  A.omega_fwd = P->omega_exp;
+  A.inverse = inverse ? 1 : 0;
   // levels per pass: at most what shared memory and one warp per butterfly (<= 32 warps)
   // allow, fewer while the launch would not cover the SMs; then split the levels evenly
   int nlv = P->nlv_max;
@@ -78,6 +81,8 @@ void smul_fft(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool inverse,
   switch (P->Q) {
     case 1: return smul_fft_q<1>(P, x, top, npoly, inverse, normalise, s);
     case 2: return smul_fft_q<2>(P, x, top, npoly, inverse, normalise, s);
+    case 3: return smul_fft_q<3>(P, x, top, npoly, inverse, normalise, s);
+    case 6: return smul_fft_q<6>(P, x, top, npoly, inverse, normalise, s);
     case 4: return smul_fft_q<4>(P, x, top, npoly, inverse, normalise, s);
     case 8: return smul_fft_q<8>(P, x, top, npoly, inverse, normalise, s);
     case 16: return smul_fft_q<16>(P, x, top, npoly, inverse, normalise, s);
@@ -85,10 +90,10 @@ void smul_fft(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool inverse,
   }
 }
 
-// small K: a warp per product (4 per CTA); K >= 4096: a CTA of 8 warps per product
+// small K: a warp per product (4 per CTA); K >= 2080 (3+ limbs per lane): a CTA of 8 warps per product
 template <int Q>
 void smul_pw_q(smul_plan* P, const SmulPwArgs& A, cudaStream_t s) {
-  if (Q >= 4) {
+  if (Q >= 3) {
     launch_k(k_smul_pointwise<Q, 8>, dim3((unsigned)std::min<long long>(A.count, 148LL * 8)), dim3(256),
              (size_t)10 * P->KW * 4, s, A);
     return;
@@ -102,6 +107,8 @@ void smul_pointwise(smul_plan* P, const SmulPwArgs& A, cudaStream_t s) {
   switch (P->Q) {
     case 1: return smul_pw_q<1>(P, A, s);
     case 2: return smul_pw_q<2>(P, A, s);
+    case 3: return smul_pw_q<3>(P, A, s);
+    case 6: return smul_pw_q<6>(P, A, s);
     case 4: return smul_pw_q<4>(P, A, s);
     case 8: return smul_pw_q<8>(P, A, s);
     case 16: return smul_pw_q<16>(P, A, s);
@@ -226,7 +233,12 @@ int smul_plan_create(const smul_plan_desc* d, int device, smul_plan** out) {
   P->omega_exp = d->omega_exp;
   P->prod_limbs = (d->N + 31) / 32;
   int q = (P->KW + 31) / 32, Q = 1;
-  while (Q < q) Q <<= 1;
+  static const int kQs[] = {1, 2, 3, 4, 6, 8, 16, 32};  // limbs per lane the kernels are built for
+  for (int qq : kQs)
+    if (qq >= q) {
+      Q = qq;
+      break;
+    }
   P->Q = Q;
   // FFT passes: up to 64 elements (32 butterfly warps) per CTA, as shared memory allows
   int nlv_max = 1;

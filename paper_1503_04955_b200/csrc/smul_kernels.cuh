@@ -27,7 +27,8 @@ struct SmulFftArgs {
   uint32_t* x;    // [npoly][n][KW]
   uint32_t* top;  // [npoly][n]
   int log_n, KW, K;
-  int omega_exp;  // root 2^omega_exp of order n (forward or inverse direction)
+  int omega_fwd;  // forward root 2^omega_fwd of order n (= 2K/n on the outermost level)
+  int inverse;    // 1: transform with the inverse root 2^(2K - omega_fwd)
   int lv0, nlv;   // DIT levels [lv0, lv0 + nlv): merges of length 2^(l+1)
   int post_e;     // >= 0: multiply every element by 2^post_e after the last level
 };
@@ -103,7 +104,8 @@ __device__ __forceinline__ int w_addmod(uint32_t (&r)[Q], const uint32_t (&u)[Q]
                                         int KW) {
   const uint32_t c = w_add<Q>(r, u, t, 0u, false, KW);
   int T = ut + tt + (int)c;
-  if (T >= 2 || (T == 1 && w_nonzero<Q>(r))) {  // value >= 2^K + 1: subtract it
+  const bool nz = w_nonzero<Q>(r);
+  if (T >= 2 || (T == 1 && nz)) {  // value >= 2^K + 1: subtract it
     uint32_t z[Q];
 #pragma unroll
     for (int j = 0; j < Q; ++j) z[j] = 0;
@@ -229,14 +231,17 @@ __global__ void __launch_bounds__(1024) k_smul_fft(SmulFftArgs A) {
     if (lane == 0) stop[j] = T[gidx(j)];
   }
   __syncthreads();
-  const long long twoK = 2LL * K;
   for (int l = A.lv0; l < A.lv0 + A.nlv; ++l) {
     const int lb = l - A.lv0;
     const long long half = 1LL << l;
     for (int pr = warp; pr < G / 2; pr += nw) {
       const int ja = ((pr >> lb) << (lb + 1)) | (pr & ((1 << lb) - 1)), jb = ja | (1 << lb);
-      const long long k = gidx(ja) & (half - 1);
-      const int e = (int)(((k << (A.log_n - l - 1)) * (long long)A.omega_exp) % twoK);
+      // root power k * n/len; omega^(n/2) = -1 = 2^K, so the exponent k * (n/len) * omega_exp
+      // stays below K for the forward root 2^(2K/n); the inverse root 2^(2K - 2K/n) gives
+      // 2K minus that (bigmul/fermat.py:91-93) -- 32-bit arithmetic, no modulo
+      const int k = (int)(gidx(ja) & (half - 1));
+      const int ef = (k << (A.log_n - l - 1)) * A.omega_fwd;
+      const int e = A.inverse && ef ? 2 * K - ef : ef;
       uint32_t* pa = sx + (long long)ja * KW;
       uint32_t* pb = sx + (long long)jb * KW;
       uint32_t t[Q], u[Q], s[Q], d[Q];

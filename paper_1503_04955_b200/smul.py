@@ -140,11 +140,11 @@ _MAX = 32
 
 
 def _device_cost(p: SmulPlan) -> float:
-    """Device cost of a candidate: transform limb work (a lane holds a power of two of limbs,
-    ~8 instructions per limb per butterfly), the schoolbook pointwise products, and a
-    penalty when the n products cannot fill the 148 SMs."""
+    """Device cost of a candidate: transform limb work (a lane holds 1, 2, 3, 4, 6, 8, 16 or
+    32 limbs, ~8 instructions per limb per butterfly), the schoolbook pointwise products, and
+    a penalty when the n products cannot fill the 148 SMs."""
     kw = p.K // 32
-    q = 1 << max(0, (-(-kw // 32) - 1).bit_length())
+    q = next(x for x in (1, 2, 3, 4, 6, 8, 16, 32, 64) if 32 * x >= kw)  # limbs per lane, csrc/smul_capi.cuh
     work = 1.5 * p.n * p.m * 32 * q * 8 + p.n * kw * kw
     return work / min(1.0, p.n / 2048)
 
