@@ -29,9 +29,9 @@ template <int Q>
 int smul_set_attrs(smul_plan* P) {
   CUCHK(cudaFuncSetAttribute(k_smul_fft<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmulFftSmemMax));
   // the attribute is per kernel, not per plan: allow the largest plan this Q serves
-  const int pw_max = kSmulPwWarps * 10 * 32 * Q * 4;
+  const int pw_max = kSmulPwWarps * (10 * 32 * Q + 8) * 4;
   CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, pw_max));
-  CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 10 * 32 * Q * 4));
+  CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (10 * 32 * Q + 8) * 4));
   return 0;
 }
 
@@ -95,7 +95,7 @@ template <int Q>
 void smul_pw_q(smul_plan* P, const SmulPwArgs& A, cudaStream_t s) {
   if (Q >= 3) {
     launch_k(k_smul_pointwise<Q, 8>, dim3((unsigned)std::min<long long>(A.count, 148LL * 8)), dim3(256),
-             (size_t)10 * P->KW * 4, s, A);
+             (size_t)(10 * P->KW + 8) * 4, s, A);
     return;
   }
   const long long blocks = (A.count + kSmulPwWarps - 1) / kSmulPwWarps;
@@ -244,7 +244,7 @@ int smul_plan_create(const smul_plan_desc* d, int device, smul_plan** out) {
   int nlv_max = 1;
   while (nlv_max < 6 && nlv_max < d->m && ((size_t)P->KW * 4 + 4) << (nlv_max + 1) <= kSmulFftSmemMax) ++nlv_max;
   P->nlv_max = std::min(nlv_max, d->m);
-  P->smem_pw = (size_t)kSmulPwWarps * 10 * P->KW * 4;
+  P->smem_pw = (size_t)kSmulPwWarps * (10 * P->KW + 8) * 4;
   int rc;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking);

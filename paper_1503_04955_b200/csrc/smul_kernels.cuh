@@ -300,10 +300,10 @@ __global__ void __launch_bounds__(WPP == 1 ? 128 : 32 * WPP) k_smul_pointwise(Sm
   extern __shared__ uint32_t smem[];
   const int KW = A.KW, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = warp / WPP, gw = warp % WPP, ngrp = (blockDim.x >> 5) / WPP, gt = gw * 32 + lane;
-  const int per = 2 * KW + 2 * KW * 3 + 2 * KW;
+  const int per = 10 * KW + 8;
   uint32_t* sa = smem + (long long)grp * per;
-  uint32_t* sb = sa + KW;
-  uint32_t* scol = sb + KW;        // [2KW][3]: low, mid, high words of the column sum
+  uint32_t* sb = sa + KW + 2;      // b with two zero limbs on either side
+  uint32_t* scol = sb + KW + 2;    // [2KW][3]: low, mid, high words of the column sum
   uint32_t* sp = scol + 6 * KW;    // product limbs
   const long long n = 1LL << A.log_n;
   for (long long pk = (long long)blockIdx.x * ngrp + grp; pk < A.count; pk += (long long)gridDim.x * ngrp) {
@@ -317,30 +317,35 @@ __global__ void __launch_bounds__(WPP == 1 ? 128 : 32 * WPP) k_smul_pointwise(Sm
         sa[i] = xa[i];
         sb[i] = yb[i];
       }
+      if (gt < 2) {  // zero pads: the column windows run one limb off either end of b
+        sb[-1 - gt] = 0u;
+        sb[KW + gt] = 0u;
+      }
       group_sync<WPP>();
-      for (int c = gt; c < 2 * KW; c += 32 * WPP) {
-        unsigned long long acc = 0, acc2 = 0;
-        uint32_t h = 0, h2 = 0;
-        const int i0 = c - KW + 1 > 0 ? c - KW + 1 : 0, i1 = c < KW - 1 ? c : KW - 1;
-        int i = i0;
-        for (; i + 1 <= i1; i += 2) {  // two independent chains
-          const unsigned long long p = (unsigned long long)sa[i] * sb[c - i];
-          const unsigned long long p2 = (unsigned long long)sa[i + 1] * sb[c - i - 1];
-          acc += p;
-          h += acc < p;
-          acc2 += p2;
-          h2 += acc2 < p2;
+      // two adjacent columns per thread: a[i] is loaded once for both, the b window slides by
+      // one limb per step (one shared load per limb product); each column's 96-bit sum is a
+      // mad.lo.cc / madc.hi.cc / addc chain, three instructions per limb product
+      for (int c0 = 2 * gt; c0 < 2 * KW - 1; c0 += 2 * 32 * WPP) {
+        uint32_t x0 = 0, x1 = 0, x2 = 0, y0 = 0, y1 = 0, y2 = 0;
+        const int i0 = c0 - KW + 1 > 0 ? c0 - KW + 1 : 0, i1 = c0 + 1 < KW - 1 ? c0 + 1 : KW - 1;
+        uint32_t bl = sb[c0 - i0], bh = sb[c0 + 1 - i0];  // b[c0 - i], b[c0 + 1 - i]
+        for (int i = i0; i <= i1; ++i) {
+          const uint32_t ai = sa[i];
+          asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\tmadc.hi.cc.u32 %1, %3, %4, %1;\n\taddc.u32 %2, %2, 0;"
+              : "+r"(x0), "+r"(x1), "+r"(x2) : "r"(ai), "r"(bl));
+          asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\tmadc.hi.cc.u32 %1, %3, %4, %1;\n\taddc.u32 %2, %2, 0;"
+              : "+r"(y0), "+r"(y1), "+r"(y2) : "r"(ai), "r"(bh));
+          bh = bl;
+          bl = sb[c0 - i - 1];
         }
-        if (i <= i1) {
-          const unsigned long long p = (unsigned long long)sa[i] * sb[c - i];
-          acc += p;
-          h += acc < p;
+        scol[3 * c0] = x0;
+        scol[3 * c0 + 1] = x1;
+        scol[3 * c0 + 2] = x2;
+        if (c0 + 1 < 2 * KW) {
+          scol[3 * c0 + 3] = y0;
+          scol[3 * c0 + 4] = y1;
+          scol[3 * c0 + 5] = y2;
         }
-        acc += acc2;
-        h += h2 + (acc < acc2);
-        scol[3 * c] = (uint32_t)acc;
-        scol[3 * c + 1] = (uint32_t)(acc >> 32);
-        scol[3 * c + 2] = h;
       }
       group_sync<WPP>();
     }
