@@ -71,7 +71,7 @@ void smul_fft_q(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool invers
     lv += nl;
     A.post_e = (normalise && i + 1 == npass) ? (2 * P->K - P->m) % (2 * P->K) : -1;
     const int G = 1 << A.nlv;
-    const size_t smem = (size_t)G * P->KW * 4 + (size_t)G * 4;
+    const size_t smem = (size_t)G * smul_elem_stride(P->KW, smul_pad<Q>()) * 4 + (size_t)G * 4;
     const int nt = std::max(32, G / 2 * 32);
     launch_k(k_smul_fft<Q>, dim3((unsigned)(P->n >> A.nlv), npoly), dim3(nt), smem, s, A);
   }
@@ -242,7 +242,8 @@ int smul_plan_create(const smul_plan_desc* d, int device, smul_plan** out) {
   P->Q = Q;
   // FFT passes: up to 64 elements (32 butterfly warps) per CTA, as shared memory allows
   int nlv_max = 1;
-  while (nlv_max < 6 && nlv_max < d->m && ((size_t)P->KW * 4 + 4) << (nlv_max + 1) <= kSmulFftSmemMax) ++nlv_max;
+  const size_t es = (size_t)P->KW + (P->KW + 31) / 32 + 1;  // padded element + its top word, upper bound
+  while (nlv_max < 6 && nlv_max < d->m && (es * 4) << (nlv_max + 1) <= kSmulFftSmemMax) ++nlv_max;
   P->nlv_max = std::min(nlv_max, d->m);
   P->smem_pw = (size_t)kSmulPwWarps * (10 * P->KW + 8) * 4;
   int rc;

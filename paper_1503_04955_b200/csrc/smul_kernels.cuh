@@ -55,6 +55,15 @@ struct SmulEncodeArgs {
 
 // ---- warp-distributed multi-limb arithmetic ---------------------------------------------
 
+// Shared-memory element layout: lane l touches limbs l*Q + j, a stride-Q pattern that is a
+// Q-way bank conflict for Q a power of two; those layouts insert one pad word after every
+// 32 limbs (limb i at i + i/32), which spreads the 32 lanes over 32 banks.
+template <int Q>
+__host__ __device__ constexpr bool smul_pad() { return Q >= 2 && (Q & (Q - 1)) == 0; }
+template <int Q>
+__device__ __forceinline__ int spos(int i) { return smul_pad<Q>() ? i + (i >> 5) : i; }
+__host__ __device__ inline int smul_elem_stride(int KW, bool pad) { return KW + (pad ? (KW + 31) / 32 : 0); }
+
 // r = x + (sub ? ~y : y) + cin over KW limbs; returns the carry out of limb KW-1
 template <int Q>
 __device__ __forceinline__ uint32_t w_add(uint32_t (&r)[Q], const uint32_t (&x)[Q], const uint32_t (&y)[Q], uint32_t cin,
@@ -144,7 +153,7 @@ __device__ __forceinline__ int w_mulpow2(uint32_t (&r)[Q], const uint32_t* sx, i
   }
   if (e == 0 && !neg) {
 #pragma unroll
-    for (int j = 0; j < Q; ++j) r[j] = base + j < KW ? sx[base + j] : 0u;
+    for (int j = 0; j < Q; ++j) r[j] = base + j < KW ? sx[spos<Q>(base + j)] : 0u;
     return xtop;
   }
   const int ew = e >> 5, eb = e & 31;
@@ -159,22 +168,23 @@ __device__ __forceinline__ int w_mulpow2(uint32_t (&r)[Q], const uint32_t* sx, i
       continue;
     }
     const int s1 = i - ew;  // limb i of (x << e) mod 2^K
-    const uint32_t a1 = s1 >= 0 ? sx[s1] : 0u, a0 = s1 >= 1 ? sx[s1 - 1] : 0u;
+    const uint32_t a1 = s1 >= 0 ? sx[spos<Q>(s1)] : 0u, a0 = s1 >= 1 ? sx[spos<Q>(s1 - 1)] : 0u;
     lo[j] = eb ? __funnelshift_l(a0, a1, eb) : a1;
     const int s2 = i + KW - ew;  // limb i of (x << e) >> K
-    const uint32_t b1 = s2 < KW ? sx[s2] : 0u, b0 = s2 - 1 < KW ? sx[s2 - 1] : 0u;
+    const uint32_t b1 = s2 < KW ? sx[spos<Q>(s2)] : 0u, b0 = s2 - 1 < KW ? sx[spos<Q>(s2 - 1)] : 0u;
     hi[j] = eb ? __funnelshift_l(b0, b1, eb) : b1;
   }
   // lo - hi (or hi - lo for e >= K: 2^K == -1 negates)
   return neg ? w_submod<Q>(r, hi, 0, lo, 0, KW) : w_submod<Q>(r, lo, 0, hi, 0, KW);
 }
 
-template <int Q>
+// SMEM: sx is an element in the padded shared-memory layout (else plain limbs in HBM)
+template <int Q, bool SMEM = false>
 __device__ __forceinline__ void w_store(uint32_t* sx, const uint32_t (&r)[Q], int KW) {
   const int base = (threadIdx.x & 31) * Q;
 #pragma unroll
   for (int j = 0; j < Q; ++j)
-    if (base + j < KW) sx[base + j] = r[j];
+    if (base + j < KW) sx[SMEM ? spos<Q>(base + j) : base + j] = r[j];
 }
 
 // ---- kernels ----------------------------------------------------------------------------
@@ -217,7 +227,8 @@ __global__ void __launch_bounds__(1024) k_smul_fft(SmulFftArgs A) {
   extern __shared__ uint32_t smem[];
   const int G = 1 << A.nlv, KW = A.KW, K = A.K;
   uint32_t* sx = smem;
-  uint32_t* stop = smem + (long long)G * KW;
+  const int ES = smul_elem_stride(KW, smul_pad<Q>());
+  uint32_t* stop = smem + (long long)G * ES;
   const long long n = 1LL << A.log_n;
   uint32_t* X = A.x + (long long)blockIdx.y * n * KW;
   uint32_t* T = A.top + (long long)blockIdx.y * n;
@@ -227,7 +238,7 @@ __global__ void __launch_bounds__(1024) k_smul_fft(SmulFftArgs A) {
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
   for (int j = warp; j < G; j += nw) {  // a warp per element: contiguous KW-limb rows
     const uint32_t* src = X + gidx(j) * KW;
-    for (int i = lane; i < KW; i += 32) sx[j * KW + i] = src[i];
+    for (int i = lane; i < KW; i += 32) sx[j * ES + spos<Q>(i)] = src[i];
     if (lane == 0) stop[j] = T[gidx(j)];
   }
   __syncthreads();
@@ -242,19 +253,19 @@ __global__ void __launch_bounds__(1024) k_smul_fft(SmulFftArgs A) {
       const int k = (int)(gidx(ja) & (half - 1));
       const int ef = (k << (A.log_n - l - 1)) * A.omega_fwd;
       const int e = A.inverse && ef ? 2 * K - ef : ef;
-      uint32_t* pa = sx + (long long)ja * KW;
-      uint32_t* pb = sx + (long long)jb * KW;
+      uint32_t* pa = sx + ja * ES;
+      uint32_t* pb = sx + jb * ES;
       uint32_t t[Q], u[Q], s[Q], d[Q];
       const int tt = w_mulpow2<Q>(t, pb, (int)stop[jb], e, KW);
       const int base = lane * Q;
 #pragma unroll
-      for (int q = 0; q < Q; ++q) u[q] = base + q < KW ? pa[base + q] : 0u;
+      for (int q = 0; q < Q; ++q) u[q] = base + q < KW ? pa[spos<Q>(base + q)] : 0u;
       const int ut = (int)stop[ja];
       const int st = w_addmod<Q>(s, u, ut, t, tt, KW);
       const int dt = w_submod<Q>(d, u, ut, t, tt, KW);
       __syncwarp();
-      w_store<Q>(pa, s, KW);
-      w_store<Q>(pb, d, KW);
+      w_store<Q, true>(pa, s, KW);
+      w_store<Q, true>(pb, d, KW);
       if (lane == 0) {
         stop[ja] = (uint32_t)st;
         stop[jb] = (uint32_t)dt;
@@ -266,9 +277,9 @@ __global__ void __launch_bounds__(1024) k_smul_fft(SmulFftArgs A) {
   if (A.post_e >= 0) {  // normalisation by 2^-m (bigmul/smul.py:268-270)
     for (int j = warp; j < G; j += nw) {
       uint32_t r[Q];
-      const int rt = w_mulpow2<Q>(r, sx + (long long)j * KW, (int)stop[j], A.post_e, KW);
+      const int rt = w_mulpow2<Q>(r, sx + j * ES, (int)stop[j], A.post_e, KW);
       __syncwarp();
-      w_store<Q>(sx + (long long)j * KW, r, KW);
+      w_store<Q, true>(sx + j * ES, r, KW);
       if (lane == 0) stop[j] = (uint32_t)rt;
       __syncwarp();
     }
@@ -276,7 +287,7 @@ __global__ void __launch_bounds__(1024) k_smul_fft(SmulFftArgs A) {
   }
   for (int j = warp; j < G; j += nw) {
     uint32_t* dst = X + gidx(j) * KW;
-    for (int i = lane; i < KW; i += 32) dst[i] = sx[j * KW + i];
+    for (int i = lane; i < KW; i += 32) dst[i] = sx[j * ES + spos<Q>(i)];
     if (lane == 0) T[gidx(j)] = stop[j];
   }
 }
