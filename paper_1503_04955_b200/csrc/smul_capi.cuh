@@ -27,7 +27,8 @@ constexpr size_t kSmulFftSmemMax = 96 * 1024;
 
 template <int Q>
 int smul_set_attrs(smul_plan* P) {
-  CUCHK(cudaFuncSetAttribute(k_smul_fft<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmulFftSmemMax));
+  CUCHK(cudaFuncSetAttribute(k_smul_fft<Q, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmulFftSmemMax));
+  CUCHK(cudaFuncSetAttribute(k_smul_fft<Q, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmulFftSmemMax));
   // the attribute is per kernel, not per plan: allow the largest plan this Q serves
   const int pw_max = kSmulPwWarps * (10 * 32 * Q + 8) * 4;
   CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, pw_max));
@@ -73,7 +74,10 @@ void smul_fft_q(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool invers
     const int G = 1 << A.nlv;
     const size_t smem = (size_t)G * smul_elem_stride(P->KW, smul_pad<Q>()) * 4 + (size_t)G * 4;
     const int nt = std::max(32, G / 2 * 32);
-    launch_k(k_smul_fft<Q>, dim3((unsigned)(P->n >> A.nlv), npoly), dim3(nt), smem, s, A);
+    if (P->KW == 32 * Q)  // every limb slot live: the kernel drops its bounds checks
+      launch_k(k_smul_fft<Q, true>, dim3((unsigned)(P->n >> A.nlv), npoly), dim3(nt), smem, s, A);
+    else
+      launch_k(k_smul_fft<Q, false>, dim3((unsigned)(P->n >> A.nlv), npoly), dim3(nt), smem, s, A);
   }
 }
 

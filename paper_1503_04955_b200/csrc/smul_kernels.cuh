@@ -65,7 +65,7 @@ __device__ __forceinline__ int spos(int i) { return smul_pad<Q>() ? i + (i >> 5)
 __host__ __device__ inline int smul_elem_stride(int KW, bool pad) { return KW + (pad ? (KW + 31) / 32 : 0); }
 
 // r = x + (sub ? ~y : y) + cin over KW limbs; returns the carry out of limb KW-1
-template <int Q>
+template <int Q, bool FULL = false>  // FULL: KW == 32*Q, every limb slot is live
 __device__ __forceinline__ uint32_t w_add(uint32_t (&r)[Q], const uint32_t (&x)[Q], const uint32_t (&y)[Q], uint32_t cin,
                                           bool sub, int KW) {
   const int lane = threadIdx.x & 31, base = lane * Q;
@@ -73,7 +73,7 @@ __device__ __forceinline__ uint32_t w_add(uint32_t (&r)[Q], const uint32_t (&x)[
   bool ones = true;
 #pragma unroll
   for (int j = 0; j < Q; ++j) {
-    if (base + j < KW) {
+    if (FULL || base + j < KW) {
       const unsigned long long s = (unsigned long long)x[j] + (sub ? ~y[j] : y[j]) + c;
       r[j] = (uint32_t)s;
       c = (uint32_t)(s >> 32);
@@ -82,20 +82,20 @@ __device__ __forceinline__ uint32_t w_add(uint32_t (&r)[Q], const uint32_t (&x)[
       r[j] = 0;
     }
   }
-  const bool valid = base < KW;
+  const bool valid = FULL || base < KW;
   const unsigned G = __ballot_sync(0xFFFFFFFFu, valid && c), P = __ballot_sync(0xFFFFFFFFu, valid && ones && !c);
   const unsigned long long a = (unsigned long long)(G | P), b = G;
   const unsigned long long carries = (a + b + cin) ^ a ^ b;  // bit l: carry into lane l
   uint32_t ci = (uint32_t)(carries >> lane) & 1u;
 #pragma unroll
   for (int j = 0; j < Q; ++j) {
-    if (base + j < KW) {
+    if (FULL || base + j < KW) {
       const uint32_t t = r[j] + ci;
       ci = ci && t == 0u;
       r[j] = t;
     }
   }
-  const int lk = (KW - 1) / Q;  // lane holding limb KW-1
+  const int lk = FULL ? 31 : (KW - 1) / Q;  // lane holding limb KW-1
   return (uint32_t)(carries >> (lk + 1)) & 1u;
 }
 
@@ -108,33 +108,33 @@ __device__ __forceinline__ bool w_nonzero(const uint32_t (&x)[Q]) {
 }
 
 // (u + t) mod 2^K+1 for canonical u, t (bigmul/fermat.py:25-28)
-template <int Q>
+template <int Q, bool FULL = false>
 __device__ __forceinline__ int w_addmod(uint32_t (&r)[Q], const uint32_t (&u)[Q], int ut, const uint32_t (&t)[Q], int tt,
                                         int KW) {
-  const uint32_t c = w_add<Q>(r, u, t, 0u, false, KW);
+  const uint32_t c = w_add<Q, FULL>(r, u, t, 0u, false, KW);
   int T = ut + tt + (int)c;
   const bool nz = w_nonzero<Q>(r);
   if (T >= 2 || (T == 1 && nz)) {  // value >= 2^K + 1: subtract it
     uint32_t z[Q];
 #pragma unroll
     for (int j = 0; j < Q; ++j) z[j] = 0;
-    const uint32_t nb = w_add<Q>(r, r, z, 0u, true, KW);  // r - 1
+    const uint32_t nb = w_add<Q, FULL>(r, r, z, 0u, true, KW);  // r - 1
     T = T - 1 - (nb ? 0 : 1);
   }
   return T;
 }
 
 // (u - t) mod 2^K+1 for canonical u, t (bigmul/fermat.py:31-33)
-template <int Q>
+template <int Q, bool FULL = false>
 __device__ __forceinline__ int w_submod(uint32_t (&r)[Q], const uint32_t (&u)[Q], int ut, const uint32_t (&t)[Q], int tt,
                                         int KW) {
-  const uint32_t c = w_add<Q>(r, u, t, 1u, true, KW);
+  const uint32_t c = w_add<Q, FULL>(r, u, t, 1u, true, KW);
   int T = ut - tt - (c ? 0 : 1);
   if (T < 0) {  // add 2^K + 1
     uint32_t z[Q];
 #pragma unroll
     for (int j = 0; j < Q; ++j) z[j] = 0;
-    const uint32_t c2 = w_add<Q>(r, r, z, 1u, false, KW);
+    const uint32_t c2 = w_add<Q, FULL>(r, r, z, 1u, false, KW);
     T += 1 + (int)c2;
   }
   return T;
@@ -142,7 +142,7 @@ __device__ __forceinline__ int w_submod(uint32_t (&r)[Q], const uint32_t (&u)[Q]
 
 // r = x * 2^e mod 2^K+1, x canonical in shared memory (limbs sx[0..KW), bit K = xtop),
 // 0 <= e < 2K (bigmul/fermat.py:37-49)
-template <int Q>
+template <int Q, bool FULL = false>
 __device__ __forceinline__ int w_mulpow2(uint32_t (&r)[Q], const uint32_t* sx, int xtop, int e, int KW) {
   const int lane = threadIdx.x & 31, base = lane * Q;
   const int K = 32 * KW;
@@ -153,7 +153,7 @@ __device__ __forceinline__ int w_mulpow2(uint32_t (&r)[Q], const uint32_t* sx, i
   }
   if (e == 0 && !neg) {
 #pragma unroll
-    for (int j = 0; j < Q; ++j) r[j] = base + j < KW ? sx[spos<Q>(base + j)] : 0u;
+    for (int j = 0; j < Q; ++j) r[j] = (FULL || base + j < KW) ? sx[spos<Q>(base + j)] : 0u;
     return xtop;
   }
   const int ew = e >> 5, eb = e & 31;
@@ -162,7 +162,7 @@ __device__ __forceinline__ int w_mulpow2(uint32_t (&r)[Q], const uint32_t* sx, i
   for (int j = 0; j < Q; ++j) {
     const int i = base + j;
     lo[j] = hi[j] = 0;
-    if (i >= KW) continue;
+    if (!FULL && i >= KW) continue;
     if (xtop) {  // x = 2^K = -1: x * 2^e = -2^e
       hi[j] = i == ew ? (1u << eb) : 0u;
       continue;
@@ -175,16 +175,16 @@ __device__ __forceinline__ int w_mulpow2(uint32_t (&r)[Q], const uint32_t* sx, i
     hi[j] = eb ? __funnelshift_l(b0, b1, eb) : b1;
   }
   // lo - hi (or hi - lo for e >= K: 2^K == -1 negates)
-  return neg ? w_submod<Q>(r, hi, 0, lo, 0, KW) : w_submod<Q>(r, lo, 0, hi, 0, KW);
+  return neg ? w_submod<Q, FULL>(r, hi, 0, lo, 0, KW) : w_submod<Q, FULL>(r, lo, 0, hi, 0, KW);
 }
 
 // SMEM: sx is an element in the padded shared-memory layout (else plain limbs in HBM)
-template <int Q, bool SMEM = false>
+template <int Q, bool SMEM = false, bool FULL = false>
 __device__ __forceinline__ void w_store(uint32_t* sx, const uint32_t (&r)[Q], int KW) {
   const int base = (threadIdx.x & 31) * Q;
 #pragma unroll
   for (int j = 0; j < Q; ++j)
-    if (base + j < KW) sx[SMEM ? spos<Q>(base + j) : base + j] = r[j];
+    if (FULL || base + j < KW) sx[SMEM ? spos<Q>(base + j) : base + j] = r[j];
 }
 
 // ---- kernels ----------------------------------------------------------------------------
@@ -220,7 +220,7 @@ __global__ void k_smul_encode(SmulEncodeArgs A) {
 
 // nlv radix-2 DIT levels of bigmul/fft.py:82-104 on the 2^nlv elements
 // hi | (j << lv0) | lo of one transform, held in shared memory; a warp per butterfly
-template <int Q>
+template <int Q, bool FULL>
 __global__ void __launch_bounds__(1024) k_smul_fft(SmulFftArgs A) {
   griddep_wait();
   griddep_launch();
@@ -256,16 +256,16 @@ __global__ void __launch_bounds__(1024) k_smul_fft(SmulFftArgs A) {
       uint32_t* pa = sx + ja * ES;
       uint32_t* pb = sx + jb * ES;
       uint32_t t[Q], u[Q], s[Q], d[Q];
-      const int tt = w_mulpow2<Q>(t, pb, (int)stop[jb], e, KW);
+      const int tt = w_mulpow2<Q, FULL>(t, pb, (int)stop[jb], e, KW);
       const int base = lane * Q;
 #pragma unroll
-      for (int q = 0; q < Q; ++q) u[q] = base + q < KW ? pa[spos<Q>(base + q)] : 0u;
+      for (int q = 0; q < Q; ++q) u[q] = (FULL || base + q < KW) ? pa[spos<Q>(base + q)] : 0u;
       const int ut = (int)stop[ja];
-      const int st = w_addmod<Q>(s, u, ut, t, tt, KW);
-      const int dt = w_submod<Q>(d, u, ut, t, tt, KW);
+      const int st = w_addmod<Q, FULL>(s, u, ut, t, tt, KW);
+      const int dt = w_submod<Q, FULL>(d, u, ut, t, tt, KW);
       __syncwarp();
-      w_store<Q, true>(pa, s, KW);
-      w_store<Q, true>(pb, d, KW);
+      w_store<Q, true, FULL>(pa, s, KW);
+      w_store<Q, true, FULL>(pb, d, KW);
       if (lane == 0) {
         stop[ja] = (uint32_t)st;
         stop[jb] = (uint32_t)dt;
@@ -277,9 +277,9 @@ __global__ void __launch_bounds__(1024) k_smul_fft(SmulFftArgs A) {
   if (A.post_e >= 0) {  // normalisation by 2^-m (bigmul/smul.py:268-270)
     for (int j = warp; j < G; j += nw) {
       uint32_t r[Q];
-      const int rt = w_mulpow2<Q>(r, sx + j * ES, (int)stop[j], A.post_e, KW);
+      const int rt = w_mulpow2<Q, FULL>(r, sx + j * ES, (int)stop[j], A.post_e, KW);
       __syncwarp();
-      w_store<Q, true>(sx + j * ES, r, KW);
+      w_store<Q, true, FULL>(sx + j * ES, r, KW);
       if (lane == 0) stop[j] = (uint32_t)rt;
       __syncwarp();
     }
