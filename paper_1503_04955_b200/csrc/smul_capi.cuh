@@ -31,8 +31,12 @@ int smul_set_attrs(smul_plan* P) {
   CUCHK(cudaFuncSetAttribute(k_smul_fft<Q, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmulFftSmemMax));
   // the attribute is per kernel, not per plan: allow the largest plan this Q serves
   const int pw_max = kSmulPwWarps * (10 * 32 * Q + 8) * 4;
-  CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, pw_max));
-  CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (10 * 32 * Q + 8) * 4));
+  CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, pw_max));
+  CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pw_max));
+  CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q, 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (10 * 32 * Q + 8) * 4));
+  CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (10 * 32 * Q + 8) * 4));
   return 0;
 }
 
@@ -97,14 +101,22 @@ void smul_fft(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool inverse,
 // small K: a warp per product (4 per CTA); K >= 2080 (3+ limbs per lane): a CTA of 8 warps per product
 template <int Q>
 void smul_pw_q(smul_plan* P, const SmulPwArgs& A, cudaStream_t s) {
+  const bool full = P->KW == 32 * Q;
   if (Q >= 3) {
-    launch_k(k_smul_pointwise<Q, 8>, dim3((unsigned)std::min<long long>(A.count, 148LL * 8)), dim3(256),
-             (size_t)(10 * P->KW + 8) * 4, s, A);
+    const dim3 g((unsigned)std::min<long long>(A.count, 148LL * 8));
+    const size_t sm = (size_t)(10 * P->KW + 8) * 4;
+    if (full)
+      launch_k(k_smul_pointwise<Q, 8, true>, g, dim3(256), sm, s, A);
+    else
+      launch_k(k_smul_pointwise<Q, 8, false>, g, dim3(256), sm, s, A);
     return;
   }
   const long long blocks = (A.count + kSmulPwWarps - 1) / kSmulPwWarps;
-  launch_k(k_smul_pointwise<Q, 1>, dim3((unsigned)std::min<long long>(blocks, 148LL * 16)), dim3(32 * kSmulPwWarps),
-           P->smem_pw, s, A);
+  const dim3 g((unsigned)std::min<long long>(blocks, 148LL * 16));
+  if (full)
+    launch_k(k_smul_pointwise<Q, 1, true>, g, dim3(32 * kSmulPwWarps), P->smem_pw, s, A);
+  else
+    launch_k(k_smul_pointwise<Q, 1, false>, g, dim3(32 * kSmulPwWarps), P->smem_pw, s, A);
 }
 
 void smul_pointwise(smul_plan* P, const SmulPwArgs& A, cudaStream_t s) {

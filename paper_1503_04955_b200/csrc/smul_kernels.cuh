@@ -304,7 +304,7 @@ __device__ __forceinline__ void group_sync() {
     __syncthreads();  // WPP > 1: the group is the whole CTA
 }
 
-template <int Q, int WPP>
+template <int Q, int WPP, bool FULL>
 __global__ void __launch_bounds__(WPP == 1 ? 128 : 32 * WPP) k_smul_pointwise(SmulPwArgs A) {
   griddep_wait();
   griddep_launch();
@@ -369,14 +369,14 @@ __global__ void __launch_bounds__(WPP == 1 ? 128 : 32 * WPP) k_smul_pointwise(Sm
 #pragma unroll
         for (int j = 0; j < Q; ++j) {
           z[j] = 0;
-          v[j] = base + j < KW ? (at ? yb[base + j] : xa[base + j]) : 0u;
+          v[j] = (FULL || base + j < KW) ? (at ? yb[base + j] : xa[base + j]) : 0u;
         }
         if (at && bt) {
 #pragma unroll
           for (int j = 0; j < Q; ++j) r[j] = (base + j == 0) ? 1u : 0u;
           rt = 0;
         } else {
-          rt = w_submod<Q>(r, z, 0, v, at ? bt : at, KW);
+          rt = w_submod<Q, FULL>(r, z, 0, v, at ? bt : at, KW);
         }
       } else {
         // limb c = low(C_c) + mid(C_(c-1)) + high(C_(c-2)) + carries; lane owns 2Q limbs
@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(WPP == 1 ? 128 : 32 * WPP) k_smul_pointwise(Sm
         for (int j = 0; j < 2 * Q; ++j) {
           const int i = b2 + j;
           unsigned long long v = c;
-          if (i < 2 * KW) {
+          if (FULL || i < 2 * KW) {
             v += scol[3 * i];
             if (i >= 1) v += scol[3 * (i - 1) + 1];
             if (i >= 2) v += scol[3 * (i - 2) + 2];
@@ -416,19 +416,19 @@ __global__ void __launch_bounds__(WPP == 1 ? 128 : 32 * WPP) k_smul_pointwise(Sm
           const uint32_t t = w[j] + ci;
           ci = ci && t == 0u;
           w[j] = t;
-          if (b2 + j < 2 * KW) sp[b2 + j] = w[j];
+          if (FULL || b2 + j < 2 * KW) sp[b2 + j] = w[j];
         }
         __syncwarp();
         uint32_t plo[Q], phi[Q];
         const int base = lane * Q;
 #pragma unroll
         for (int j = 0; j < Q; ++j) {
-          plo[j] = base + j < KW ? sp[base + j] : 0u;
-          phi[j] = base + j < KW ? sp[KW + base + j] : 0u;
+          plo[j] = (FULL || base + j < KW) ? sp[base + j] : 0u;
+          phi[j] = (FULL || base + j < KW) ? sp[KW + base + j] : 0u;
         }
-        rt = w_submod<Q>(r, plo, 0, phi, 0, KW);
+        rt = w_submod<Q, FULL>(r, plo, 0, phi, 0, KW);
       }
-      w_store<Q>(A.out + opos * KW, r, KW);
+      w_store<Q, false, FULL>(A.out + opos * KW, r, KW);
       if (lane == 0) A.otop[opos] = (uint32_t)rt;
     }
     group_sync<WPP>();  // the group's shared memory is reused by the next product
