@@ -146,7 +146,8 @@ def _device_cost(p: SmulPlan) -> float:
     kw = p.K // 32
     q = next(x for x in (1, 2, 3, 4, 6, 8, 16, 32, 64) if 32 * x >= kw)  # limbs per lane, csrc/smul_capi.cuh
     work = 1.5 * p.n * p.m * 32 * q * 8 + p.n * kw * kw
-    return work / min(1.0, p.n / 2048)
+    full = 1.0 if kw == 32 * q else 1.2  # kernels with every lane slot live skip the bounds checks
+    return full * work / min(1.0, p.n / 2048)
 
 
 def device_select_params(n0: int, w: int, table: ThresholdTable | None = None) -> SmulPlan:
