@@ -65,9 +65,15 @@ void smul_fft_q(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool invers
   A.omega_fwd = P->omega_exp;
   A.inverse = inverse ? 1 : 0;
   // levels per pass: at most what shared memory and one warp per butterfly (<= 32 warps)
-  // allow, fewer while the launch would not cover the SMs; then split the levels evenly
+  // allow, fewer while the launch has under 64 CTAs (measured: a level costs about one
+  // butterfly latency however many CTAs share it, so fewer passes beat covering all 148
+  // SMs -- 2^18 -10%, 2^20 -5% against a 148-CTA floor); then split the levels evenly
+  static const long long min_ctas = [] {
+    const char* e = getenv("DKSS_SMUL_MINCTA");  // experiment knob
+    return e ? atoll(e) : 64LL;
+  }();
   int nlv = P->nlv_max;
-  while (nlv > 3 && (P->n >> nlv) * npoly < 148) --nlv;
+  while (nlv > 3 && (P->n >> nlv) * npoly < min_ctas) --nlv;
   const int npass = (P->m + nlv - 1) / nlv;
   for (int i = 0, lv = 0; i < npass; ++i) {
     const int nl = (P->m - lv + (npass - i) - 1) / (npass - i);
