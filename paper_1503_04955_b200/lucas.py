@@ -45,6 +45,11 @@ def lucas_lehmer(p: int, multiplier: str = "dmul", thresholds=None):
         raise ValueError("exponent must be an odd prime")
     if multiplier not in ALGORITHMS:
         raise ValueError(f"unknown algorithm {multiplier!r}")
+    if multiplier == "smul":
+        # the comparison baseline: one GPU smul square per step, reduced on the host
+        # (bigmul/bench.py:210-216 with ALGORITHMS["smul"])
+        fn = ALGORITHMS["smul"]
+        return lucas_lehmer_host(p, square=lambda x: fn(x, x, thresholds, None).to_int())
     if multiplier != "dmul":
         # the reference's other rungs are not part of this build
         ALGORITHMS[multiplier](1, 1, thresholds, None)

@@ -189,3 +189,13 @@ def test_harness_quotient_dmul_over_smul(cuda_ok):
     buf = io.StringIO()
     write_csv(recs, buf)
     assert buf.getvalue().count("smul,") == 2
+
+
+@pytest.mark.gpu
+def test_lucas_lehmer_with_smul(cuda_ok):
+    from paper_1503_04955_b200.lucas import lucas_lehmer, lucas_lehmer_host
+
+    for p in (521, 607, 1279):  # Mersenne prime exponents
+        assert lucas_lehmer(p, "smul") == (True, 0)
+    for p in (523, 1277):       # composite 2^p - 1: residue64 as Python's int loop
+        assert lucas_lehmer(p, "smul") == lucas_lehmer_host(p)
