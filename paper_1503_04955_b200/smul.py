@@ -26,7 +26,7 @@ import numpy as np
 
 from ._native import SmulDevicePlan
 from .dispatch import ThresholdTable, default_thresholds
-from .words import Natural, ScratchArena, as_natural, current_arena, int_to_u32, word_bits
+from .words import Natural, ScratchArena, current_arena, int_to_u32, word_bits
 
 DEVICE_K_MAX = 32768  # include/smul.h: K up to 32768 bits
 
@@ -196,11 +196,13 @@ def _device_plan(plan: SmulPlan, device: int):
 def smul(a, b, thresholds: ThresholdTable | None = None, arena: ScratchArena | None = None) -> Natural:
     """Full product via the outermost Schoenhage-Strassen level on the GPU
     (bigmul/smul.py:286-300): a Natural of len(a) + len(b) words."""
-    a, b = as_natural(a), as_natural(b)
+    from .dkss import _as_int_len  # (value, word length) without building a Natural
+
     arena = arena or current_arena()
     w = word_bits()
-    ai, bi = a.to_int(), b.to_int()
-    outlen = max(1, len(a) + len(b))
+    ai, la_w = _as_int_len(a, w)
+    bi, lb_w = _as_int_len(b, w)
+    outlen = max(1, la_w + lb_w)
     if ai == 0 or bi == 0:
         return Natural([0] * outlen)
     n0 = ai.bit_length() + bi.bit_length()
