@@ -55,8 +55,16 @@ int smul_attrs(smul_plan* P) {
 }
 
 template <int Q>
-void smul_fft_q(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool inverse, bool normalise, cudaStream_t s) {
+void smul_fft_q(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool inverse, bool normalise, cudaStream_t s,
+                const SmulFftArgs* enc) {
   SmulFftArgs A{};
+  if (enc) {  // encode fused into the first pass
+    A.enc_a = enc->enc_a;
+    A.enc_b = enc->enc_b;
+    A.enc_na = enc->enc_na;
+    A.enc_s = enc->enc_s;
+    A.enc_batch = enc->enc_batch;
+  }
   A.x = x;
   A.top = top;
   A.log_n = P->m;
@@ -88,19 +96,21 @@ void smul_fft_q(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool invers
       launch_k(k_smul_fft<Q, true>, dim3((unsigned)(P->n >> A.nlv), npoly), dim3(nt), smem, s, A);
     else
       launch_k(k_smul_fft<Q, false>, dim3((unsigned)(P->n >> A.nlv), npoly), dim3(nt), smem, s, A);
+    A.enc_a = nullptr;
   }
 }
 
-void smul_fft(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool inverse, bool normalise, cudaStream_t s) {
+void smul_fft(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool inverse, bool normalise, cudaStream_t s,
+              const SmulFftArgs* enc = nullptr) {
   switch (P->Q) {
-    case 1: return smul_fft_q<1>(P, x, top, npoly, inverse, normalise, s);
-    case 2: return smul_fft_q<2>(P, x, top, npoly, inverse, normalise, s);
-    case 3: return smul_fft_q<3>(P, x, top, npoly, inverse, normalise, s);
-    case 6: return smul_fft_q<6>(P, x, top, npoly, inverse, normalise, s);
-    case 4: return smul_fft_q<4>(P, x, top, npoly, inverse, normalise, s);
-    case 8: return smul_fft_q<8>(P, x, top, npoly, inverse, normalise, s);
-    case 16: return smul_fft_q<16>(P, x, top, npoly, inverse, normalise, s);
-    case 32: return smul_fft_q<32>(P, x, top, npoly, inverse, normalise, s);
+    case 1: return smul_fft_q<1>(P, x, top, npoly, inverse, normalise, s, enc);
+    case 2: return smul_fft_q<2>(P, x, top, npoly, inverse, normalise, s, enc);
+    case 3: return smul_fft_q<3>(P, x, top, npoly, inverse, normalise, s, enc);
+    case 6: return smul_fft_q<6>(P, x, top, npoly, inverse, normalise, s, enc);
+    case 4: return smul_fft_q<4>(P, x, top, npoly, inverse, normalise, s, enc);
+    case 8: return smul_fft_q<8>(P, x, top, npoly, inverse, normalise, s, enc);
+    case 16: return smul_fft_q<16>(P, x, top, npoly, inverse, normalise, s, enc);
+    case 32: return smul_fft_q<32>(P, x, top, npoly, inverse, normalise, s, enc);
   }
 }
 
@@ -180,19 +190,13 @@ int run_smul(smul_plan* P, int batch, const uint32_t* a, const uint32_t* b, long
   int rc;
   if ((rc = smul_ensure(P, ops, nc))) return rc;
   const long long vec = P->n * P->KW;
-  SmulEncodeArgs E{};
-  E.na = na;
-  E.log_n = P->m;
-  E.KW = P->KW;
-  E.s = P->s;
-  const int gx = (int)std::max<long long>(1, std::min<long long>((vec + 255) / 256, 1184 / std::max(1, batch) + 1));
-  for (int q = 0; q < (sq ? 1 : 2); ++q) {
-    E.a = q ? b : a;
-    E.x = P->d_x + (size_t)q * batch * vec;
-    E.top = P->d_xt + (size_t)q * batch * P->n;
-    launch_k(k_smul_encode, dim3(gx, batch), dim3(256), 0, s, E);
-  }
-  smul_fft(P, P->d_x, P->d_xt, ops, false, false, s);
+  SmulFftArgs enc{};  // encode (bit_slices + shuffle) fused into the first forward pass
+  enc.enc_a = a;
+  enc.enc_b = sq ? a : b;
+  enc.enc_na = na;
+  enc.enc_s = P->s;
+  enc.enc_batch = batch;
+  smul_fft(P, P->d_x, P->d_xt, ops, false, false, s, &enc);
   SmulPwArgs W{};
   W.x = P->d_x;
   W.xtop = P->d_xt;

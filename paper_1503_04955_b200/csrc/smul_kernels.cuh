@@ -31,7 +31,27 @@ struct SmulFftArgs {
   int inverse;    // 1: transform with the inverse root 2^(2K - omega_fwd)
   int lv0, nlv;   // DIT levels [lv0, lv0 + nlv): merges of length 2^(l+1)
   int post_e;     // >= 0: multiply every element by 2^post_e after the last level
+  // encode fused into the first pass (enc_a non-null): polynomial q < enc_batch is the slices
+  // of operand q of enc_a, q >= enc_batch of operand q - enc_batch of enc_b ([batch][enc_na])
+  const uint32_t* enc_a;
+  const uint32_t* enc_b;
+  long long enc_na, enc_s;
+  int enc_batch;
 };
+
+// limb i of the s-bit slice j of operand a (na limbs): bigmul/words.py:307-329
+__device__ __forceinline__ uint32_t smul_slice_limb(const uint32_t* a, long long na, long long s, long long j, int i) {
+  const long long rel = 32LL * i;  // bit offset inside the slice
+  if (rel >= s) return 0u;
+  const long long bit = j * s + rel;
+  const long long wi = bit >> 5;
+  const int sh = (int)(bit & 31);
+  const uint32_t l0 = wi < na ? a[wi] : 0u, l1 = wi + 1 < na ? a[wi + 1] : 0u;
+  uint32_t w = sh ? __funnelshift_r(l0, l1, sh) : l0;
+  const long long keep = s - rel;
+  if (keep < 32) w &= (1u << keep) - 1u;
+  return w;
+}
 
 struct SmulPwArgs {
   const uint32_t* x;     // transforms of a: [batch][n][KW] + top
@@ -42,15 +62,6 @@ struct SmulPwArgs {
   uint32_t* otop;
   int log_n, KW;
   long long count;       // batch * n products
-};
-
-struct SmulEncodeArgs {
-  const uint32_t* a;     // [nops][na] limbs
-  long long na;
-  uint32_t* x;           // [nops][n][KW], element i = slice bitrev(i)
-  uint32_t* top;
-  int log_n, KW;
-  long long s;           // bits per slice
 };
 
 // ---- warp-distributed multi-limb arithmetic ---------------------------------------------
@@ -189,37 +200,10 @@ __device__ __forceinline__ void w_store(uint32_t* sx, const uint32_t (&r)[Q], in
 
 // ---- kernels ----------------------------------------------------------------------------
 
-// slices of s bits (bigmul/words.py:307-329), shuffled into bit-reversed order
-// (bigmul/smul.py:260-261); one thread per output limb
-__global__ void k_smul_encode(SmulEncodeArgs A) {
-  griddep_wait();
-  griddep_launch();
-  const int q = blockIdx.y;
-  const long long n = 1LL << A.log_n, total = n * A.KW;
-  const uint32_t* a = A.a + (long long)q * A.na;
-  uint32_t* x = A.x + (long long)q * total;
-  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (long long)gridDim.x * blockDim.x) {
-    const long long pos = g / A.KW;
-    const int i = (int)(g - pos * A.KW);
-    const long long j = __brev((unsigned)pos) >> (32 - A.log_n);  // slice index at this position
-    uint32_t w = 0;
-    const long long rel = 32LL * i;  // bit offset inside the slice
-    if (rel < A.s) {
-      const long long bit = j * A.s + rel;
-      const long long wi = bit >> 5;
-      const int sh = (int)(bit & 31);
-      const uint32_t l0 = wi < A.na ? a[wi] : 0u, l1 = wi + 1 < A.na ? a[wi + 1] : 0u;
-      w = sh ? __funnelshift_r(l0, l1, sh) : l0;
-      const long long keep = A.s - rel;
-      if (keep < 32) w &= (1u << keep) - 1u;
-    }
-    x[g] = w;
-    if (i == 0) A.top[(long long)q * n + pos] = 0u;
-  }
-}
-
 // nlv radix-2 DIT levels of bigmul/fft.py:82-104 on the 2^nlv elements
-// hi | (j << lv0) | lo of one transform, held in shared memory; a warp per butterfly
+// hi | (j << lv0) | lo of one transform, held in shared memory; a warp per butterfly.  The
+// first forward pass reads the operand limbs directly: element p is the s-bit slice
+// bitrev(p) (bit_slices + the shuffle, bigmul/smul.py:260-261)
 template <int Q, bool FULL>
 __global__ void __launch_bounds__(1024) k_smul_fft(SmulFftArgs A) {
   griddep_wait();
@@ -236,10 +220,20 @@ __global__ void __launch_bounds__(1024) k_smul_fft(SmulFftArgs A) {
   const long long lo = g & ((1LL << A.lv0) - 1), hi = (g >> A.lv0) << (A.lv0 + A.nlv);
   auto gidx = [&](int j) { return hi | ((long long)j << A.lv0) | lo; };
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
-  for (int j = warp; j < G; j += nw) {  // a warp per element: contiguous KW-limb rows
-    const uint32_t* src = X + gidx(j) * KW;
-    for (int i = lane; i < KW; i += 32) sx[j * ES + spos<Q>(i)] = src[i];
-    if (lane == 0) stop[j] = T[gidx(j)];
+  if (A.enc_a) {  // first forward pass: the shuffled slices straight from the operand limbs
+    const int q = blockIdx.y;
+    const uint32_t* op = q < A.enc_batch ? A.enc_a + (long long)q * A.enc_na : A.enc_b + (long long)(q - A.enc_batch) * A.enc_na;
+    for (int j = warp; j < G; j += nw) {
+      const long long sl = __brev((unsigned)gidx(j)) >> (32 - A.log_n);
+      for (int i = lane; i < KW; i += 32) sx[j * ES + spos<Q>(i)] = smul_slice_limb(op, A.enc_na, A.enc_s, sl, i);
+      if (lane == 0) stop[j] = 0u;
+    }
+  } else {
+    for (int j = warp; j < G; j += nw) {  // a warp per element: contiguous KW-limb rows
+      const uint32_t* src = X + gidx(j) * KW;
+      for (int i = lane; i < KW; i += 32) sx[j * ES + spos<Q>(i)] = src[i];
+      if (lane == 0) stop[j] = T[gidx(j)];
+    }
   }
   __syncthreads();
   for (int l = A.lv0; l < A.lv0 + A.nlv; ++l) {
