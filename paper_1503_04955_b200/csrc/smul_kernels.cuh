@@ -229,11 +229,20 @@ __global__ void __launch_bounds__(1024) k_smul_fft(SmulFftArgs A) {
       if (lane == 0) stop[j] = 0u;
     }
   } else {
-    for (int j = warp; j < G; j += nw) {  // a warp per element: contiguous KW-limb rows
+    // a warp per element (contiguous KW-limb rows), copied global -> shared with cp.async so
+    // every load of the tile is in flight at once (a register round trip serialised them)
+    for (int j = warp; j < G; j += nw) {
       const uint32_t* src = X + gidx(j) * KW;
-      for (int i = lane; i < KW; i += 32) sx[j * ES + spos<Q>(i)] = src[i];
-      if (lane == 0) stop[j] = T[gidx(j)];
+      for (int i = lane; i < KW; i += 32) {
+        const unsigned d = (unsigned)__cvta_generic_to_shared(sx + j * ES + spos<Q>(i));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src + i) : "memory");
+      }
+      if (lane == 0) {
+        const unsigned d = (unsigned)__cvta_generic_to_shared(stop + j);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(T + gidx(j)) : "memory");
+      }
     }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
   }
   __syncthreads();
   for (int l = A.lv0; l < A.lv0 + A.nlv; ++l) {
