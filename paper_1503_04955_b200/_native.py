@@ -195,14 +195,18 @@ class DevicePlan:
                                          _ptr(out), nc))
         return out
 
-    def mul_batch_digits(self, a_ptrs, na, b_ptrs, nb, digit_bits: int, nc: int) -> np.ndarray:
-        """Products of pairs of radix-2^digit_bits digit strings (host addresses + counts)."""
+    def mul_batch_digits(self, a_ptrs, na, b_ptrs, nb, digit_bits: int, nc: int, out=None) -> np.ndarray:
+        """Products of pairs of radix-2^digit_bits digit strings (host addresses + counts);
+        `out`, if given, is a C-contiguous uint32[batch][nc] the products are written to."""
         batch = len(a_ptrs)
         vpa = (ctypes.c_void_p * batch)(*a_ptrs)
         vpb = (ctypes.c_void_p * batch)(*b_ptrs)
         cna = (ctypes.c_size_t * batch)(*na)
         cnb = (ctypes.c_size_t * batch)(*nb)
-        out = np.empty((batch, nc), dtype=np.uint32)
+        if out is None:
+            out = np.empty((batch, nc), dtype=np.uint32)
+        elif out.shape != (batch, nc) or out.dtype != np.uint32 or not out.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous uint32[batch][nc] array")
         _check(self._lib.dkss_mul_batch_digits(self._h, batch, vpa, cna, vpb, cnb, digit_bits, _ptr(out), nc))
         return out
 

@@ -90,14 +90,15 @@ def plan_capacity(plan: DkssPlan) -> int:
     return plan.M * (plan.m // 2) * plan.u
 
 
-def device_plan(plan: DkssPlan, device: int | None = None) -> DevicePlan:
+def device_plan(plan: DkssPlan, device: int | None = None, lane: int = 0) -> DevicePlan:
     """Upload (once) and return the device plan for a host plan.
 
     Device plans are shared by every N with the same geometry (M, m, u, p): they are built for
     the geometry's capacity, so multiplying operands of many different sizes does not create
-    a device plan (twiddle table + workspace) per size."""
+    a device plan (twiddle table + workspace) per size.  ``lane`` > 0 gives further handles of
+    the same geometry (own stream and workspace) for concurrent host threads."""
     device = _device() if device is None else device
-    key = (plan.M, plan.m, plan.u, plan.p, device)
+    key = (plan.M, plan.m, plan.u, plan.p, device) + ((lane,) if lane else ())
     with _dev_lock:
         dp = _dev_plans.get(key)
         if dp is None:
@@ -264,6 +265,39 @@ def dmul(a, b, thresholds=None, arena: ScratchArena | None = None) -> Natural:
     return Natural._from_u32(c, outlen, w)
 
 
+_PIPE_MIN_PAIRS = 64   # batches at least this large run as chunks on two device lanes
+_PIPE_CHUNKS = 2  # measured at 1024 x 2^18: 1 chunk 23.2 ms, 2: 20.1, 4: 20.5, 8: 20.8, 16: 22.0
+_pipe_pool = None
+
+
+def _pipelined_batch(plan, da, db, digit_bits: int, nc: int) -> np.ndarray:
+    """The batch as _PIPE_CHUNKS chunks on two device plans (own stream and workspace each),
+    driven by two host threads: one chunk's host staging, H2D and D2H overlap the other
+    lane's device work (the C call releases the GIL).  Same products as one batch call."""
+    global _pipe_pool
+    from concurrent.futures import ThreadPoolExecutor
+
+    if _pipe_pool is None:
+        _pipe_pool = ThreadPoolExecutor(max_workers=2, thread_name_prefix="dkss-lane")
+    n = len(da)
+    step = -(-n // _PIPE_CHUNKS)
+    chunks = [(i, min(n, i + step)) for i in range(0, n, step)]
+    out = np.empty((n, nc), dtype=np.uint32)
+    device = _device()
+
+    def lane_work(lane):
+        dpl = device_plan(plan, device, lane)
+        for k in range(lane, len(chunks), 2):
+            lo, hi = chunks[k]
+            dpl.mul_batch_digits([d[1] for d in da[lo:hi]], [d[2] for d in da[lo:hi]], [d[1] for d in db[lo:hi]],
+                                 [d[2] for d in db[lo:hi]], digit_bits, nc, out=out[lo:hi])
+
+    futs = [_pipe_pool.submit(lane_work, lane) for lane in (0, 1)]
+    for f in futs:
+        f.result()
+    return out
+
+
 def dmul_many(pairs, thresholds=None) -> list:
     """Independent products sharing one plan, batched in one device call (config 3).
 
@@ -282,7 +316,9 @@ def dmul_many(pairs, thresholds=None) -> list:
     da = [_digits(a, ai) for (a, _), ((ai, _), _) in zip(pairs, vals)]
     db = [_digits(b, bi) for (_, b), (_, (bi, _)) in zip(pairs, vals)]
     bits = {d[3] for d in da} | {d[3] for d in db}
-    if len(bits) == 1:
+    if len(bits) == 1 and len(pairs) >= _PIPE_MIN_PAIRS:
+        C = _pipelined_batch(plan, da, db, bits.pop(), nc)
+    elif len(bits) == 1:
         C = dp.mul_batch_digits([d[1] for d in da], [d[2] for d in da], [d[1] for d in db], [d[2] for d in db],
                                 bits.pop(), nc)
     else:

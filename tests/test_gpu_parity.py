@@ -146,6 +146,20 @@ def test_batched_products(cuda_ok):
     assert got == [a * b for a, b in pairs]
 
 
+def test_pipelined_batch_ragged(cuda_ok):
+    # >= 64 pairs run as 8 chunks on two device lanes (dkss._pipelined_batch): uneven chunk
+    # sizes, ragged operand lengths, all-ones pairs, results in input order
+    rng = random.Random(21)
+    pairs = []
+    for i in range(131):
+        na, nb = rng.randrange(1, 1 << 16), rng.randrange(1, 1 << 16)
+        pairs.append((rng.getrandbits(na) | 1, rng.getrandbits(nb) | 1))
+    pairs[7] = pairs[100] = ((1 << (1 << 16)) - 1, (1 << (1 << 16)) - 1)
+    got = dmul_many(pairs)
+    assert [g.to_int() for g in got] == [a * b for a, b in pairs]
+    assert dmul_many(pairs[:3]) == [a * b for a, b in pairs[:3]]  # below the pipelining threshold
+
+
 def test_device_api_graph_replay(cuda_ok):
     import torch
 
