@@ -49,6 +49,12 @@ int64_t smul_product_limbs(const smul_plan* plan);
  * DKSS_ERANGE if the product needs more).  a == b (same pointer and size) squares. */
 int smul_mul(smul_plan* plan, const uint32_t* a, size_t na, const uint32_t* b, size_t nb, uint32_t* c, size_t nc);
 
+/* the same product from radix-2^digit_bits digit strings (8 <= digit_bits <= 32, one digit per
+ * uint32, little endian; | DKSS_DIGITS_TRUSTED skips the digit range scan), e.g. CPython's
+ * 30-bit int digits: staged to the device and repacked there (as dkss_mul_digits). */
+int smul_mul_digits(smul_plan* plan, const uint32_t* a, size_t na, const uint32_t* b, size_t nb, int digit_bits,
+                    uint32_t* c, size_t nc);
+
 /* batch device multiply: a_dev, b_dev are [batch][n_limbs] (b_dev NULL squares a), c_dev is
  * [batch][nc] with nc >= smul_product_limbs.  Stream-ordered; products must be < 2^N. */
 int smul_mul_device(smul_plan* plan, int batch, const uint32_t* a_dev, const uint32_t* b_dev, size_t n_limbs,

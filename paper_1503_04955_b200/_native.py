@@ -26,7 +26,8 @@ EXPORTS = (
     "dkss_block_transpose", "dkss_decode_device", "dkss_lucas_lehmer", "dkss_fs_decode_partial",
     "dkss_fs_decode_finish",
     # include/smul.h
-    "smul_plan_create", "smul_plan_destroy", "smul_product_limbs", "smul_mul", "smul_mul_device", "smul_fft_host",
+    "smul_plan_create", "smul_plan_destroy", "smul_product_limbs", "smul_mul", "smul_mul_digits", "smul_mul_device",
+    "smul_fft_host",
 )
 
 DKSS_OK, DKSS_EINVAL, DKSS_ECUDA, DKSS_ERANGE, DKSS_ENOMEM = 0, -1, -2, -3, -4
@@ -123,6 +124,7 @@ def load(path: str = LIB_PATH):
         L.smul_product_limbs.restype = ctypes.c_int64
         L.smul_mul.argtypes = [vp, _u32p, ctypes.c_size_t, _u32p, ctypes.c_size_t, _u32p, ctypes.c_size_t]
         L.smul_mul_device.argtypes = [vp, ctypes.c_int, vp, vp, ctypes.c_size_t, vp, ctypes.c_size_t, vp]
+        L.smul_mul_digits.argtypes = [vp, vp, ctypes.c_size_t, vp, ctypes.c_size_t, ctypes.c_int, _u32p, ctypes.c_size_t]
         L.smul_fft_host.argtypes = [vp, _u32p, _u32p, ctypes.c_int]
         for name in EXPORTS:
             if not hasattr(L, name):
@@ -330,6 +332,12 @@ class SmulDevicePlan:
             _check(self._lib.smul_mul(self._h, _ptr(a), a.size, _ptr(a), a.size, _ptr(out), nc))
         else:
             _check(self._lib.smul_mul(self._h, _ptr(a), a.size, _ptr(b), b.size, _ptr(out), nc))
+        return out[:nc]
+
+    def mul_digits(self, a_ptr: int, na: int, b_ptr: int, nb: int, digit_bits: int, nc: int) -> np.ndarray:
+        """Product of two radix-2^digit_bits digit strings (host addresses + counts)."""
+        out = np.zeros(max(nc, 1), dtype=np.uint32)
+        _check(self._lib.smul_mul_digits(self._h, a_ptr, na, b_ptr, nb, digit_bits, _ptr(out), nc))
         return out[:nc]
 
     def mul_device(self, batch: int, a_ptr: int, b_ptr: int, n_limbs: int, c_ptr: int, nc: int, stream: int = 0):

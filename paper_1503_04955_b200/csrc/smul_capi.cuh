@@ -17,6 +17,9 @@ struct smul_plan {
   long long cap_nc = 0;
   uint32_t *d_x = nullptr, *d_xt = nullptr, *d_o = nullptr, *d_ot = nullptr;
   uint32_t *d_ops = nullptr, *d_prod = nullptr, *d_gmask = nullptr, *d_pmask = nullptr, *d_bstat = nullptr;
+  uint32_t* h_pin = nullptr;    // pinned staging of the digits entry point
+  uint32_t* d_stage = nullptr;
+  size_t pin_words = 0;
   std::mutex mu;
 };
 
@@ -292,6 +295,8 @@ void smul_plan_destroy(smul_plan* P) {
   if (!P) return;
   cudaSetDevice(P->device);
   smul_free(P);
+  if (P->h_pin) cudaFreeHost(P->h_pin);
+  if (P->d_stage) cudaFree(P->d_stage);
   if (P->stream) cudaStreamDestroy(P->stream);
   delete P;
 }
@@ -333,6 +338,75 @@ int smul_mul(smul_plan* P, const uint32_t* a, size_t na, const uint32_t* b, size
   for (size_t k = ncopy; k < full.size(); ++k)
     if (full[k]) return fail(DKSS_ERANGE, "product does not fit nc=%zu limbs", nc);
   if (ncopy) memcpy(c, full.data(), ncopy * 4);
+  if (nc > ncopy) memset(c + ncopy, 0, (nc - ncopy) * 4);
+  return DKSS_OK;
+}
+
+int smul_mul_digits(smul_plan* P, const uint32_t* a, size_t na, const uint32_t* b, size_t nb, int digit_bits,
+                    uint32_t* c, size_t nc) {
+  if (!P || (!a && na) || (!b && nb) || (!c && nc)) return fail(DKSS_EINVAL, "bad argument");
+  const bool trusted = digit_bits & DKSS_DIGITS_TRUSTED;
+  digit_bits &= ~DKSS_DIGITS_TRUSTED;
+  if (digit_bits < 8 || digit_bits > 32) return fail(DKSS_EINVAL, "digit_bits=%d outside [8, 32]", digit_bits);
+  const bool sq = a == b && na == nb;
+  const uint32_t* ops[2] = {a, b};
+  size_t nd[2] = {na, nb};
+  long long bits[2];
+  for (int q = 0; q < 2; ++q) {
+    while (nd[q] > 0 && ops[q][nd[q] - 1] == 0) --nd[q];
+    if (digit_bits < 32 && !trusted) {
+      uint32_t any = 0;
+      for (size_t i = 0; i < nd[q]; ++i) any |= ops[q][i];
+      if (any >> digit_bits) return fail(DKSS_EINVAL, "a digit exceeds %d bits", digit_bits);
+    }
+    const uint32_t top = nd[q] ? ops[q][nd[q] - 1] : 0u;
+    if (digit_bits < 32 && (top >> digit_bits)) return fail(DKSS_EINVAL, "a digit exceeds %d bits", digit_bits);
+    bits[q] = nd[q] ? (long long)(nd[q] - 1) * digit_bits + (32 - __builtin_clz(top)) : 0;
+  }
+  if (bits[0] + bits[1] > P->N) return fail(DKSS_ERANGE, "product of %lld + %lld bits exceeds N=%lld", bits[0], bits[1], P->N);
+  const size_t nl = (size_t)std::max<long long>(1, (std::max(bits[0], bits[1]) + 31) / 32);
+  const int nops = sq ? 1 : 2;
+  const size_t head = 2 * (size_t)(nops + 1);  // long long offsets, in u32 words
+  const size_t cap = head + nd[0] + (sq ? 0 : nd[1]);
+  std::lock_guard<std::mutex> lk(P->mu);
+  CUCHK(cudaSetDevice(P->device));
+  int rc;
+  if ((rc = smul_ensure(P, 2, P->prod_limbs))) return rc;
+  const size_t pin_need = std::max(cap, (size_t)P->prod_limbs);
+  if (pin_need > P->pin_words) {
+    if (P->h_pin) cudaFreeHost(P->h_pin);
+    if (P->d_stage) cudaFree(P->d_stage);
+    P->h_pin = nullptr;
+    P->d_stage = nullptr;
+    P->pin_words = 0;
+    CUCHK(cudaMallocHost(&P->h_pin, pin_need * 4));
+    CUCHK(cudaMalloc(&P->d_stage, pin_need * 4));
+    P->pin_words = pin_need;
+  }
+  long long* off = reinterpret_cast<long long*>(P->h_pin);
+  off[0] = 0;
+  off[1] = (long long)nd[0];
+  if (!sq) off[2] = (long long)(nd[0] + nd[1]);
+  if (nd[0]) memcpy(P->h_pin + head, a, nd[0] * 4);
+  if (!sq && nd[1]) memcpy(P->h_pin + head + nd[0], b, nd[1] * 4);
+  cudaStream_t s = P->stream;
+  CUCHK(cudaMemcpyAsync(P->d_stage, P->h_pin, cap * 4, cudaMemcpyHostToDevice, s));
+  RepackArgs R{};  // radix change on the device (k_repack_bits, shared with the DKSS entry point)
+  R.stage = P->d_stage + head;
+  R.off = reinterpret_cast<const long long*>(P->d_stage);
+  R.dst = P->d_ops;
+  R.ndst = (long long)nl;
+  R.sbits = digit_bits;
+  const int gx = (int)std::max<size_t>(1, std::min<size_t>((nl + 255) / 256, 592));
+  launch_k(k_repack_bits, dim3(gx, nops), dim3(256), 0, s, R);
+  if ((rc = run_smul(P, 1, P->d_ops, sq ? nullptr : P->d_ops + nl, (long long)nl, P->d_prod, P->prod_limbs, s)))
+    return rc;
+  CUCHK(cudaMemcpyAsync(P->h_pin, P->d_prod, P->prod_limbs * 4, cudaMemcpyDeviceToHost, s));
+  CUCHK(cudaStreamSynchronize(s));
+  const size_t ncopy = std::min<size_t>(nc, (size_t)P->prod_limbs);
+  for (size_t k = ncopy; k < (size_t)P->prod_limbs; ++k)
+    if (P->h_pin[k]) return fail(DKSS_ERANGE, "product does not fit nc=%zu limbs", nc);
+  if (ncopy) memcpy(c, P->h_pin, ncopy * 4);
   if (nc > ncopy) memset(c + ncopy, 0, (nc - ncopy) * 4);
   return DKSS_OK;
 }

@@ -73,9 +73,11 @@ def _round_up(v: int, a: int) -> int:
     return (v + a - 1) // a * a
 
 
-def smul_plan_candidates(N: int, outermost: bool, w: int | None = None) -> list:
+def smul_plan_candidates(N: int, outermost: bool, w: int | None = None, validate: bool = True) -> list:
     """Every feasible (m, K) for an N-bit modulus (bigmul/smul.py:75-105): per depth m the
-    smallest admissible K, then the next power of two if it is at most twice that."""
+    smallest admissible K, then the next power of two if it is at most twice that.
+    ``validate=False`` skips the per-plan checks (a modular power over 2^K + 1 each; the
+    candidates satisfy them by construction) -- the device planner's fast path."""
     w = word_bits() if w is None else w
     out = []
     for m in range(1, 27):
@@ -100,7 +102,8 @@ def smul_plan_candidates(N: int, outermost: bool, w: int | None = None) -> list:
                 om, th = 2 * K // n, 0
             else:
                 om, th = 2 * (K // n), K // n
-            out.append(SmulPlan(s * n, m, n, s, K, om, th, outermost, w).validate())
+            p = SmulPlan(s * n, m, n, s, K, om, th, outermost, w)
+            out.append(p.validate() if validate else p)
         if n >= 2 * k_floor and n >= 2 * w:
             break
     return out
@@ -164,18 +167,35 @@ def device_select_params(n0: int, w: int, table: ThresholdTable | None = None) -
         p = smul_select_params(n0, True, wd, table)
         if p.m == forced and p.K % 32 == 0 and p.K <= DEVICE_K_MAX:
             return p
-    cands = [p for p in smul_plan_candidates(n0, True, wd) if p.K % 32 == 0 and p.K <= DEVICE_K_MAX]
+    cands = [p for p in smul_plan_candidates(n0, True, wd, validate=False) if p.K % 32 == 0 and p.K <= DEVICE_K_MAX]
     if not cands:
         raise ValueError(f"no device Schoenhage-Strassen plan for N={n0}")
     return min(cands, key=_device_cost)
 
 
+_sel_cache: dict = {}
+
+
 def device_plan_for(n0: int, w: int, table: ThresholdTable | None = None, device: int | None = None):
-    """(host plan, device plan) for a product of n0 bits at word size w."""
+    """(host plan, device plan) for a product of n0 bits at word size w.  The selection is
+    cached per (n0, w, pinned depth): enumerating the candidates validates every one with a
+    modular power over 2^K + 1 (milliseconds at 2^20), far more than the multiply."""
     from .dkss import _device
 
     device = _device() if device is None else device
-    plan = device_select_params(n0, w, table)
+    table = table or default_thresholds()
+    # nearby sizes share a plan: n0 rounded up to 1/32 of its octave (any plan with N >= n0
+    # computes the product exactly)
+    step = 1 << max(0, n0.bit_length() - 6)
+    n0r = -(-n0 // step) * step
+    key = (n0r, w, table.smul_fft_m.get(max(0, (n0 // w).bit_length() - 1)))
+    plan = _sel_cache.get(key)
+    if plan is None:
+        plan = device_select_params(n0r, w, table)
+        with _lock:
+            _sel_cache[key] = plan
+            while len(_sel_cache) > 1024:
+                _sel_cache.pop(next(iter(_sel_cache)))
     return plan, _device_plan(plan, device)
 
 
@@ -196,7 +216,7 @@ def _device_plan(plan: SmulPlan, device: int):
 def smul(a, b, thresholds: ThresholdTable | None = None, arena: ScratchArena | None = None) -> Natural:
     """Full product via the outermost Schoenhage-Strassen level on the GPU
     (bigmul/smul.py:286-300): a Natural of len(a) + len(b) words."""
-    from .dkss import _as_int_len  # (value, word length) without building a Natural
+    from .dkss import _as_int_len, _digits  # (value, word length) without building a Natural
 
     arena = arena or current_arena()
     w = word_bits()
@@ -211,8 +231,14 @@ def smul(a, b, thresholds: ThresholdTable | None = None, arena: ScratchArena | N
     la, lb = -(-ai.bit_length() // 32), -(-bi.bit_length() // 32)
     with arena.frame():
         arena.alloc_words(2 * plan.n * plan.fe_word_count() + plan.fe_word_count())  # bigmul/smul.py:232
-        A = int_to_u32(ai, la)
-        c = dp.mul_limbs(A, A if bi == ai else int_to_u32(bi, lb), nc)
+        ka, pa, na, ba = _digits(a, ai)
+        kb, pb, nb, bb = (ka, pa, na, ba) if b is a else _digits(b, bi)
+        if ba == bb:  # CPython's own digits (or limbs) go straight to the device
+            c = dp.mul_digits(pa, na, pb, nb, ba, nc)
+        else:
+            A = int_to_u32(ai, la)
+            c = dp.mul_limbs(A, A if bi == ai else int_to_u32(bi, lb), nc)
+        del ka, kb
     return Natural._from_u32(c, outlen, w)
 
 

@@ -199,3 +199,25 @@ def test_lucas_lehmer_with_smul(cuda_ok):
         assert lucas_lehmer(p, "smul") == (True, 0)
     for p in (523, 1277):       # composite 2^p - 1: residue64 as Python's int loop
         assert lucas_lehmer(p, "smul") == lucas_lehmer_host(p)
+
+
+@pytest.mark.gpu
+def test_smul_digits_entry_point(cuda_ok):
+    from paper_1503_04955_b200.smul import device_plan_for
+
+    rng = random.Random(13)
+    a, b = rng.getrandbits(90000) | 1, rng.getrandbits(70001) | 1
+    _, dp = device_plan_for(a.bit_length() + b.bit_length(), 64)
+
+    def digits(x, k):
+        return np.array([(x >> (k * i)) & ((1 << k) - 1) for i in range(-(-x.bit_length() // k))], dtype=np.uint32)
+
+    nc = -(-(a.bit_length() + b.bit_length()) // 32)
+    for k in (8, 30, 32):  # radix 2^k digit strings, repacked on the device
+        da, db = digits(a, k), digits(b, k)
+        c = dp.mul_digits(da.ctypes.data, da.size, db.ctypes.data, db.size, k, nc)
+        assert int.from_bytes(c.tobytes(), "little") == a * b
+    bad = digits(a, 30)
+    bad[5] |= 1 << 30  # a digit above 30 bits is rejected unless the caller vouches for it
+    with pytest.raises(ValueError):
+        dp.mul_digits(bad.ctypes.data, bad.size, bad.ctypes.data, bad.size, 30, nc)
