@@ -85,13 +85,15 @@ class Natural:
     and build the word list only when ``words`` is first read.
     """
 
-    __slots__ = ("_words", "_limbs", "_w", "_len")
+    __slots__ = ("_words", "_limbs", "_w", "_len", "_ival", "_iw")
 
     def __init__(self, words):
         self._words = list(words)
         self._limbs = None
         self._w = None
         self._len = len(self._words)
+        self._ival = None  # value cache (the object is immutable): (value, word size it was read at)
+        self._iw = None
 
     @classmethod
     def _from_u32(cls, limbs: np.ndarray, length: int, w: int) -> "Natural":
@@ -104,6 +106,8 @@ class Natural:
         obj._w = w
         obj._len = length
         obj._words = None
+        obj._ival = None
+        obj._iw = None
         return obj
 
     @property
@@ -127,13 +131,20 @@ class Natural:
             length = need
         elif length < need:
             raise ValueError(f"value needs {need} words, got length={length}")
-        return cls(int_to_words(value, length, w))
+        obj = cls(int_to_words(value, length, w))
+        obj._ival, obj._iw = value, w
+        return obj
 
     def to_int(self, w: int | None = None) -> int:
         w = word_bits() if w is None else w
+        if self._iw == w:
+            return self._ival
         if self._words is None and w == self._w:
-            return int.from_bytes(np.ascontiguousarray(self._limbs, dtype=np.uint32).tobytes(), "little")
-        return words_to_int(self.words, w)
+            v = int.from_bytes(np.ascontiguousarray(self._limbs, dtype=np.uint32).tobytes(), "little")
+        else:
+            v = words_to_int(self.words, w)
+        self._ival, self._iw = v, w
+        return v
 
     def normalized(self) -> "Natural":
         ws = self.words
