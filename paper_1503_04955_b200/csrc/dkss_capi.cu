@@ -762,12 +762,12 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
       }
     }
     // row phase as one persistent dependency-driven kernel: default for m = 32 two-level plans
-    // with a base case of at most 16 (2^24: 1.375 vs 1.389 ms); at 2^26 (b = 64) and for m = 16
-    // the three ticketed launches measured faster.  DKSS_DYN=1 forces it
-    // on, DKSS_NO_DYN=1 off.
+    // with a base case of 4 to 16 (2^24: 1.375 vs 1.389 ms; 2^22: 434 vs 443 us); at 2^26
+    // (b = 64), at 2^21 (b = 2: 289 vs 267 us) and for m = 16 the three ticketed launches
+    // measured faster.  DKSS_DYN=1 forces it on, DKSS_NO_DYN=1 off.
     const char* nd = getenv("DKSS_NO_DYN");
     const char* fd = getenv("DKSS_DYN");
-    const bool want_dyn = (fd && *fd && *fd != '0') || (m == 32 && P->base_len <= 16);
+    const bool want_dyn = (fd && *fd && *fd != '0') || (m == 32 && P->base_len >= 4 && P->base_len <= 16);
     if (!P->rows_cs && P->levels == 2 && kt.dyn && want_dyn && !(nd && *nd && *nd != '0') &&
         (1LL << P->log_top_mu) % kt.ne == 0) {
       CUCHK(cudaFuncSetAttribute((const void*)kt.dyn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kt.smem_dyn));
