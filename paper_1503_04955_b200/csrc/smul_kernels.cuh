@@ -442,6 +442,7 @@ struct SmulDecodeArgs {
   const uint32_t* x;  // [batch][n][KW] normalised coefficients (natural order)
   int log_n, KW;
   long long s;        // slice stride in bits
+  int s_log;          // log2(s) when s is a power of two (shifts instead of 64-bit divisions), else -1
 };
 
 // sum of the 32-bit windows of coefficients k*s landing on product limb t
@@ -449,9 +450,14 @@ struct SmulDecodeArgs {
 __device__ __forceinline__ unsigned long long smul_window_sum(const SmulDecodeArgs& D, int pidx, long long t) {
   const long long n = 1LL << D.log_n, K = 32LL * D.KW;
   const uint32_t* v = D.x + (long long)pidx * n * D.KW;
-  long long k0 = 32 * t - K + 1;
-  k0 = k0 <= 0 ? 0 : (k0 + D.s - 1) / D.s;
-  long long k1 = (32 * t + 31) / D.s;
+  long long k0 = 32 * t - K + 1, k1;
+  if (D.s_log >= 0) {
+    k0 = k0 <= 0 ? 0 : (k0 + D.s - 1) >> D.s_log;
+    k1 = (32 * t + 31) >> D.s_log;
+  } else {
+    k0 = k0 <= 0 ? 0 : (k0 + D.s - 1) / D.s;
+    k1 = (32 * t + 31) / D.s;
+  }
   if (k1 > n - 1) k1 = n - 1;
   unsigned long long S = 0;
   for (long long k = k0; k <= k1; ++k) {
