@@ -30,7 +30,7 @@ from .words import (Natural, ScratchArena, as_natural, current_arena, int_to_u32
                     word_bits, PYLONG_DIGIT_BITS)
 
 # The reference hands products below 2048 result bits to smul (bigmul/dkss.py:517,
-# 533-535); that rung is out of scope here, so such inputs run through DKSS on the GPU
+# 533-535); here dmul always measures DKSS, so such inputs run through DKSS on the GPU
 # with the plan for N = _MIN_PLAN_BITS (any input below 2^N fits a plan for N).
 _MIN_DKSS_BITS = 2048
 _MIN_PLAN_BITS = 1024

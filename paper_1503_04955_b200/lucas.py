@@ -7,8 +7,9 @@ scrambles it.  With ``multiplier="dmul"`` the whole loop runs on the device
 (``dkss_lucas_lehmer``): every square goes through the DKSS pipeline in squaring mode (one
 forward transform, pointwise squares, inverse, decode) and the reduction
 mod 2^p - 1 and the "- 2" run in one more kernel; the state never leaves the GPU between
-steps.  Other multiplier names are the reference's other rungs, which are out of scope
-here (dispatch.ALGORITHMS raises NotImplementedError for them).
+steps.  ``multiplier="smul"`` squares with the GPU Schoenhage-Strassen multiply and reduces
+on the host; the reference's other rungs are out of scope here (dispatch.ALGORITHMS raises
+NotImplementedError for them).
 """
 
 from __future__ import annotations
