@@ -221,3 +221,32 @@ def test_smul_digits_entry_point(cuda_ok):
     bad[5] |= 1 << 30  # a digit above 30 bits is rejected unless the caller vouches for it
     with pytest.raises(ValueError):
         dp.mul_digits(bad.ctypes.data, bad.size, bad.ctypes.data, bad.size, 30, nc)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("idx", range(3))
+def test_stage_pipeline_matches_reference_coefficients(cuda_ok, idx):
+    # _cyclic_coeff_product (bigmul/smul.py:256-271) composed from the device transforms:
+    # slices -> shuffle -> forward fft_eval (GPU) -> pointwise mod 2^K+1 -> shuffle ->
+    # inverse fft_eval (GPU) -> 2^-m; equals the reference's normalised coefficients
+    from paper_1503_04955_b200.words import bit_slices
+
+    e = _stage_sets()[idx]
+    p = SmulPlan(**e["plan"])
+    z = np.load(os.path.join(GOLD, "smul_stages.npz"))
+    t = e["tag"]
+    a = int.from_bytes(z[f"{t}_a"].tobytes(), "little")
+    b = int.from_bytes(z[f"{t}_b"].tobytes(), "little")
+    idxs = [int(bin(i)[2:].zfill(p.m)[::-1], 2) for i in range(p.n)]
+    mod = (1 << p.K) + 1
+    av, bv = bit_slices(a, p.s, p.n), bit_slices(b, p.s, p.n)
+    aw = [av[idxs[i]] for i in range(p.n)]
+    bw = [bv[idxs[i]] for i in range(p.n)]
+    fft_eval_fermat(aw, p)
+    fft_eval_fermat(bw, p)
+    cw = [x * y % mod for x, y in zip(aw, bw)]
+    cv = [cw[idxs[i]] for i in range(p.n)]
+    fft_eval_fermat(cv, p, inverse=True)
+    inv = pow(2, -p.m, mod)
+    got = [x * inv % mod for x in cv]
+    assert got == _elems(z[f"{t}_coeffs"], z[f"{t}_coeffs_top"], p.K)
