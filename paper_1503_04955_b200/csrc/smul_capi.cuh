@@ -11,7 +11,7 @@ struct smul_plan {
   int m = 0, K = 0, KW = 0, Q = 1, omega_exp = 0;
   long long prod_limbs = 0;
   int nlv_max = 1;  // most DIT levels one FFT pass runs in shared memory
-  size_t smem_fft = 0, smem_pw = 0;
+  size_t smem_pw = 0;  // pointwise kernel, warp-per-product form
   cudaStream_t stream = nullptr;
   int cap = 0;  // operands the workspace holds (a's and b's)
   long long cap_nc = 0;

@@ -21,7 +21,6 @@
 
 namespace dkss {
 
-constexpr int kSmulThreads = 256;
 
 struct SmulFftArgs {
   uint32_t* x;    // [npoly][n][KW]
