@@ -455,6 +455,22 @@ int launch_bottom(dkss_plan* P, uint32_t* a, const uint32_t* b, int npoly, int m
   return 0;
 }
 
+// carry resolution after a decode1-style kernel: one self-scanning kernel for products of at
+// most kSelfScanBlocks blocks (DKSS_NO_SELFSCAN=1: always the scan + apply pair)
+void launch_carry_tail(const DecodeArgs& A, int npoly, cudaStream_t s) {
+  static const bool off = [] {
+    const char* e = getenv("DKSS_NO_SELFSCAN");
+    return e && *e && *e != '0';
+  }();
+  const dim3 grid((unsigned)(A.blocks_per_poly * npoly));
+  if (!off && A.blocks_per_poly <= kSelfScanBlocks) {
+    launch_k(k_decode2s, grid, dim3(kDecThreads), 0, s, A);
+    return;
+  }
+  launch_k(k_decode_scan, dim3(npoly), dim3(kScanThreads), 0, s, A);
+  launch_k(k_decode2, grid, dim3(kDecThreads), 0, s, A);
+}
+
 int launch_decode(dkss_plan* P, const uint32_t* v, uint32_t* out, int npoly, cudaStream_t s,
                   const unsigned long long* sglob = nullptr) {
   DecodeArgs A{};
@@ -474,10 +490,8 @@ int launch_decode(dkss_plan* P, const uint32_t* v, uint32_t* out, int npoly, cud
   const int grid = A.blocks_per_poly * npoly;
   launch_k(k_decode1, dim3(grid), dim3(kDecThreads), 0, s, A);
   CUCHK(cudaGetLastError());
-  launch_k(k_decode_scan, dim3(npoly), dim3(kScanThreads), 0, s, A);
-  CUCHK(cudaGetLastError());
   mark(P, s, DKSS_K_DECODE1, 0, npoly * (P->poly_words * 4 + P->prod_limbs * 4));
-  launch_k(k_decode2, dim3(grid), dim3(kDecThreads), 0, s, A);
+  launch_carry_tail(A, npoly, s);
   CUCHK(cudaGetLastError());
   mark(P, s, DKSS_K_DECODE2, 0, npoly * 2LL * P->prod_limbs * 4);
   return 0;
@@ -870,8 +884,13 @@ int dkss_plan_get_info(const dkss_plan* P, dkss_plan_info* o) {
   o->product_limbs = P->prod_limbs;
   o->twiddles_per_fft = P->twiddles;
   o->ring_products = 3 * P->twiddles + 2LL * P->M;
-  o->launches_per_mul =
-      (P->rows_cs || P->dyn_grid) ? 1 + 1 + 1 + 3 : (P->levels > 0 ? 0 : 2) + P->levels + 1 + P->levels + 3;
+  {
+    const char* e = getenv("DKSS_NO_SELFSCAN");
+    const bool self = !(e && *e && *e != '0') && dec_blocks(P) <= kSelfScanBlocks;
+    const int dec = self ? 2 : 3;  // decode1 + (self-scanning apply | scan + apply)
+    o->launches_per_mul =
+        (P->rows_cs || P->dyn_grid) ? 1 + 1 + 1 + dec : (P->levels > 0 ? 0 : 2) + P->levels + 1 + P->levels + dec;
+  }
   o->workspace_bytes = (int64_t)P->ws_bytes;
   return DKSS_OK;
 }

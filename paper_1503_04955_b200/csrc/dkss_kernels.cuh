@@ -1236,16 +1236,11 @@ __global__ void __launch_bounds__(kScanThreads) k_decode_scan(DecodeArgs A) {
 }
 
 // phase 3: apply carries inside each block
-__global__ void __launch_bounds__(kDecThreads) k_decode2(DecodeArgs A) {
-  griddep_wait();  // PDL: predecessor grid complete, its writes visible
-  griddep_launch();
-  const int pidx = blockIdx.x / A.blocks_per_poly;
-  const int blk = blockIdx.x % A.blocks_per_poly;
+__device__ __forceinline__ void decode2_body(const DecodeArgs& A, int pidx, int blk, unsigned cin) {
   const long long t = (long long)blk * kDecThreads + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ unsigned s_wcin[kDecWarps];
   if (warp == 0) {
-    const unsigned cin = (A.bstat[(long long)pidx * A.blocks_per_poly + blk] >> 2) & 1u;
     const long long wi = ((long long)pidx * A.blocks_per_poly + blk) * kDecWarps + lane;
     const unsigned G = lane < kDecWarps ? A.gmask[wi] : 0u, P = lane < kDecWarps ? A.pmask[wi] : 0u;
     const unsigned long long a = (unsigned long long)(G | P), b = G;
@@ -1263,6 +1258,45 @@ __global__ void __launch_bounds__(kDecThreads) k_decode2(DecodeArgs A) {
   const unsigned long long carries = (a + b + s_wcin[warp]) ^ a ^ b;
   const unsigned c = (unsigned)((carries >> lane) & 1ull);
   A.out[(long long)pidx * A.nout + t] += c;
+}
+
+__global__ void __launch_bounds__(kDecThreads) k_decode2(DecodeArgs A) {
+  griddep_wait();  // PDL: predecessor grid complete, its writes visible
+  griddep_launch();
+  const int pidx = blockIdx.x / A.blocks_per_poly;
+  const int blk = blockIdx.x % A.blocks_per_poly;
+  decode2_body(A, pidx, blk, (A.bstat[(long long)pidx * A.blocks_per_poly + blk] >> 2) & 1u);
+}
+
+// phases 2 + 3 in one kernel for products of at most kSelfScanBlocks blocks: warp 0 of every
+// block composes the carry functions of the blocks before it (each lane a contiguous chunk,
+// then the (generate | propagate) + generate add across lanes) -- no scan launch.  Measured:
+// 2^20 (256 blocks) -2%, 2^22 (1024 blocks) +1%, so only up to 256 blocks
+constexpr int kSelfScanBlocks = 256;
+__global__ void __launch_bounds__(kDecThreads) k_decode2s(DecodeArgs A) {
+  griddep_wait();  // PDL: predecessor grid complete, its writes visible
+  griddep_launch();
+  const int pidx = blockIdx.x / A.blocks_per_poly;
+  const int blk = blockIdx.x % A.blocks_per_poly;
+  __shared__ unsigned s_cin;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const uint32_t* st = A.bstat + (long long)pidx * A.blocks_per_poly;
+    const int per = (blk + 31) / 32;
+    const int b0 = lane * per, b1 = min(blk, b0 + per);
+    unsigned f0 = 0, f1 = 1;  // identity: cout(cin = 0), cout(cin = 1)
+    for (int b = b0; b < b1; ++b) {
+      const unsigned sv = st[b];
+      const unsigned c0 = sv & 1u, c1 = (sv >> 1) & 1u;
+      f0 = f0 ? c1 : c0;
+      f1 = f1 ? c1 : c0;
+    }
+    const unsigned G = __ballot_sync(0xFFFFFFFFu, f0), P = __ballot_sync(0xFFFFFFFFu, f1 && !f0);
+    const unsigned long long a = (unsigned long long)(G | P), b = G;
+    if (lane == 0) s_cin = (unsigned)((a + b) >> 32) & 1u;  // carry out of all predecessors (product cin 0)
+  }
+  __syncthreads();
+  decode2_body(A, pidx, blk, s_cin);
 }
 
 // ---------------------------------------------------------------------------

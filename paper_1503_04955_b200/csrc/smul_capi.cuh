@@ -226,8 +226,7 @@ int run_smul(smul_plan* P, int batch, const uint32_t* a, const uint32_t* b, long
   D.s = P->s;
   D.s_log = (P->s & (P->s - 1)) ? -1 : ilog2i(P->s);
   launch_k(k_smul_decode1, dim3(A.blocks_per_poly * batch), dim3(kDecThreads), 0, s, A, D);
-  launch_k(k_decode_scan, dim3(batch), dim3(kScanThreads), 0, s, A);
-  launch_k(k_decode2, dim3(A.blocks_per_poly * batch), dim3(kDecThreads), 0, s, A);
+  launch_carry_tail(A, batch, s);
   CUCHK(cudaGetLastError());
   return 0;
 }
