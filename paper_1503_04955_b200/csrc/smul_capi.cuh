@@ -26,6 +26,9 @@ struct smul_plan {
 namespace {
 
 constexpr int kSmulPwWarps = 4;
+#ifndef DKSS_SMUL_WPP  // warps per product of the CTA-wide pointwise kernel (experiment override)
+#define DKSS_SMUL_WPP 4  // measured: 4 beats 8 by 1.4-2.7% from 2^22 up, equal at 2^20
+#endif
 constexpr size_t kSmulFftSmemMax = 96 * 1024;
 
 template <int Q>
@@ -36,9 +39,9 @@ int smul_set_attrs(smul_plan* P) {
   const int pw_max = kSmulPwWarps * (10 * 32 * Q + 8) * 4;
   CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, pw_max));
   CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pw_max));
-  CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q, 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q, DKSS_SMUL_WPP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (10 * 32 * Q + 8) * 4));
-  CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CUCHK(cudaFuncSetAttribute(k_smul_pointwise<Q, DKSS_SMUL_WPP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (10 * 32 * Q + 8) * 4));
   return 0;
 }
@@ -117,17 +120,18 @@ void smul_fft(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool inverse,
   }
 }
 
-// small K: a warp per product (4 per CTA); K >= 2080 (3+ limbs per lane): a CTA of 8 warps per product
+// small K: a warp per product (4 per CTA); K >= 2080 (3+ limbs per lane): DKSS_SMUL_WPP warps per product
 template <int Q>
 void smul_pw_q(smul_plan* P, const SmulPwArgs& A, cudaStream_t s) {
   const bool full = P->KW == 32 * Q;
   if (Q >= 3) {
-    const dim3 g((unsigned)std::min<long long>(A.count, 148LL * 8));
+    constexpr int W = DKSS_SMUL_WPP;
+    const dim3 g((unsigned)std::min<long long>(A.count, 148LL * 64 / W));
     const size_t sm = (size_t)(10 * P->KW + 8) * 4;
     if (full)
-      launch_k(k_smul_pointwise<Q, 8, true>, g, dim3(256), sm, s, A);
+      launch_k(k_smul_pointwise<Q, W, true>, g, dim3(32 * W), sm, s, A);
     else
-      launch_k(k_smul_pointwise<Q, 8, false>, g, dim3(256), sm, s, A);
+      launch_k(k_smul_pointwise<Q, W, false>, g, dim3(32 * W), sm, s, A);
     return;
   }
   const long long blocks = (A.count + kSmulPwWarps - 1) / kSmulPwWarps;
