@@ -90,7 +90,9 @@ void smul_fft_q(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool invers
   while (nlv > 3 && (P->n >> nlv) * npoly < min_ctas) --nlv;
   const int npass = (P->m + nlv - 1) / nlv;
   for (int i = 0, lv = 0; i < npass; ++i) {
-    const int nl = (P->m - lv + (npass - i) - 1) / (npass - i);
+    // the shorter passes first (2^18 -7%, 2^20 -6%): the first forward pass also builds its
+    // elements from the operand limbs
+    const int nl = (P->m - lv) / (npass - i);
     A.lv0 = lv;
     A.nlv = nl;
     lv += nl;
