@@ -79,12 +79,12 @@ void smul_fft_q(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool invers
   A.omega_fwd = P->omega_exp;
   A.inverse = inverse ? 1 : 0;
   // levels per pass: at most what shared memory and one warp per butterfly (<= 32 warps)
-  // allow, fewer while the launch has under 64 CTAs (measured: a level costs about one
-  // butterfly latency however many CTAs share it, so fewer passes beat covering all 148
-  // SMs -- 2^18 -10%, 2^20 -5% against a 148-CTA floor); then split the levels evenly
+  // allow, fewer while the launch has under 96 CTAs (measured with the shorter passes first:
+  // 2^20 65 us at 96, 68 at 64, 67 at 148; fewer, deeper passes beat covering all 148 SMs);
+  // then split the levels evenly
   static const long long min_ctas = [] {
     const char* e = getenv("DKSS_SMUL_MINCTA");  // experiment knob
-    return e ? atoll(e) : 64LL;
+    return e ? atoll(e) : 96LL;
   }();
   int nlv = P->nlv_max;
   while (nlv > 3 && (P->n >> nlv) * npoly < min_ctas) --nlv;
