@@ -59,14 +59,41 @@ typedef struct {
   int64_t twiddles_per_fft; /* (2m-1)(mu-1) summed over levels (bigmul/dkss.py:483-492) */
   int32_t launches_per_mul; /* kernels launched by one dkss_mul_device call */
   int64_t workspace_bytes;  /* device workspace currently held */
+  int64_t footprint_bytes;  /* device bytes one multiply of host operands holds: twiddle tables, two
+                               polynomials, operand staging, operands, product, decode scratch
+                               (the arena figure dmul reports, cf. bigmul/dkss.py:538-539) */
 } dkss_plan_info;
+
+/* Kernel-shape choices of a plan.  Zero-initialised options (or dkss_plan_create) pick the
+ * measured-fastest shape for the plan; the others exist for parity tests of every variant. */
+#define DKSS_ROWS_AUTO 0        /* per plan */
+#define DKSS_ROWS_LAUNCHES 1    /* row phase as three ticketed persistent launches */
+#define DKSS_ROWS_PERSISTENT 2  /* row phase as one dependency-driven kernel (k_rows_dyn) */
+#define DKSS_ROWS_CLUSTER 3     /* row phase as one thread-block-cluster kernel (k_rows) */
+#define DKSS_PASS_AUTO 0
+#define DKSS_PASS_CTA 1         /* column pass: one CTA per column tile */
+#define DKSS_PASS_WARP 2        /* column pass: warp per column */
+#define DKSS_PASS_SPLIT 3       /* column DFT kernel + elementwise twiddle kernel */
+typedef struct {
+  int32_t row_phase; /* DKSS_ROWS_*; ignored by plans that are not two-level */
+  int32_t pass_kind; /* DKSS_PASS_* */
+} dkss_plan_opts;
 
 /* plan lifetime -------------------------------------------------------------------- */
 int dkss_plan_create(const dkss_plan_desc* desc, int device, dkss_plan** out);
+int dkss_plan_create_ex(const dkss_plan_desc* desc, const dkss_plan_opts* opts, int device, dkss_plan** out);
 void dkss_plan_destroy(dkss_plan* plan);
 int dkss_plan_get_info(const dkss_plan* plan, dkss_plan_info* out);
 const char* dkss_last_error(void);
 int dkss_version(void);
+/* kernels this process has launched through the library so far (a CUDA-graph replay counts
+ * each of its kernel nodes); instrumentation for benchmarks (bench.py "gpu_launches") */
+int64_t dkss_kernel_launches(void);
+/* device bytes one multiply of host operands holds for a plan of this shape (twiddle tables,
+ * the two polynomials, operand staging, operands, product, decode scratch): the memory figure
+ * dmul records in the caller's ScratchArena (cf. bigmul/dkss.py:538-539).  Needs no GPU; -1 for a
+ * bad shape. */
+int64_t dkss_footprint_bytes(int64_t N, int32_t M, int32_t m, int32_t L);
 
 /* dmul (bigmul/dkss.py:520-548) for operands below 2^N: c = a * b.
  * Host buffers; na, nb <= operand_limbs; nc limbs are written (zero padded); the call

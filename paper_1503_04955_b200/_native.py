@@ -19,7 +19,8 @@ LIB_PATH = os.environ.get("DKSS_LIB") or os.path.join(HERE, "_lib", "libdkss.so"
 
 # every symbol include/dkss.h declares (checked by tests/test_native_abi.py)
 EXPORTS = (
-    "dkss_plan_create", "dkss_plan_destroy", "dkss_plan_get_info", "dkss_last_error", "dkss_version",
+    "dkss_plan_create", "dkss_plan_create_ex", "dkss_plan_destroy", "dkss_plan_get_info", "dkss_last_error",
+    "dkss_version", "dkss_kernel_launches", "dkss_footprint_bytes",
     "dkss_mul", "dkss_mul_digits", "dkss_mul_batch_digits", "dkss_mul_batch", "dkss_mul_device", "dkss_profile_device",
     "dkss_encode_host", "dkss_fft_host", "dkss_rmul_host", "dkss_decode_host",
     "dkss_fs_layout_get", "dkss_fs_columns_fwd", "dkss_fs_rows", "dkss_fs_columns_inv",
@@ -32,6 +33,9 @@ EXPORTS = (
 
 DKSS_OK, DKSS_EINVAL, DKSS_ECUDA, DKSS_ERANGE, DKSS_ENOMEM = 0, -1, -2, -3, -4
 DKSS_DIGITS_TRUSTED = 0x100  # digit_bits flag: digits already known to fit (include/dkss.h)
+# dkss_plan_opts values (include/dkss.h)
+ROW_PHASES = {"auto": 0, "launches": 1, "persistent": 2, "cluster": 3}
+PASS_KINDS = {"auto": 0, "cta": 1, "warp": 2, "split": 3}
 
 
 class NativeUnavailable(RuntimeError):
@@ -56,7 +60,11 @@ class PlanInfo(ctypes.Structure):
                 ("poly_bytes", ctypes.c_int64), ("operand_limbs", ctypes.c_int64),
                 ("product_limbs", ctypes.c_int64), ("ring_products", ctypes.c_int64),
                 ("twiddles_per_fft", ctypes.c_int64), ("launches_per_mul", ctypes.c_int32),
-                ("workspace_bytes", ctypes.c_int64)]
+                ("workspace_bytes", ctypes.c_int64), ("footprint_bytes", ctypes.c_int64)]
+
+
+class PlanOpts(ctypes.Structure):
+    _fields_ = [("row_phase", ctypes.c_int32), ("pass_kind", ctypes.c_int32)]
 
 
 class FsLayout(ctypes.Structure):
@@ -88,6 +96,12 @@ def load(path: str = LIB_PATH):
             raise NativeUnavailable(f"cannot load {path}: {e}") from e
         vp = ctypes.c_void_p
         L.dkss_plan_create.argtypes = [ctypes.POINTER(PlanDesc), ctypes.c_int, ctypes.POINTER(vp)]
+        L.dkss_plan_create_ex.argtypes = [ctypes.POINTER(PlanDesc), ctypes.POINTER(PlanOpts), ctypes.c_int,
+                                          ctypes.POINTER(vp)]
+        L.dkss_kernel_launches.restype = ctypes.c_int64
+        L.dkss_kernel_launches.argtypes = []
+        L.dkss_footprint_bytes.restype = ctypes.c_int64
+        L.dkss_footprint_bytes.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
         L.dkss_plan_destroy.argtypes = [vp]
         L.dkss_plan_destroy.restype = None
         L.dkss_plan_get_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]
@@ -150,7 +164,10 @@ def _check(rc: int):
 class DevicePlan:
     """A plan uploaded to one GPU (twiddle table in Montgomery form + workspace)."""
 
-    def __init__(self, N: int, M: int, m: int, u: int, p: int, rho_powers, device: int = 0):
+    def __init__(self, N: int, M: int, m: int, u: int, p: int, rho_powers, device: int = 0,
+                 row_phase: str = "auto", pass_kind: str = "auto"):
+        """row_phase / pass_kind pick a kernel shape (include/dkss.h dkss_plan_opts); "auto" is the
+        measured-fastest one for the plan, the others exist so every variant can be tested."""
         lib = load()
         self.N, self.M, self.m, self.u, self.p, self.device = N, M, m, u, p, device
         self.L = L = -(-p.bit_length() // 32)
@@ -159,7 +176,8 @@ class DevicePlan:
         rho_l = np.frombuffer(raw, dtype=np.uint32).copy()
         desc = PlanDesc(N, M, m, u, L, _ptr(p_l), _ptr(rho_l))
         h = ctypes.c_void_p()
-        _check(lib.dkss_plan_create(ctypes.byref(desc), device, ctypes.byref(h)))
+        opts = PlanOpts(ROW_PHASES[row_phase], PASS_KINDS[pass_kind])
+        _check(lib.dkss_plan_create_ex(ctypes.byref(desc), ctypes.byref(opts), device, ctypes.byref(h)))
         self._h = h
         self._lib = lib
         self.info = self.get_info()
@@ -346,3 +364,18 @@ class SmulDevicePlan:
     def fft(self, x: np.ndarray, top: np.ndarray, inverse: bool = False):
         """fft_eval in place: x uint32[n][K/32], top uint32[n]; shuffled in, natural out."""
         _check(self._lib.smul_fft_host(self._h, _ptr(x), _ptr(top), 1 if inverse else 0))
+
+
+def kernel_launches() -> int:
+    """Kernels launched through libdkss by this process so far (graph replays count each kernel
+    node; include/dkss.h dkss_kernel_launches)."""
+    return int(load().dkss_kernel_launches())
+
+
+def footprint_bytes(N: int, M: int, m: int, L: int) -> int:
+    """Device bytes one multiply of host operands holds for a plan of this shape
+    (include/dkss.h dkss_footprint_bytes; no GPU needed)."""
+    v = int(load().dkss_footprint_bytes(N, M, m, L))
+    if v < 0:
+        raise ValueError("bad plan shape")
+    return v

@@ -27,8 +27,10 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# experiment libraries also read the DKSS_* environment switches (csrc/dkss_capi.cu DKSS_KNOB);
+# the product library reads none
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE,
-         *os.environ.get("DKSS_EXTRA_FLAGS", "").split()]
+         *(["-DDKSS_EXPERIMENTS"] if VARIANT else []), *os.environ.get("DKSS_EXTRA_FLAGS", "").split()]
 
 INSTANCES = [(m, L) for m in (8, 16, 32) for L in (2, 3, 4, 5, 6)]
 

@@ -2,6 +2,7 @@
 // See include/dkss.h for the contract and DESIGN.md for the kernel/roofline story.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdarg>
 #include <cstdlib>
 #include <cstdio>
@@ -39,6 +40,107 @@ int fail(int code, const char* fmt, ...) {
     cudaError_t _e = (expr);                                                                     \
     if (_e != cudaSuccess) return fail(DKSS_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
   } while (0)
+
+// Experiment switches (timing studies, kernel A/B runs) exist only in DKSS_VARIANT builds
+// (paper_1503_04955_b200/build.py defines DKSS_EXPERIMENTS there); the product library reads
+// no environment variables.
+#ifdef DKSS_EXPERIMENTS
+#define DKSS_KNOB(name) getenv(name)
+#else
+#define DKSS_KNOB(name) ((const char*)nullptr)
+#endif
+
+bool knob_on(const char* v) { return v && *v && *v != '0'; }
+
+// kernels this library launched (graph replays add their kernel nodes), for dkss_kernel_launches()
+std::atomic<long long> g_launches{0};
+// set while a stream of this thread is being captured into a graph: launches then become graph
+// nodes and are counted when the graph is replayed
+thread_local bool tl_capturing = false;
+inline void count_launch() {
+  if (!tl_capturing) g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+struct CaptureScope {
+  CaptureScope() { tl_capturing = true; }
+  ~CaptureScope() { tl_capturing = false; }
+};
+
+int graph_kernel_nodes(cudaGraph_t g) {
+  size_t n = 0;
+  if (cudaGraphGetNodes(g, nullptr, &n) != cudaSuccess) return 0;
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (n && cudaGraphGetNodes(g, nodes.data(), &n) != cudaSuccess) return 0;
+  int k = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++k;
+  }
+  return k;
+}
+
+// Executable graphs keyed by K, least recently used evicted beyond `cap`.  Each entry keeps an
+// event recorded after its last replay, so an evicted graph is destroyed only once its last
+// replay has finished.
+template <class K>
+struct GraphLru {
+  struct Ent {
+    cudaGraphExec_t exec = nullptr;
+    cudaEvent_t done = nullptr;
+    int kernels = 0;
+    unsigned long long stamp = 0;
+  };
+  explicit GraphLru(size_t cap_) : cap(cap_) {}
+  std::map<K, Ent> m;
+  unsigned long long clock = 0;
+  size_t cap;
+  Ent* find(const K& k) {
+    auto it = m.find(k);
+    if (it == m.end()) return nullptr;
+    it->second.stamp = ++clock;
+    return &it->second;
+  }
+  static void destroy(Ent& e) {
+    if (e.done) {
+      cudaEventSynchronize(e.done);
+      cudaEventDestroy(e.done);
+    }
+    if (e.exec) cudaGraphExecDestroy(e.exec);
+  }
+  // instantiate g (consumed) under key k; returns nullptr and sets *err on failure
+  Ent* put(const K& k, cudaGraph_t g, cudaError_t* err) {
+    while (m.size() >= cap) {
+      auto old = m.begin();
+      for (auto it = m.begin(); it != m.end(); ++it)
+        if (it->second.stamp < old->second.stamp) old = it;
+      destroy(old->second);
+      m.erase(old);
+    }
+    Ent e;
+    e.kernels = graph_kernel_nodes(g);
+    cudaError_t r = cudaGraphInstantiate(&e.exec, g, 0);
+    cudaGraphDestroy(g);
+    if (r == cudaSuccess) r = cudaEventCreateWithFlags(&e.done, cudaEventDisableTiming);
+    if (r != cudaSuccess) {
+      if (e.exec) cudaGraphExecDestroy(e.exec);
+      *err = r;
+      return nullptr;
+    }
+    e.stamp = ++clock;
+    return &(m[k] = e);
+  }
+  cudaError_t launch(Ent* e, cudaStream_t s) {
+    cudaError_t r = cudaGraphLaunch(e->exec, s);
+    if (r == cudaSuccess) r = cudaEventRecord(e->done, s);
+    if (r == cudaSuccess) g_launches.fetch_add(e->kernels, std::memory_order_relaxed);
+    return r;
+  }
+  void clear() {
+    for (auto& kv : m) destroy(kv.second);
+    m.clear();
+  }
+  size_t size() const { return m.size(); }
+};
 
 int ilog2i(long long v) {
   int k = 0;
@@ -114,6 +216,10 @@ struct GraphKey {
   }
 };
 
+// device-pointer graphs kept per plan: a caller cycling through more buffer triples than this
+// re-captures (about 20 us for a two-level plan) instead of growing the cache without bound
+constexpr size_t kGraphCacheCap = 16;
+
 struct dkss_plan {
   int device = 0;
   long long N = 0;
@@ -152,9 +258,11 @@ struct dkss_plan {
   size_t h_pin_words = 0;
   size_t ws_bytes = 0;
   cudaStream_t stream = nullptr;
-  std::map<GraphKey, cudaGraphExec_t> graphs;
-  std::map<std::pair<long long, int>, cudaGraphExec_t> ll_graphs;  // (p, iterations per graph)
-  std::map<std::tuple<int, bool, int>, cudaGraphExec_t> dgraphs;   // host digits path: (batch, square, bits)
+  // replayed multiplies: device-pointer entry (keyed by the caller's buffers), Lucas-Lehmer
+  // steps (p, iterations per graph), host digits path (batch, square, digit bits)
+  GraphLru<GraphKey> graphs{kGraphCacheCap};
+  GraphLru<std::pair<long long, int>> ll_graphs{8};
+  GraphLru<std::tuple<int, bool, int>> dgraphs{8};
   std::mutex mu;
   struct Prof {
     static constexpr int kMax = 64;
@@ -179,11 +287,8 @@ void free_ws(dkss_plan* P) {
   cudaFree(P->d_dyn);
   P->d_dyn = nullptr;
   P->d_poly = P->d_ops = P->d_prod = P->d_gmask = P->d_pmask = P->d_bstat = nullptr;
-  for (auto& kv : P->graphs) cudaGraphExecDestroy(kv.second);
   P->graphs.clear();
-  for (auto& kv : P->ll_graphs) cudaGraphExecDestroy(kv.second);
   P->ll_graphs.clear();
-  for (auto& kv : P->dgraphs) cudaGraphExecDestroy(kv.second);
   P->dgraphs.clear();
   P->cap_batch = 0;
   P->ws_bytes = 0;
@@ -210,8 +315,7 @@ int ensure_ws(dkss_plan* P, int batch) {
 
 int ensure_pin(dkss_plan* P, size_t words) {
   if (words <= P->h_pin_words) return 0;
-  for (auto& kv : P->dgraphs) cudaGraphExecDestroy(kv.second);  // they copy to/from h_pin
-  P->dgraphs.clear();
+  P->dgraphs.clear();  // they copy to/from h_pin
   if (P->h_pin) cudaFreeHost(P->h_pin);
   P->h_pin = nullptr;
   CUCHK(cudaMallocHost(&P->h_pin, words * 4));
@@ -244,8 +348,7 @@ size_t smem_two(const dkss_plan* P) { return P->kt.smem_bot; }
 // before touching their predecessor's output); DKSS_NO_PDL=1 turns it off
 bool pdl_enabled() {
   static const bool on = [] {
-    const char* e = getenv("DKSS_NO_PDL");
-    return !(e && *e && *e != '0');
+    return !knob_on(DKSS_KNOB("DKSS_NO_PDL"));
   }();
   return on;
 }
@@ -263,6 +366,7 @@ void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStrea
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, k, args...);
+  count_launch();
 }
 
 // --- launch helpers (all stream-ordered) ---------------------------------------------
@@ -361,7 +465,7 @@ int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s, c
     // auto mode: the first level (fused encode) runs the CTA-wide kernel, deeper levels may use
     // warp-per-column (batch 1024 x 2^18: forward 6.35 -> 5.95 ms)
     int kind = (lv == 0 && ops_a && !P->pass_mode) ? 1 : pass_kind(P, cols);
-    if (const char* fk = getenv("DKSS_FWD_KINDS")) {  // experiment: comma-separated kind per level
+    if (const char* fk = DKSS_KNOB("DKSS_FWD_KINDS")) {  // experiment: comma-separated kind per level
       int lvl = 0;
       for (const char* c = fk; *c; ++c) {
         if (*c == ',') ++lvl;
@@ -458,10 +562,7 @@ int launch_bottom(dkss_plan* P, uint32_t* a, const uint32_t* b, int npoly, int m
 // carry resolution after a decode1-style kernel: one self-scanning kernel for products of at
 // most kSelfScanBlocks blocks (DKSS_NO_SELFSCAN=1: always the scan + apply pair)
 void launch_carry_tail(const DecodeArgs& A, int npoly, cudaStream_t s) {
-  static const bool off = [] {
-    const char* e = getenv("DKSS_NO_SELFSCAN");
-    return e && *e && *e != '0';
-  }();
+  static const bool off = knob_on(DKSS_KNOB("DKSS_NO_SELFSCAN"));
   const dim3 grid((unsigned)(A.blocks_per_poly * npoly));
   if (!off && A.blocks_per_poly <= kSelfScanBlocks) {
     launch_k(k_decode2s, grid, dim3(kDecThreads), 0, s, A);
@@ -521,6 +622,7 @@ int launch_rows(dkss_plan* P, uint32_t* a, const uint32_t* b, int batch, bool sq
   cfg.attrs = at;
   cfg.numAttrs = 2;
   CUCHK(cudaLaunchKernelEx(&cfg, P->rows_fn, R, P->mc));
+  count_launch();
   const long long lt1 = level_twiddles(P, 1);
   mark(P, s, DKSS_K_ROWS, rp_work(P, (sq ? 2 : 3) * batch * lt1 + 2LL * P->M * batch),
        (sq ? 2LL : 3LL) * batch * P->poly_words * 4);
@@ -583,11 +685,15 @@ int run_mul(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, long 
     if ((rc = launch_encode(P, a, nl, pa, batch, s))) return rc;
     if (!sq && (rc = launch_encode(P, b, nl, pb, batch, s))) return rc;
   }
+#ifdef DKSS_EXPERIMENTS
   // DKSS_EXP_SKIP (timing experiments only, wrong products): bit 0 bottom, 1 inverse, 2 decode
   static const int skip = [] {
     const char* e = getenv("DKSS_EXP_SKIP");
     return e ? atoi(e) : 0;
   }();
+#else
+  constexpr int skip = 0;
+#endif
   if (!(skip & 1) && (rc = launch_bottom(P, pa, pb, batch, 1, P->levels == 0, s))) return rc;
   if (!(skip & 2) && (rc = launch_inv_levels(P, pa, batch, true, s))) return rc;
   if (!(skip & 4) && (rc = launch_decode(P, pa, prod, batch, s))) return rc;
@@ -605,6 +711,8 @@ int check_operand(const dkss_plan* P, const uint32_t* a, size_t na) {
   return 0;
 }
 
+int plan_init(dkss_plan* P, const dkss_plan_desc* d, const dkss_plan_opts& opts, const KTable& kt, int device);
+
 }  // namespace
 
 // =====================================================================================
@@ -612,9 +720,29 @@ extern "C" {
 
 int dkss_version(void) { return 1; }
 
+int64_t dkss_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int64_t dkss_footprint_bytes(int64_t N, int32_t M, int32_t m, int32_t L) {
+  if (N < 1 || M < m || m < 2 || L < 2) return -1;
+  // what a batch-1 multiply through dkss_mul_digits holds on the device: plan_init's tables
+  // (d_tw, d_twr, d_twr_s), ensure_ws(P, 1), the digits staging of run_digits_graph (30-bit digits)
+  const long long op = (N + 31) / 32, prod = (2 * N + 31) / 32, poly_b = 2LL * M * m * L * 4;
+  const long long blocks = (prod + kDecThreads - 1) / kDecThreads;
+  const long long tables = (long long)(M / m) * m * L * 4 * (1 + 2 + 2);
+  const long long ws = 2 * poly_b + 2 * op * 4 + prod * 4 + blocks * kDecWarps * 8 + blocks * 4 +
+                       (4 + 2LL * 2 * m) * 4 + 2LL * kTickSlots * 4;
+  const long long stage = 4 * (2 * 3 + 2 * ((N + 29) / 30));
+  return tables + ws + stage;
+}
+
 const char* dkss_last_error(void) { return g_err.c_str(); }
 
 int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
+  return dkss_plan_create_ex(d, nullptr, device, out);
+}
+
+int dkss_plan_create_ex(const dkss_plan_desc* d, const dkss_plan_opts* o, int device, dkss_plan** out) {
+  const dkss_plan_opts opts = o ? *o : dkss_plan_opts{};
   if (!d || !out || !d->p || !d->rho_powers) return fail(DKSS_EINVAL, "null argument");
   *out = nullptr;
   const int M = d->M, m = d->m, L = d->L;
@@ -623,8 +751,25 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
   if (d->p[L - 1] == 0 || !(d->p[0] & 1)) return fail(DKSS_EINVAL, "p must be odd with exactly L=%d limbs", L);
   KTable kt;
   if (!lookup(m, L, &kt)) return fail(DKSS_EINVAL, "no kernels for m=%d, L=%d (m in {8,16,32})", m, L);
+  if (opts.row_phase < DKSS_ROWS_AUTO || opts.row_phase > DKSS_ROWS_CLUSTER || opts.pass_kind < DKSS_PASS_AUTO ||
+      opts.pass_kind > DKSS_PASS_SPLIT)
+    return fail(DKSS_EINVAL, "bad plan options (row_phase %d, pass_kind %d)", opts.row_phase, opts.pass_kind);
   CUCHK(cudaSetDevice(device));
   dkss_plan* P = new dkss_plan();
+  const int rc = plan_init(P, d, opts, kt, device);
+  if (rc) {
+    dkss_plan_destroy(P);  // every partially built resource is released on the error paths
+    return rc;
+  }
+  *out = P;
+  return DKSS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+int plan_init(dkss_plan* P, const dkss_plan_desc* d, const dkss_plan_opts& opts, const KTable& kt, int device) {
+  const int M = d->M, m = d->m, L = d->L;
   P->device = device;
   P->N = d->N;
   P->M = M;
@@ -666,8 +811,7 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
   {
     bool pr = L >= 2 && p[0] == 1u;
     for (int i = 1; i + 1 < L; ++i) pr = pr && p[i] == 0u;
-    const char* np = getenv("DKSS_NO_PROTH");
-    P->mc.proth = (pr && !(np && *np && *np != '0')) ? 1u : 0u;
+    P->mc.proth = (pr && !knob_on(DKSS_KNOB("DKSS_NO_PROTH"))) ? 1u : 0u;
   }
   {
     // qbias = p * 2^(32L + 5) in 2L+1 limbs (pointwise bias removal, ring_mul BiasFromY)
@@ -709,14 +853,10 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
     CUCHK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, kt.fwd, kt.nt, kt.smem_pass));
     CUCHK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_i, kt.inv, kt.nt, kt.smem_pass));
     CUCHK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, kt.bottom, kt.nt, kt.smem_bot));
-    if (occ_f < 1 || occ_i < 1 || occ_b < 1) {
-      delete P;
-      return fail(DKSS_EINVAL, "kernels for m=%d L=%d do not fit an SM", m, L);
-    }
+    if (occ_f < 1 || occ_i < 1 || occ_b < 1) return fail(DKSS_EINVAL, "kernels for m=%d L=%d do not fit an SM", m, L);
     P->grid_pass = sms * std::min(occ_f, occ_i);
     P->grid_bot = sms * occ_b;
-    const char* nowarp = getenv("DKSS_NO_WARP_PASS");
-    if (kt.fwd_w && !(nowarp && *nowarp == '1')) {
+    if (kt.fwd_w && !knob_on(DKSS_KNOB("DKSS_NO_WARP_PASS"))) {
       int ofw = 0, oiw = 0;
       CUCHK(cudaFuncSetAttribute((const void*)kt.fwd_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kt.smem_fwd_w));
       CUCHK(cudaFuncSetAttribute((const void*)kt.inv_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kt.smem_inv_w));
@@ -738,17 +878,15 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
       CUCHK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ot, kt.tw, 256, 0));
       P->grid_tw = sms * std::max(ot, 1);
     }
-    const char* pm = getenv("DKSS_PASS_MODE");
-    if (pm) P->pass_mode = atoi(pm);
+    P->pass_mode = opts.pass_kind;
     // row phase in one cluster kernel: two column levels, base length b = cluster size.
-    // Opt-in (DKSS_ROWS=1): measured slower than the three persistent launches it replaces
+    // Opt-in (DKSS_ROWS_CLUSTER): measured slower than the three persistent launches it replaces
     // -- second-level column 0 has no twiddles, so one CTA of every
     // cluster idles through both level-1 phases, and the cluster barriers keep the CTAs in
     // lockstep where the persistent kernels overlap tiles
-    const char* nr = getenv("DKSS_ROWS");
     const int b = P->base_len;
     const int ri = b == 2 ? 1 : b == 4 ? 2 : b == 8 ? 3 : b == 16 ? 4 : 0;
-    if (P->levels == 2 && ri && kt.rows[ri] && nr && *nr && *nr != '0') {
+    if (P->levels == 2 && ri && kt.rows[ri] && opts.row_phase == DKSS_ROWS_CLUSTER) {
       auto fn = kt.rows[ri];
       bool ok = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kt.smem_rows) ==
                 cudaSuccess;
@@ -778,11 +916,10 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
     // row phase as one persistent dependency-driven kernel: default for m = 32 two-level plans
     // with a base case of 4 to 16 (2^24: 1.375 vs 1.389 ms; 2^22: 434 vs 443 us); at 2^26
     // (b = 64), at 2^21 (b = 2: 289 vs 267 us) and for m = 16 the three ticketed launches
-    // measured faster.  DKSS_DYN=1 forces it on, DKSS_NO_DYN=1 off.
-    const char* nd = getenv("DKSS_NO_DYN");
-    const char* fd = getenv("DKSS_DYN");
-    const bool want_dyn = (fd && *fd && *fd != '0') || (m == 32 && P->base_len >= 4 && P->base_len <= 16);
-    if (!P->rows_cs && P->levels == 2 && kt.dyn && want_dyn && !(nd && *nd && *nd != '0') &&
+    // measured faster.  DKSS_ROWS_PERSISTENT forces it on, DKSS_ROWS_LAUNCHES off.
+    const bool want_dyn = opts.row_phase == DKSS_ROWS_PERSISTENT ||
+                          (opts.row_phase == DKSS_ROWS_AUTO && m == 32 && P->base_len >= 4 && P->base_len <= 16);
+    if (!P->rows_cs && P->levels == 2 && kt.dyn && want_dyn &&
         (1LL << P->log_top_mu) % kt.ne == 0) {
       CUCHK(cudaFuncSetAttribute((const void*)kt.dyn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kt.smem_dyn));
       int od = 0;
@@ -809,8 +946,7 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
   }
   CUCHK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
   {
-    const char* nt = getenv("DKSS_NO_DYNTILES");
-    P->dyn_tiles = !(nt && *nt && *nt != '0');
+    P->dyn_tiles = !knob_on(DKSS_KNOB("DKSS_NO_DYNTILES"));
     CUCHK(cudaMalloc(&P->d_tick, 2 * kTickSlots * sizeof(unsigned)));
     CUCHK(cudaMemset(P->d_tick, 0, 2 * kTickSlots * sizeof(unsigned)));
   }
@@ -819,12 +955,14 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
   cudaError_t e = cudaMalloc(&P->d_tw, tw_words * 4);
   if (e == cudaSuccess) e = cudaMemcpy(P->d_tw, d->rho_powers, tw_words * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
+    count_launch();
     kt.mscale<<<(int)std::min<size_t>((tw_words / L + 255) / 256, 4096), 256, 0, P->stream>>>(P->d_tw, tw_words / L, 0,
                                                                                                P->mc);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaMalloc(&P->d_twr, (size_t)(M / m) * 2 * m * L * 4);
   if (e == cudaSuccess) {
+    count_launch();
     kt.build_twr<<<(int)std::min<size_t>(((size_t)(M / m) * m + 255) / 256, 4096), 256, 0, P->stream>>>(
         P->d_tw, P->d_twr, (long long)(M / m), m, P->mc);
     e = cudaGetLastError();
@@ -835,25 +973,26 @@ int dkss_plan_create(const dkss_plan_desc* d, int device, dkss_plan** out) {
   if (e == cudaSuccess) e = cudaMalloc(&tw_s, tw_words * 4);
   if (e == cudaSuccess) e = cudaMemcpyAsync(tw_s, P->d_tw, tw_words * 4, cudaMemcpyDeviceToDevice, P->stream);
   if (e == cudaSuccess) {
+    count_launch();
     kt.mscale<<<(int)std::min<size_t>((tw_words / L + 255) / 256, 4096), 256, 0, P->stream>>>(tw_s, tw_words / L, 2,
                                                                                                P->mc);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaMalloc(&P->d_twr_s, (size_t)(M / m) * 2 * m * L * 4);
   if (e == cudaSuccess) {
+    count_launch();
     kt.build_twr<<<(int)std::min<size_t>(((size_t)(M / m) * m + 255) / 256, 4096), 256, 0, P->stream>>>(
         tw_s, P->d_twr_s, (long long)(M / m), m, P->mc);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(P->stream);
   cudaFree(tw_s);
-  if (e != cudaSuccess) {
-    dkss_plan_destroy(P);
-    return fail(DKSS_ECUDA, "plan upload failed: %s", cudaGetErrorString(e));
-  }
-  *out = P;
-  return DKSS_OK;
+  if (e != cudaSuccess) return fail(DKSS_ECUDA, "plan upload failed: %s", cudaGetErrorString(e));
+  return 0;
 }
+}  // namespace
+
+extern "C" {
 
 void dkss_plan_destroy(dkss_plan* P) {
   if (!P) return;
@@ -885,13 +1024,13 @@ int dkss_plan_get_info(const dkss_plan* P, dkss_plan_info* o) {
   o->twiddles_per_fft = P->twiddles;
   o->ring_products = 3 * P->twiddles + 2LL * P->M;
   {
-    const char* e = getenv("DKSS_NO_SELFSCAN");
-    const bool self = !(e && *e && *e != '0') && dec_blocks(P) <= kSelfScanBlocks;
+    const bool self = !knob_on(DKSS_KNOB("DKSS_NO_SELFSCAN")) && dec_blocks(P) <= kSelfScanBlocks;
     const int dec = self ? 2 : 3;  // decode1 + (self-scanning apply | scan + apply)
     o->launches_per_mul =
         (P->rows_cs || P->dyn_grid) ? 1 + 1 + 1 + dec : (P->levels > 0 ? 0 : 2) + P->levels + 1 + P->levels + dec;
   }
   o->workspace_bytes = (int64_t)P->ws_bytes;
+  o->footprint_bytes = dkss_footprint_bytes(P->N, P->M, P->m, P->L);
   return DKSS_OK;
 }
 
@@ -904,12 +1043,15 @@ int launch_graph(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, 
   int rc;
   if ((rc = ensure_ws(P, batch))) return rc;
   GraphKey key{batch, a, b, c, nl, nc};
-  auto it = P->graphs.find(key);
-  if (it == P->graphs.end()) {
+  auto* ent = P->graphs.find(key);
+  if (!ent) {
     cudaStream_t cap;
     CUCHK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     CUCHK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-    rc = run_mul(P, batch, a, b, (long long)nl, P->d_prod, cap);
+    {
+      CaptureScope cs;
+      rc = run_mul(P, batch, a, b, (long long)nl, P->d_prod, cap);
+    }
     if (!rc && c != P->d_prod) {
       if ((long long)nc == P->prod_limbs) {
         cudaMemcpyAsync(c, P->d_prod, (size_t)batch * P->prod_limbs * 4, cudaMemcpyDeviceToDevice, cap);
@@ -922,15 +1064,14 @@ int launch_graph(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, 
     cudaGraph_t g;
     cudaError_t e = cudaStreamEndCapture(cap, &g);
     cudaStreamDestroy(cap);
-    if (rc) return rc;
+    if (rc) {
+      if (e == cudaSuccess) cudaGraphDestroy(g);
+      return rc;
+    }
     if (e != cudaSuccess) return fail(DKSS_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
-    cudaGraphExec_t ge;
-    e = cudaGraphInstantiate(&ge, g, 0);
-    cudaGraphDestroy(g);
-    if (e != cudaSuccess) return fail(DKSS_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
-    it = P->graphs.emplace(key, ge).first;
+    if (!(ent = P->graphs.put(key, g, &e))) return fail(DKSS_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
   }
-  CUCHK(cudaGraphLaunch(it->second, s));
+  CUCHK(P->graphs.launch(ent, s));
   return 0;
 }
 }  // namespace
@@ -1022,8 +1163,7 @@ struct HostTimer {
   char buf[512];
   int n = 0;
   HostTimer() {
-    const char* e = getenv("DKSS_HOST_TIMING");
-    on = e && *e && *e != '0';
+    on = knob_on(DKSS_KNOB("DKSS_HOST_TIMING"));
     t0 = last = std::chrono::steady_clock::now();
     buf[0] = 0;
   }
@@ -1097,7 +1237,6 @@ int run_digits_graph(dkss_plan* P, int batch, bool sq, int nops, const uint32_t*
   int rc;
   if ((rc = ensure_pin(P, std::max(cap, prw)))) return rc;
   if (cap > P->stage_words) {
-    for (auto& kv : P->dgraphs) cudaGraphExecDestroy(kv.second);
     P->dgraphs.clear();
     cudaFree(P->d_stage);
     P->d_stage = nullptr;
@@ -1105,33 +1244,35 @@ int run_digits_graph(dkss_plan* P, int batch, bool sq, int nops, const uint32_t*
     P->stage_words = cap;
   }
   auto key = std::make_tuple(batch, sq, digit_bits);
-  auto it = P->dgraphs.find(key);
-  if (it == P->dgraphs.end()) {
+  auto* ent = P->dgraphs.find(key);
+  if (!ent) {
     cudaStream_t cap_s;
     CUCHK(cudaStreamCreateWithFlags(&cap_s, cudaStreamNonBlocking));
     CUCHK(cudaStreamBeginCapture(cap_s, cudaStreamCaptureModeThreadLocal));
-    cudaMemcpyAsync(P->d_stage, P->h_pin, cap * 4, cudaMemcpyHostToDevice, cap_s);
-    RepackArgs R{};
-    R.stage = P->d_stage + head;
-    R.off = reinterpret_cast<const long long*>(P->d_stage);
-    R.dst = P->d_ops;
-    R.ndst = P->op_limbs;
-    R.sbits = digit_bits;
-    const int gx = (int)std::max<long long>(1, std::min<long long>((P->op_limbs + 255) / 256, 1184 / nops + 1));
-    launch_k(k_repack_bits, dim3(gx, nops), dim3(256), 0, cap_s, R);
-    const uint32_t* bo = sq ? nullptr : P->d_ops + (size_t)batch * P->op_limbs;
-    rc = run_mul(P, batch, P->d_ops, bo, P->op_limbs, P->d_prod, cap_s);
-    cudaMemcpyAsync(P->h_pin, P->d_prod, prw * 4, cudaMemcpyDeviceToHost, cap_s);
+    {
+      CaptureScope cs;
+      cudaMemcpyAsync(P->d_stage, P->h_pin, cap * 4, cudaMemcpyHostToDevice, cap_s);
+      RepackArgs R{};
+      R.stage = P->d_stage + head;
+      R.off = reinterpret_cast<const long long*>(P->d_stage);
+      R.dst = P->d_ops;
+      R.ndst = P->op_limbs;
+      R.sbits = digit_bits;
+      const int gx = (int)std::max<long long>(1, std::min<long long>((P->op_limbs + 255) / 256, 1184 / nops + 1));
+      launch_k(k_repack_bits, dim3(gx, nops), dim3(256), 0, cap_s, R);
+      const uint32_t* bo = sq ? nullptr : P->d_ops + (size_t)batch * P->op_limbs;
+      rc = run_mul(P, batch, P->d_ops, bo, P->op_limbs, P->d_prod, cap_s);
+      cudaMemcpyAsync(P->h_pin, P->d_prod, prw * 4, cudaMemcpyDeviceToHost, cap_s);
+    }
     cudaGraph_t g;
     cudaError_t e = cudaStreamEndCapture(cap_s, &g);
     cudaStreamDestroy(cap_s);
-    if (rc) return rc;
+    if (rc) {
+      if (e == cudaSuccess) cudaGraphDestroy(g);
+      return rc;
+    }
     if (e != cudaSuccess) return fail(DKSS_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
-    cudaGraphExec_t ge;
-    e = cudaGraphInstantiate(&ge, g, 0);
-    cudaGraphDestroy(g);
-    if (e != cudaSuccess) return fail(DKSS_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
-    it = P->dgraphs.emplace(key, ge).first;
+    if (!(ent = P->dgraphs.put(key, g, &e))) return fail(DKSS_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
   }
   long long* off = reinterpret_cast<long long*>(P->h_pin);
   uint32_t* dig = P->h_pin + head;
@@ -1145,7 +1286,7 @@ int run_digits_graph(dkss_plan* P, int batch, bool sq, int nops, const uint32_t*
     if (nd[q]) memcpy(dig + off[q], ptrs[q], nd[q] * 4);
   });
   ht_mark("stage_copy");
-  CUCHK(cudaGraphLaunch(it->second, P->stream));
+  CUCHK(P->dgraphs.launch(ent, P->stream));
   ht_mark("graph_launch");
   CUCHK(cudaStreamSynchronize(P->stream));
   ht_mark("sync");
@@ -1384,6 +1525,7 @@ int dkss_block_transpose(dkss_plan* P, const uint32_t* src, uint32_t* dst, int n
   CUCHK(cudaSetDevice(P->device));
   const long long run = run_words / 4;
   const int gx = (int)std::max<long long>(1, std::min<long long>((run + 255) / 256, std::max(1, 1184 / (n * A * B))));
+  count_launch();
   k_block_transpose<<<dim3(gx, n * A * B), 256, 0, (cudaStream_t)stream>>>((const uint4*)src, (uint4*)dst, A, B, run);
   CUCHK(cudaGetLastError());
   mark(P, (cudaStream_t)stream, DKSS_K_TRANSPOSE, 0, 2LL * n * A * B * run_words * 4);
@@ -1406,32 +1548,30 @@ int dkss_decode_device(dkss_plan* P, const uint32_t* v, uint32_t* out, size_t nc
 
 // --- Lucas-Lehmer driver (bigmul/bench.py:197-217) -----------------------------------
 namespace {
-int ll_graph(dkss_plan* P, long long p, int k, cudaGraphExec_t* out) {
-  auto it = P->ll_graphs.find({p, k});
-  if (it != P->ll_graphs.end()) {
-    *out = it->second;
-    return 0;
-  }
+int ll_graph(dkss_plan* P, long long p, int k, GraphLru<std::pair<long long, int>>::Ent** out) {
+  if ((*out = P->ll_graphs.find({p, k}))) return 0;
   cudaStream_t cap;
   CUCHK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
   CUCHK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
   int rc = 0;
-  MersArgs M{P->d_prod, P->prod_limbs, p, P->d_ops};
-  for (int i = 0; i < k && !rc; ++i) {
-    rc = run_mul(P, 1, P->d_ops, nullptr, P->op_limbs, P->d_prod, cap);
-    if (!rc) launch_k(k_mersenne_sub2, dim3(1), dim3(kMersThreads), 0, cap, M);
+  {
+    CaptureScope cs;
+    MersArgs M{P->d_prod, P->prod_limbs, p, P->d_ops};
+    for (int i = 0; i < k && !rc; ++i) {
+      rc = run_mul(P, 1, P->d_ops, nullptr, P->op_limbs, P->d_prod, cap);
+      if (!rc) launch_k(k_mersenne_sub2, dim3(1), dim3(kMersThreads), 0, cap, M);
+    }
   }
   cudaGraph_t g;
   cudaError_t e = cudaStreamEndCapture(cap, &g);
   cudaStreamDestroy(cap);
-  if (rc) return rc;
+  if (rc) {
+    if (e == cudaSuccess) cudaGraphDestroy(g);
+    return rc;
+  }
   if (e != cudaSuccess) return fail(DKSS_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
-  cudaGraphExec_t ge;
-  e = cudaGraphInstantiate(&ge, g, 0);
-  cudaGraphDestroy(g);
-  if (e != cudaSuccess) return fail(DKSS_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
-  P->ll_graphs[{p, k}] = ge;
-  *out = ge;
+  if (!(*out = P->ll_graphs.put({p, k}, g, &e)))
+    return fail(DKSS_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
   return 0;
 }
 }  // namespace
@@ -1454,9 +1594,9 @@ int dkss_lucas_lehmer(dkss_plan* P, int64_t p, int64_t iters, uint32_t* s, size_
   long long left = iters;
   while (left > 0) {
     const int k = left >= K ? K : (int)left;
-    cudaGraphExec_t ge;
+    GraphLru<std::pair<long long, int>>::Ent* ge;
     if ((rc = ll_graph(P, p, k, &ge))) return rc;
-    CUCHK(cudaGraphLaunch(ge, st));
+    CUCHK(P->ll_graphs.launch(ge, st));
     left -= k;
   }
   CUCHK(cudaMemcpyAsync(s, P->d_ops, n * 4, cudaMemcpyDeviceToHost, st));
@@ -1495,6 +1635,7 @@ int dkss_fft_host(dkss_plan* P, uint32_t* polys, int count) {
   if ((rc = launch_fwd_levels(P, work, count, s))) return rc;
   if ((rc = launch_bottom(P, work, nullptr, count, 0, false, s))) return rc;
   const long long elems = 2LL * P->M;
+  count_launch();
   k_permute<<<(int)std::min<long long>((elems * count * P->m * P->L + 255) / 256, 148LL * 32), 256, 0, s>>>(
       work, scratch, elems, P->m * P->L, P->logE, P->levels, P->logb, 1, P->poly_words, count);
   CUCHK(cudaGetLastError());
@@ -1517,6 +1658,7 @@ int dkss_rmul_host(dkss_plan* P, const uint32_t* x, const uint32_t* y, uint32_t*
   cudaMemcpyAsync(dx, x, count * ew * 4, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(dy, y, count * ew * 4, cudaMemcpyHostToDevice, s);
   const int grid = (int)((count + P->kt.ne - 1) / P->kt.ne);
+  count_launch();
   P->kt.rmul<<<grid, P->kt.nt, P->kt.smem_rmul, s>>>(dx, dy, dout, (long long)count, P->mc);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, count * ew * 4, cudaMemcpyDeviceToHost, s);
@@ -1537,6 +1679,7 @@ int dkss_decode_host(dkss_plan* P, const uint32_t* v, uint32_t* out, size_t nout
   cudaStream_t s = P->stream;
   CUCHK(cudaMemcpyAsync(P->d_poly, v, P->poly_words * 4, cudaMemcpyHostToDevice, s));
   const long long nres = 2LL * P->M * P->m;
+  count_launch();
   P->kt.mscale<<<(int)std::min<long long>((nres + 255) / 256, 4096), 256, 0, s>>>(P->d_poly, nres, 1, P->mc);
   CUCHK(cudaGetLastError());
   if ((rc = launch_decode(P, P->d_poly, P->d_prod, 1, s))) return rc;

@@ -83,7 +83,7 @@ void smul_fft_q(smul_plan* P, uint32_t* x, uint32_t* top, int npoly, bool invers
   // 2^20 65 us at 96, 68 at 64, 67 at 148; fewer, deeper passes beat covering all 148 SMs);
   // then split the levels evenly
   static const long long min_ctas = [] {
-    const char* e = getenv("DKSS_SMUL_MINCTA");  // experiment knob
+    const char* e = DKSS_KNOB("DKSS_SMUL_MINCTA");  // experiment knob
     return e ? atoll(e) : 96LL;
   }();
   int nlv = P->nlv_max;
@@ -313,6 +313,9 @@ int smul_mul_device(smul_plan* P, int batch, const uint32_t* a_dev, const uint32
                     uint32_t* c_dev, size_t nc, void* stream) {
   if (!P || batch < 1 || !a_dev || !c_dev) return fail(DKSS_EINVAL, "bad argument");
   if ((long long)nc < P->prod_limbs) return fail(DKSS_EINVAL, "nc=%zu below the plan's %lld product limbs", nc, P->prod_limbs);
+  // the fused encode reads N bits per operand: wider operands would lose their top slices
+  if ((long long)n_limbs * 32 > P->N) return fail(DKSS_ERANGE, "operands of %zu limbs exceed the plan's N=%lld bits", n_limbs, P->N);
+  if (2LL * batch > 65535) return fail(DKSS_EINVAL, "batch %d too large (grid y limit)", batch);
   std::lock_guard<std::mutex> lk(P->mu);
   CUCHK(cudaSetDevice(P->device));
   return run_smul(P, batch, a_dev, b_dev, (long long)n_limbs, c_dev, (long long)nc, (cudaStream_t)stream);

@@ -26,8 +26,8 @@ import numpy as np
 
 from ._native import DKSS_DIGITS_TRUSTED, DevicePlan
 from .plan import DkssPlan, dkss_select_params, ring_products_per_multiply, twiddle_count
-from .words import (Natural, ScratchArena, as_natural, current_arena, int_to_u32, pylong_digits, u32_to_int,
-                    word_bits, PYLONG_DIGIT_BITS)
+from .words import (Natural, ScratchArena, as_natural, current_arena, foreign_natural, int_to_u32, pylong_digits,
+                    u32_to_int, word_bits, words_to_int, PYLONG_DIGIT_BITS)
 
 # The reference hands products below 2048 result bits to smul (bigmul/dkss.py:517,
 # 533-535); here dmul always measures DKSS, so such inputs run through DKSS on the GPU
@@ -193,10 +193,31 @@ def dkss_decode(v, plan: DkssPlan, arena: ScratchArena | None = None) -> Natural
 # ---------------------------------------------------------------------------
 # the multiply
 
+def _caller(*xs):
+    """(Natural class to return, word size) of a call: the reference's own class and word size
+    when it handed in its bigmul.words.Natural (the reference's mul, run_bench and lucas_lehmer
+    convert operands before calling ALGORITHMS[...], bigmul/dispatch.py:30-36,
+    bigmul/bench.py:35-64, 210-213), else (None, this package's word size)."""
+    for x in xs:
+        fw = foreign_natural(x)
+        if fw is not None:
+            return fw
+    return None, word_bits()
+
+
+def _deliver(n: Natural, cls):
+    """The product as the caller's Natural class (same words, same word size)."""
+    return n if cls is None else cls(n.words)
+
+
 def _as_int_len(x, w: int):
-    """(value, word length) exactly as as_natural(x) would give (bigmul/words.py:112-117)."""
+    """(value, word length at word size w) exactly as as_natural(x) would give
+    (bigmul/words.py:112-117); a foreign Natural's words are read at its own word size w."""
     if isinstance(x, Natural):
-        return x.to_int(), len(x)
+        return x.to_int(w), len(x)
+    if foreign_natural(x) is not None:
+        ws = x.words
+        return words_to_int(ws, w), len(ws)
     if isinstance(x, int) and not isinstance(x, bool):
         if x < 0:
             raise ValueError("Natural is nonnegative")
@@ -229,7 +250,7 @@ def _hot_plan(N: int, w: int):
         plan = _plan_for(N, w)
         dp = device_plan(plan, key[2])
         info = dp.info
-        ent = (plan, dp, info["operand_limbs"], info["product_limbs"], 2 * info["poly_bytes"],
+        ent = (plan, dp, info["operand_limbs"], info["product_limbs"], info["footprint_bytes"],
                ring_products_per_multiply(plan))
         with _dev_lock:
             _cache_put(_hot, key, ent)
@@ -237,21 +258,24 @@ def _hot_plan(N: int, w: int):
 
 
 def dmul(a, b, thresholds=None, arena: ScratchArena | None = None) -> Natural:
-    """Full product via DKSS on the GPU (bigmul/dkss.py:520-548)."""
-    w = word_bits()
+    """Full product via DKSS on the GPU (bigmul/dkss.py:520-548).
+
+    a, b: int, this package's Natural or the reference's bigmul.words.Natural; the result is a
+    Natural of len(a) + len(b) words of the caller's class and word size.  ``arena`` records the
+    device bytes the multiply holds (dkss_plan_info.footprint_bytes)."""
+    cls, w = _caller(a, b)
     ai, la = _as_int_len(a, w)
     bi, lb = _as_int_len(b, w)
     arena = arena or current_arena()
     outlen = max(1, la + lb)
     if ai == 0 or bi == 0:
-        return Natural([0] * outlen)
+        return _deliver(Natural([0] * outlen), cls)
     n_bits = max(ai.bit_length(), bi.bit_length())
-    plan, dp, nl, npl, poly2_bytes, rp = _hot_plan(max(n_bits, _MIN_PLAN_BITS), w)
+    plan, dp, nl, npl, footprint, rp = _hot_plan(max(n_bits, _MIN_PLAN_BITS), w)
     nc = max(npl, -(-outlen * w // 32))
     mark = arena.acquire()
     try:
-        # device workspace per multiply: 2 polynomials + operands + product, in words
-        arena.alloc_words((poly2_bytes + 4 * (2 * nl + nc)) * 8 // w)
+        arena.alloc_words(-(-footprint * 8 // w))
         ka, pa, na, ba = _digits(a, ai)
         kb, pb, nb, bb = (ka, pa, na, ba) if b is a else _digits(b, bi)
         if ba == bb:
@@ -262,7 +286,7 @@ def dmul(a, b, thresholds=None, arena: ScratchArena | None = None) -> Natural:
     finally:
         arena.release(mark)
     plan.ks_calls += rp
-    return Natural._from_u32(c, outlen, w)
+    return _deliver(Natural._from_u32(c, outlen, w), cls)
 
 
 _PIPE_MIN_PAIRS = 64   # batches at least this large run as chunks on two device lanes
@@ -305,7 +329,7 @@ def dmul_many(pairs, thresholds=None) -> list:
     pairs = list(pairs)
     if not pairs:
         return []
-    w = word_bits()
+    cls, w = _caller(*pairs[0])
     vals = [(_as_int_len(a, w), _as_int_len(b, w)) for a, b in pairs]
     n_bits = max(max(ai.bit_length(), bi.bit_length()) for (ai, _), (bi, _) in vals)
     plan = _plan_for(max(n_bits, _MIN_PLAN_BITS), w)
@@ -327,4 +351,4 @@ def dmul_many(pairs, thresholds=None) -> list:
         C = dp.mul_batch(A, B, nc)
     del da, db
     plan.ks_calls += len(pairs) * ring_products_per_multiply(plan)
-    return [Natural._from_u32(C[i], lens[i], w) for i in range(len(pairs))]
+    return [_deliver(Natural._from_u32(C[i], lens[i], w), cls) for i in range(len(pairs))]

@@ -38,14 +38,16 @@ def lucas_lehmer_steps(p: int, iters: int, s: int = 4) -> int:
     return u32_to_int(out)
 
 
-def lucas_lehmer(p: int, multiplier: str = "dmul", thresholds=None):
-    """Lucas-Lehmer test of 2^p - 1 (bigmul/bench.py:197-217) -> (is_prime, residue64)."""
+def lucas_lehmer(p: int, multiplier: str = "smul", thresholds=None):
+    """Lucas-Lehmer test of 2^p - 1 (bigmul/bench.py:197-217) -> (is_prime, residue64).
+
+    Same signature and default multiplier as the reference; an unknown name raises KeyError
+    from the table lookup, as the reference's ``ALGORITHMS[multiplier]`` does (bigmul/bench.py:210)."""
     if p == 2:
         return True, 4 & ((1 << 64) - 1)
     if p < 2 or p % 2 == 0:
         raise ValueError("exponent must be an odd prime")
-    if multiplier not in ALGORITHMS:
-        raise ValueError(f"unknown algorithm {multiplier!r}")
+    ALGORITHMS[multiplier]  # KeyError for an unknown rung, before any work
     if multiplier == "smul":
         # the comparison baseline: one GPU smul square per step, reduced on the host
         # (bigmul/bench.py:210-216 with ALGORITHMS["smul"])

@@ -7,8 +7,8 @@ the caller wants every product everywhere -- the products are all-gathered.
 There is no collective on the data path: the plan (rho table) is replicated,
 each rank owns its operands and products.
 
-The single large multiply does not shard here: its four-step split is listed as
-next work in DESIGN.md (it needs an all-to-all transpose per transform).
+One large multiply is split across GPUs by the four-step layout instead
+(fourstep.py: column phase, NCCL all-to-all, row phase, all-to-all back).
 """
 
 from __future__ import annotations

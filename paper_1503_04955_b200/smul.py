@@ -209,22 +209,24 @@ def _device_plan(plan: SmulPlan, device: int):
             dp = SmulDevicePlan(plan.N, plan.m, plan.s, plan.K, plan.omega_exp, device)
             _dev[key] = dp
             while len(_dev) > _MAX:
-                _dev.pop(next(iter(_dev))).close()
+                # dropped, not closed: a thread may still be multiplying on the evicted plan;
+                # SmulDevicePlan.__del__ frees it once the last reference goes
+                _dev.pop(next(iter(_dev)))
     return dp
 
 
 def smul(a, b, thresholds: ThresholdTable | None = None, arena: ScratchArena | None = None) -> Natural:
     """Full product via the outermost Schoenhage-Strassen level on the GPU
     (bigmul/smul.py:286-300): a Natural of len(a) + len(b) words."""
-    from .dkss import _as_int_len, _digits  # (value, word length) without building a Natural
+    from .dkss import _as_int_len, _caller, _deliver, _digits  # (value, word length) without a Natural
 
     arena = arena or current_arena()
-    w = word_bits()
+    cls, w = _caller(a, b)  # the reference's Natural class and word size when it passed its own
     ai, la_w = _as_int_len(a, w)
     bi, lb_w = _as_int_len(b, w)
     outlen = max(1, la_w + lb_w)
     if ai == 0 or bi == 0:
-        return Natural([0] * outlen)
+        return _deliver(Natural([0] * outlen), cls)
     n0 = ai.bit_length() + bi.bit_length()
     plan, dp = device_plan_for(n0, w, thresholds)
     nc = max(1, -(-outlen * w // 32))
@@ -239,7 +241,7 @@ def smul(a, b, thresholds: ThresholdTable | None = None, arena: ScratchArena | N
             A = int_to_u32(ai, la)
             c = dp.mul_limbs(A, A if bi == ai else int_to_u32(bi, lb), nc)
         del ka, kb
-    return Natural._from_u32(c, outlen, w)
+    return _deliver(Natural._from_u32(c, outlen, w), cls)
 
 
 def fft_eval_fermat(v: list, plan: SmulPlan, inverse: bool = False) -> None:

@@ -164,6 +164,9 @@ class Natural:
             return self.to_int() == other.to_int()
         if isinstance(other, int):
             return self.to_int() == other
+        fw = foreign_natural(other)
+        if fw is not None:  # the reference's bigmul.words.Natural (or any word-list Natural)
+            return self.to_int() == words_to_int(other.words, fw[1])
         return NotImplemented
 
     __hash__ = None
@@ -172,9 +175,25 @@ class Natural:
         return f"Natural({self.words!r})"
 
 
+def foreign_natural(x):
+    """(class, word size) when x is another package's Natural -- an object with a ``words`` list
+    and ``to_int``, like the reference's ``bigmul.words.Natural`` (bigmul/words.py:56-109) -- else
+    None.  Its words are at ITS package's thread-local word size: the reference keeps its own
+    ``word_bits()`` (bigmul/words.py:17-23), read from the class's module when it has one."""
+    if isinstance(x, (Natural, int)) or not hasattr(x, "words") or not hasattr(x, "to_int"):
+        return None
+    mod = sys.modules.get(type(x).__module__)
+    wb = getattr(mod, "word_bits", None)
+    w = wb() if callable(wb) else word_bits()
+    return type(x), w
+
+
 def as_natural(x) -> Natural:
     if isinstance(x, Natural):
         return x
+    fw = foreign_natural(x)
+    if fw is not None:  # same words at the same word size; else the same value
+        return Natural(x.words) if fw[1] == word_bits() else Natural.from_int(words_to_int(x.words, fw[1]))
     if isinstance(x, int) and not isinstance(x, bool):
         return Natural.from_int(x)
     if isinstance(x, bool):

@@ -316,30 +316,66 @@ def test_square_batch_and_all_ones(cuda_ok):
     assert [g.to_int() for g in got] == [x * x for x in xs]
 
 
-@pytest.mark.parametrize("env", ["DKSS_DYN=1", "DKSS_NO_DYN=1", "DKSS_ROWS=1"])
-def test_row_phase_variants_subprocess(cuda_ok, env):
-    # the row-phase implementation is chosen at plan creation from the environment: run the
-    # two-level sizes of both inner lengths in a fresh process per variant
-    import subprocess
-    import sys
+@pytest.mark.parametrize("row_phase,pass_kind", [("persistent", "auto"), ("launches", "auto"), ("cluster", "auto"),
+                                                  ("launches", "warp"), ("launches", "split"), ("auto", "cta")])
+def test_kernel_shape_variants(cuda_ok, row_phase, pass_kind):
+    # every kernel shape a plan can be built with (include/dkss.h dkss_plan_opts) gives the same
+    # products: two-level sizes of both inner lengths, squares and a batch
+    from paper_1503_04955_b200._native import DevicePlan
+    from paper_1503_04955_b200.dkss import plan_capacity
 
-    code = (
-        "import random\n"
-        "from paper_1503_04955_b200 import dmul, dmul_many\n"
-        "r = random.Random(11)\n"
-        "for e in (18, 20, 21, 23):\n"
-        "    N = 1 << e\n"
-        "    a, b = r.getrandbits(N), r.getrandbits(N)\n"
-        "    assert dmul(a, b).to_int() == a * b, e\n"
-        "    assert dmul(a, a).to_int() == a * a, e\n"
-        "ps = [(r.getrandbits(1 << 18), r.getrandbits(1 << 18)) for _ in range(6)]\n"
-        "assert [c.to_int() for c in dmul_many(ps)] == [x * y for x, y in ps]\n"
-        "print('ok')\n")
-    k, v = env.split("=")
-    envd = dict(os.environ, **{k: v})
-    out = subprocess.run([sys.executable, "-c", code], env=envd, capture_output=True, text=True, timeout=600,
-                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+    r = random.Random(11)
+    for e in (18, 20, 21, 23):
+        N = 1 << e
+        pl = P.dkss_select_params(N)
+        dp = DevicePlan(plan_capacity(pl), pl.M, pl.m, pl.u, pl.p, pl.rho_powers, 0, row_phase=row_phase,
+                        pass_kind=pass_kind)
+        nl, npl = dp.info["operand_limbs"], dp.info["product_limbs"]
+        a, b = r.getrandbits(N), r.getrandbits(N)
+        A, B = int_to_u32(a, nl), int_to_u32(b, nl)
+        assert u32_to_int(dp.mul_limbs(A, B, npl)) == a * b, e
+        sq = dp.mul_digits(A.ctypes.data, nl, A.ctypes.data, nl, 32, npl)  # same pointers: squaring mode
+        assert u32_to_int(sq) == a * a, e
+        if e == 18:
+            ps = [(r.getrandbits(N), r.getrandbits(N)) for _ in range(6)]
+            C = dp.mul_batch(np.stack([int_to_u32(x, nl) for x, _ in ps]), np.stack([int_to_u32(y, nl) for _, y in ps]))
+            assert [u32_to_int(c) for c in C] == [x * y for x, y in ps]
+        dp.close()
+
+
+def test_plans_and_graphs_do_not_leak(cuda_ok):
+    # 1000 plan create/destroy cycles and 100 distinct device-buffer triples (one cached CUDA
+    # graph each, LRU-capped per plan): device memory stays bounded
+    import torch
+
+    from paper_1503_04955_b200._native import DevicePlan
+    from paper_1503_04955_b200.dkss import plan_capacity
+
+    pl = P.dkss_select_params(1 << 12)
+    args = (plan_capacity(pl), pl.M, pl.m, pl.u, pl.p, pl.rho_powers, 0)
+    torch.cuda.init()
+    DevicePlan(*args).close()
+    free0, _ = torch.cuda.mem_get_info()
+    for _ in range(1000):
+        DevicePlan(*args).close()
+    dp = DevicePlan(*args)
+    nl, npl = dp.info["operand_limbs"], dp.info["product_limbs"]
+    dev = torch.device("cuda", 0)
+    r = random.Random(5)
+    for i in range(100):
+        a, b = r.getrandbits(4000), r.getrandbits(4000)
+        A = torch.from_numpy(int_to_u32(a, nl).view(np.int32)).to(dev)
+        B = torch.from_numpy(int_to_u32(b, nl).view(np.int32)).to(dev)
+        C = torch.zeros(npl + i % 3, dtype=torch.int32, device=dev)
+        dp.mul_device(1, A.data_ptr(), B.data_ptr(), nl, C.data_ptr(), C.numel())
+        torch.cuda.synchronize()
+        assert u32_to_int(C.cpu().numpy().view(np.uint32)) == a * b
+        del A, B, C
+    dp.close()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < 64 << 20, (free0, free1)
 
 
 @pytest.mark.parametrize("e", [27, 28])

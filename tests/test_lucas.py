@@ -28,28 +28,31 @@ def test_host_loop_verdicts():
 def test_argument_errors():
     with pytest.raises(ValueError):
         lucas_lehmer(4)
-    with pytest.raises(ValueError):
+    with pytest.raises(KeyError):  # the reference's ALGORITHMS[multiplier] lookup (bigmul/bench.py:210)
         lucas_lehmer(9, "nope")
     assert lucas_lehmer(2) == (True, 4)
+    import inspect
+
+    assert inspect.signature(lucas_lehmer).parameters["multiplier"].default == "smul"  # bigmul/bench.py:197
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("p", [3, 5, 7, 11, 13, 23, 29, 31, 37, 61, 89, 127, 521, 1279, 4423])
 def test_device_ll_matches_host(cuda_ok, p):
-    assert lucas_lehmer(p) == lucas_lehmer_host(p)
+    assert lucas_lehmer(p, "dmul") == lucas_lehmer_host(p)
 
 
 @pytest.mark.gpu
 def test_device_ll_known_primes(cuda_ok):
     for p in MERSENNE_PRIME_EXPONENTS:
-        assert lucas_lehmer(p)[0] is True, p
+        assert lucas_lehmer(p, "dmul")[0] is True, p
 
 
 @pytest.mark.gpu
 def test_device_ll_composite_residues(cuda_ok):
     # residue64 of composite Mersenne numbers against Python's int loop
     for p in (1277, 2311, 4457, 9697, 11239):
-        assert lucas_lehmer(p) == lucas_lehmer_host(p), p
+        assert lucas_lehmer(p, "dmul") == lucas_lehmer_host(p), p
 
 
 @pytest.mark.gpu

@@ -180,9 +180,19 @@ def test_smul_range_errors(cuda_ok):
 def test_harness_quotient_dmul_over_smul(cuda_ok):
     import io
 
-    from paper_1503_04955_b200.harness import quotient_column, run_bench, write_csv
+    # the REFERENCE's harness (bigmul/bench.py:42-91) with both GPU rungs installed in its table
+    from test_reference_callers import _import_reference
 
-    recs = run_bench(["dmul", "smul"], [64, 1024], reps=3, seed=5)
+    from paper_1503_04955_b200.integration import install
+
+    bigmul = _import_reference()
+    from bigmul.bench import quotient_column, run_bench, write_csv
+
+    undo = install(bigmul, smul=True)
+    try:
+        recs = run_bench(["dmul", "smul"], [64, 1024], reps=3, seed=5, reference="t3mul")
+    finally:
+        undo()
     assert {(r.algorithm, r.input_words) for r in recs} == {(a, s) for a in ("dmul", "smul") for s in (64, 1024)}
     q = quotient_column(recs)  # T_DMUL / T_SMUL (bigmul/bench.py:80-91)
     assert [s for s, _ in q] == [64, 1024] and all(v > 0 for _, v in q)
