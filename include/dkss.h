@@ -95,6 +95,12 @@ int64_t dkss_kernel_launches(void);
  * bad shape. */
 int64_t dkss_footprint_bytes(int64_t N, int32_t M, int32_t m, int32_t L);
 
+/* Page-locked host buffers from a library pool (recycled by size).  A product buffer `c` from
+ * here receives the products of dkss_mul_digits / dkss_mul_batch_digits straight from the device
+ * (no staging copy); dkss_host_free returns it to the pool. */
+int dkss_host_alloc(size_t bytes, void** out);
+void dkss_host_free(void* p);
+
 /* dmul (bigmul/dkss.py:520-548) for operands below 2^N: c = a * b.
  * Host buffers; na, nb <= operand_limbs; nc limbs are written (zero padded); the call
  * fails with DKSS_ERANGE if the product does not fit nc limbs. */

@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("DKSS_LIB") or os.path.join(HERE, "_lib", "libdkss.so"
 # every symbol include/dkss.h declares (checked by tests/test_native_abi.py)
 EXPORTS = (
     "dkss_plan_create", "dkss_plan_create_ex", "dkss_plan_destroy", "dkss_plan_get_info", "dkss_last_error",
-    "dkss_version", "dkss_kernel_launches", "dkss_footprint_bytes",
+    "dkss_version", "dkss_kernel_launches", "dkss_footprint_bytes", "dkss_host_alloc", "dkss_host_free",
     "dkss_mul", "dkss_mul_digits", "dkss_mul_batch_digits", "dkss_mul_batch", "dkss_mul_device", "dkss_profile_device",
     "dkss_encode_host", "dkss_fft_host", "dkss_rmul_host", "dkss_decode_host",
     "dkss_fs_layout_get", "dkss_fs_columns_fwd", "dkss_fs_rows", "dkss_fs_columns_inv",
@@ -102,6 +102,9 @@ def load(path: str = LIB_PATH):
         L.dkss_kernel_launches.argtypes = []
         L.dkss_footprint_bytes.restype = ctypes.c_int64
         L.dkss_footprint_bytes.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
+        L.dkss_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(vp)]
+        L.dkss_host_free.argtypes = [vp]
+        L.dkss_host_free.restype = None
         L.dkss_plan_destroy.argtypes = [vp]
         L.dkss_plan_destroy.restype = None
         L.dkss_plan_get_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]
@@ -210,7 +213,7 @@ class DevicePlan:
 
     def mul_digits(self, a_ptr: int, na: int, b_ptr: int, nb: int, digit_bits: int, nc: int) -> np.ndarray:
         """Product of two radix-2^digit_bits digit strings at host addresses a_ptr / b_ptr."""
-        out = np.empty(nc, dtype=np.uint32)
+        out = pinned_empty((nc,))
         _check(self._lib.dkss_mul_digits(self._h, ctypes.c_void_p(a_ptr), na, ctypes.c_void_p(b_ptr), nb, digit_bits,
                                          _ptr(out), nc))
         return out
@@ -224,7 +227,7 @@ class DevicePlan:
         cna = (ctypes.c_size_t * batch)(*na)
         cnb = (ctypes.c_size_t * batch)(*nb)
         if out is None:
-            out = np.empty((batch, nc), dtype=np.uint32)
+            out = pinned_empty((batch, nc))
         elif out.shape != (batch, nc) or out.dtype != np.uint32 or not out.flags.c_contiguous:
             raise ValueError("out must be a C-contiguous uint32[batch][nc] array")
         _check(self._lib.dkss_mul_batch_digits(self._h, batch, vpa, cna, vpb, cnb, digit_bits, _ptr(out), nc))
@@ -379,3 +382,37 @@ def footprint_bytes(N: int, M: int, m: int, L: int) -> int:
     if v < 0:
         raise ValueError("bad plan shape")
     return v
+
+
+_PINNED_MIN_BYTES = 64 << 10  # smaller products: ordinary memory (the staging copy is negligible)
+
+
+class _PinnedBlock:
+    """A page-locked block from the library pool (dkss_host_alloc), exposed to numpy through the
+    array interface; numpy arrays (and their slices) built on it keep it alive, and the last one
+    returns it to the pool."""
+
+    __slots__ = ("ptr", "__array_interface__", "_free")
+
+    def __init__(self, shape):
+        lib = load()
+        nbytes = 4 * int(np.prod(shape))
+        p = ctypes.c_void_p()
+        _check(lib.dkss_host_alloc(nbytes, ctypes.byref(p)))
+        self.ptr = p.value
+        self._free = lib.dkss_host_free
+        self.__array_interface__ = {"shape": tuple(shape), "typestr": "<u4", "data": (self.ptr, False), "version": 3}
+
+    def __del__(self):
+        if self.ptr:
+            self._free(ctypes.c_void_p(self.ptr))
+            self.ptr = None
+
+
+def pinned_empty(shape) -> np.ndarray:
+    """uint32 array of `shape` in page-locked host memory for products (the device copies into it
+    directly); below 64 KiB an ordinary array."""
+    shape = tuple(shape)
+    if 4 * int(np.prod(shape)) < _PINNED_MIN_BYTES:
+        return np.empty(shape, dtype=np.uint32)
+    return np.asarray(_PinnedBlock(shape))

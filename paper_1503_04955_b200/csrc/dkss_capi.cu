@@ -7,6 +7,8 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <condition_variable>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
@@ -1185,29 +1187,134 @@ void ht_mark(const char* w) {
   if (g_ht) g_ht->mark(w);
 }
 
-// fn(i) for i in [0, n), spread over up to 8 host threads when `bytes` of copying is large
+// Persistent host worker threads for the staging copies of the host-buffer entry points: a
+// 4 MB operand copy is ~0.4 ms on one core; spread over the pool it overlaps the memory
+// bandwidth of several cores (thread start-up per call would cost more than it saves).
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* pool = new HostPool();  // never destroyed: workers outlive static teardown
+    return *pool;
+  }
+  unsigned size() const { return (unsigned)workers_.size() + 1; }
+  // fn(i) for i in [0, n) on the pool and the calling thread; returns when all are done
+  void run(size_t n, const std::function<void(size_t)>& fn) {
+    if (n == 0) return;
+    if (n == 1 || workers_.empty()) {
+      for (size_t i = 0; i < n; ++i) fn(i);
+      return;
+    }
+    std::unique_lock<std::mutex> call(call_mu_);  // one parallel region at a time
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &fn;
+      n_ = n;
+      next_ = 0;
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return done_ == n_; });
+    fn_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned nt = std::min(8u, hw) - 1;
+    for (unsigned t = 0; t < nt; ++t)
+      workers_.emplace_back([this] {
+        unsigned long long seen = 0;
+        for (;;) {
+          {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return gen_ != seen; });
+            seen = gen_;
+          }
+          work();
+        }
+      });
+    for (auto& w : workers_) w.detach();
+  }
+  void work() {
+    for (;;) {
+      size_t i;
+      const std::function<void(size_t)>* f;
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (!fn_ || next_ >= n_) return;
+        i = next_++;
+        f = fn_;
+      }
+      (*f)(i);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (++done_ == n_) done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, call_mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(size_t)>* fn_ = nullptr;
+  size_t n_ = 0, next_ = 0, done_ = 0;
+  unsigned long long gen_ = 0;
+};
+
+constexpr size_t kCopyChunk = 512 << 10;  // bytes per staging-copy task
+
+// memcpy in chunks over the host pool (small copies stay on the calling thread)
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  if (bytes < 2 * kCopyChunk) {
+    if (bytes) memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t n = (bytes + kCopyChunk - 1) / kCopyChunk;
+  HostPool::get().run(n, [&](size_t i) {
+    const size_t off = i * kCopyChunk;
+    memcpy((char*)dst + off, (const char*)src + off, std::min(kCopyChunk, bytes - off));
+  });
+}
+
+// fn(i) for i in [0, n) over the host pool when `bytes` of copying is large
 template <class F>
 void host_par(size_t n, size_t bytes, F fn) {
-  unsigned nt = bytes >= (8u << 20) ? std::min(8u, std::max(1u, std::thread::hardware_concurrency())) : 1u;
-  nt = (unsigned)std::min<size_t>(nt, n);
-  if (nt <= 1) {
+  if (bytes < 2 * kCopyChunk || n <= 1) {
     for (size_t i = 0; i < n; ++i) fn(i);
     return;
   }
-  std::vector<std::thread> th;
-  for (unsigned t = 0; t < nt; ++t)
-    th.emplace_back([&, t] {
-      for (size_t i = t; i < n; i += nt) fn(i);
-    });
-  for (auto& x : th) x.join();
+  HostPool::get().run(n, [&](size_t i) { fn(i); });
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// pinned host blocks handed out by dkss_host_alloc, recycled by size
+struct PinnedPool {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_;  // size -> block
+  std::map<void*, size_t> live;        // block -> size
+  size_t cached = 0;
+  static constexpr size_t kCacheCap = 512ull << 20;
+};
+PinnedPool& pinned_pool() {
+  static PinnedPool* p = new PinnedPool();
+  return *p;
 }
 
 }  // namespace
 
 namespace {
-// Host digit strings -> products in ONE graph launch: H2D of the staging buffer (offsets +
-// digits, sized for the largest operands the plan admits), radix repack, the multiply,
-// D2H of the products; the host only validates, packs and unpacks.
+// Host digit strings -> products: the staging buffer (offsets + digits) goes to the device
+// operand by operand as the host pool stages it, then ONE graph launch (radix repack, the
+// multiply), then the D2H of the products -- straight into the caller's buffer when that is
+// page-locked (dkss_host_alloc), else through the staging buffer.
 int run_digits_graph(dkss_plan* P, int batch, bool sq, int nops, const uint32_t* const* ptrs, const size_t* counts,
                      int digit_bits, bool trusted, uint32_t* c, size_t nc) {
   std::vector<size_t> nd((size_t)nops);
@@ -1251,7 +1358,6 @@ int run_digits_graph(dkss_plan* P, int batch, bool sq, int nops, const uint32_t*
     CUCHK(cudaStreamBeginCapture(cap_s, cudaStreamCaptureModeThreadLocal));
     {
       CaptureScope cs;
-      cudaMemcpyAsync(P->d_stage, P->h_pin, cap * 4, cudaMemcpyHostToDevice, cap_s);
       RepackArgs R{};
       R.stage = P->d_stage + head;
       R.off = reinterpret_cast<const long long*>(P->d_stage);
@@ -1262,7 +1368,6 @@ int run_digits_graph(dkss_plan* P, int batch, bool sq, int nops, const uint32_t*
       launch_k(k_repack_bits, dim3(gx, nops), dim3(256), 0, cap_s, R);
       const uint32_t* bo = sq ? nullptr : P->d_ops + (size_t)batch * P->op_limbs;
       rc = run_mul(P, batch, P->d_ops, bo, P->op_limbs, P->d_prod, cap_s);
-      cudaMemcpyAsync(P->h_pin, P->d_prod, prw * 4, cudaMemcpyDeviceToHost, cap_s);
     }
     cudaGraph_t g;
     cudaError_t e = cudaStreamEndCapture(cap_s, &g);
@@ -1282,25 +1387,66 @@ int run_digits_graph(dkss_plan* P, int batch, bool sq, int nops, const uint32_t*
     o += (long long)nd[q];
   }
   off[nops] = o;
-  host_par((size_t)nops, (size_t)o * 4, [&](size_t q) {
-    if (nd[q]) memcpy(dig + off[q], ptrs[q], nd[q] * 4);
-  });
+  if (nops <= 4) {
+    // one product: each operand's digits are copied in chunks over the host pool, and its H2D
+    // is issued as soon as it is staged, so operand q's transfer overlaps operand q+1's copy
+    size_t sent = 0;  // words of the staging buffer (offsets header + digits) already in flight
+    for (int q = 0; q < nops; ++q) {
+      if (nd[q]) par_memcpy(dig + off[q], ptrs[q], nd[q] * 4);
+      const size_t upto = head + (size_t)off[q + 1];
+      if (upto > sent || q + 1 == nops) {
+        CUCHK(cudaMemcpyAsync(P->d_stage + sent, P->h_pin + sent, (upto - sent) * 4, cudaMemcpyHostToDevice,
+                              P->stream));
+        sent = upto;
+      }
+    }
+  } else {
+    host_par((size_t)nops, (size_t)o * 4, [&](size_t q) {
+      if (nd[q]) memcpy(dig + off[q], ptrs[q], nd[q] * 4);
+    });
+    CUCHK(cudaMemcpyAsync(P->d_stage, P->h_pin, (head + (size_t)o) * 4, cudaMemcpyHostToDevice, P->stream));
+  }
   ht_mark("stage_copy");
   CUCHK(P->dgraphs.launch(ent, P->stream));
   ht_mark("graph_launch");
-  CUCHK(cudaStreamSynchronize(P->stream));
-  ht_mark("sync");
+  if (g_ht && g_ht->on) {  // timing study (experiment builds): the graph alone
+    CUCHK(cudaStreamSynchronize(P->stream));
+    ht_mark("graph_sync");
+  }
   const size_t ncopy = std::min<size_t>(nc, P->prod_limbs);
   std::vector<char> over((size_t)batch, 0);
-  host_par((size_t)batch, prw * 4, [&](size_t i) {
-    const uint32_t* src = P->h_pin + i * P->prod_limbs;
-    uint32_t* dst = c + i * nc;
-    memcpy(dst, src, ncopy * 4);
-    for (size_t k = ncopy; k < (size_t)P->prod_limbs; ++k)
-      if (src[k]) over[i] = 1;
-    if (nc > ncopy) memset(dst + ncopy, 0, (nc - ncopy) * 4);
-  });
-  ht_mark("copy_out");
+  if (nc >= (size_t)P->prod_limbs && is_pinned(c)) {
+    // pinned destination (dkss_host_alloc): the products come straight from the device
+    if (nc == (size_t)P->prod_limbs)
+      CUCHK(cudaMemcpyAsync(c, P->d_prod, prw * 4, cudaMemcpyDeviceToHost, P->stream));
+    else
+      CUCHK(cudaMemcpy2DAsync(c, nc * 4, P->d_prod, P->prod_limbs * 4, P->prod_limbs * 4, batch,
+                              cudaMemcpyDeviceToHost, P->stream));
+    CUCHK(cudaStreamSynchronize(P->stream));
+    ht_mark("sync_d2h_direct");
+    if (nc > ncopy)
+      for (int i = 0; i < batch; ++i) memset(c + (size_t)i * nc + ncopy, 0, (nc - ncopy) * 4);
+  } else {
+    CUCHK(cudaMemcpyAsync(P->h_pin, P->d_prod, prw * 4, cudaMemcpyDeviceToHost, P->stream));
+    CUCHK(cudaStreamSynchronize(P->stream));
+    ht_mark("sync");
+    auto row = [&](size_t i) {
+      const uint32_t* src = P->h_pin + i * P->prod_limbs;
+      uint32_t* dst = c + i * nc;
+      if (batch == 1)
+        par_memcpy(dst, src, ncopy * 4);
+      else
+        memcpy(dst, src, ncopy * 4);
+      for (size_t k = ncopy; k < (size_t)P->prod_limbs; ++k)
+        if (src[k]) over[i] = 1;
+      if (nc > ncopy) memset(dst + ncopy, 0, (nc - ncopy) * 4);
+    };
+    if (batch == 1)
+      row(0);
+    else
+      host_par((size_t)batch, prw * 4, row);
+    ht_mark("copy_out");
+  }
   for (int i = 0; i < batch; ++i)
     if (over[i]) return fail(DKSS_ERANGE, "product %d does not fit nc=%zu limbs", i, nc);
   return DKSS_OK;
@@ -1342,6 +1488,47 @@ int dkss_mul_batch_digits(dkss_plan* P, int batch, const uint32_t* const* a, con
   rc = run_digits_graph(P, batch, sq, nops, ptrs.data(), counts.data(), digit_bits, trusted, c, nc);
   g_ht = nullptr;
   return rc;
+}
+
+int dkss_host_alloc(size_t bytes, void** out) {
+  if (!out || !bytes) return fail(DKSS_EINVAL, "bad argument");
+  *out = nullptr;
+  auto& pool = pinned_pool();
+  {
+    std::lock_guard<std::mutex> lk(pool.mu);
+    auto it = pool.free_.lower_bound(bytes);
+    if (it != pool.free_.end() && it->first <= 2 * bytes) {  // reuse a block of up to twice the size
+      *out = it->second;
+      pool.cached -= it->first;
+      pool.live[it->second] = it->first;
+      pool.free_.erase(it);
+      return DKSS_OK;
+    }
+  }
+  void* p = nullptr;
+  CUCHK(cudaMallocHost(&p, bytes));
+  std::lock_guard<std::mutex> lk(pool.mu);
+  pool.live[p] = bytes;
+  *out = p;
+  return DKSS_OK;
+}
+
+void dkss_host_free(void* p) {
+  if (!p) return;
+  auto& pool = pinned_pool();
+  std::lock_guard<std::mutex> lk(pool.mu);
+  auto it = pool.live.find(p);
+  if (it == pool.live.end()) return;  // not ours
+  const size_t bytes = it->second;
+  pool.live.erase(it);
+  pool.free_.emplace(bytes, p);
+  pool.cached += bytes;
+  while (pool.cached > PinnedPool::kCacheCap && !pool.free_.empty()) {  // release the largest blocks
+    auto big = std::prev(pool.free_.end());
+    pool.cached -= big->first;
+    cudaFreeHost(big->second);
+    pool.free_.erase(big);
+  }
 }
 
 int dkss_mul_digits(dkss_plan* P, const uint32_t* a, size_t na, const uint32_t* b, size_t nb, int digit_bits,

@@ -24,7 +24,7 @@ import threading
 
 import numpy as np
 
-from ._native import DKSS_DIGITS_TRUSTED, DevicePlan
+from ._native import DKSS_DIGITS_TRUSTED, DevicePlan, pinned_empty
 from .plan import DkssPlan, dkss_select_params, ring_products_per_multiply, twiddle_count
 from .words import (Natural, ScratchArena, as_natural, current_arena, foreign_natural, int_to_u32, pylong_digits,
                     u32_to_int, word_bits, words_to_int, PYLONG_DIGIT_BITS)
@@ -306,7 +306,7 @@ def _pipelined_batch(plan, da, db, digit_bits: int, nc: int) -> np.ndarray:
     n = len(da)
     step = -(-n // _PIPE_CHUNKS)
     chunks = [(i, min(n, i + step)) for i in range(0, n, step)]
-    out = np.empty((n, nc), dtype=np.uint32)
+    out = pinned_empty((n, nc))  # the lanes' products land here straight from the device
     device = _device()
 
     def lane_work(lane):
