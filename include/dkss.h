@@ -74,9 +74,13 @@ typedef struct {
 #define DKSS_PASS_CTA 1         /* column pass: one CTA per column tile */
 #define DKSS_PASS_WARP 2        /* column pass: warp per column */
 #define DKSS_PASS_SPLIT 3       /* column DFT kernel + elementwise twiddle kernel */
+#define DKSS_TWIDDLE_AUTO 0     /* tensor cores where the plan allows (m in {16, 32}, L = 4, Proth p) */
+#define DKSS_TWIDDLE_CUDA 1     /* twiddle ring products on the CUDA cores (IMAD.WIDE carry chains) */
+#define DKSS_TWIDDLE_TENSOR 2   /* twiddle ring products on the tensor cores (tcgen05 kind::i8) */
 typedef struct {
   int32_t row_phase; /* DKSS_ROWS_*; ignored by plans that are not two-level */
   int32_t pass_kind; /* DKSS_PASS_* */
+  int32_t twiddle;   /* DKSS_TWIDDLE_*: the engine of the table-twiddle ring products */
 } dkss_plan_opts;
 
 /* plan lifetime -------------------------------------------------------------------- */
@@ -144,6 +148,7 @@ int dkss_mul_device(dkss_plan* plan, int batch, const uint32_t* a_dev, const uin
 #define DKSS_K_DECODE2 5
 #define DKSS_K_ROWS 7 /* row phase in one cluster kernel (levels >= 1, pointwise, inverse levels >= 1) */
 #define DKSS_K_TRANSPOSE 6
+#define DKSS_K_TWIDDLE_TC 8 /* one level's table-twiddle ring products on the tensor cores */
 int dkss_profile_device(dkss_plan* plan, int batch, const uint32_t* a_dev, const uint32_t* b_dev, size_t n_limbs,
                         uint32_t* c_dev, void* stream, int max_launches, int32_t* kinds, float* ms, int64_t* work,
                         int64_t* bytes, int* n_launches);

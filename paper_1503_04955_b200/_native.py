@@ -36,6 +36,7 @@ DKSS_DIGITS_TRUSTED = 0x100  # digit_bits flag: digits already known to fit (inc
 # dkss_plan_opts values (include/dkss.h)
 ROW_PHASES = {"auto": 0, "launches": 1, "persistent": 2, "cluster": 3}
 PASS_KINDS = {"auto": 0, "cta": 1, "warp": 2, "split": 3}
+TWIDDLE_ENGINES = {"auto": 0, "cuda": 1, "tensor": 2}
 
 
 class NativeUnavailable(RuntimeError):
@@ -64,7 +65,7 @@ class PlanInfo(ctypes.Structure):
 
 
 class PlanOpts(ctypes.Structure):
-    _fields_ = [("row_phase", ctypes.c_int32), ("pass_kind", ctypes.c_int32)]
+    _fields_ = [("row_phase", ctypes.c_int32), ("pass_kind", ctypes.c_int32), ("twiddle", ctypes.c_int32)]
 
 
 class FsLayout(ctypes.Structure):
@@ -168,9 +169,10 @@ class DevicePlan:
     """A plan uploaded to one GPU (twiddle table in Montgomery form + workspace)."""
 
     def __init__(self, N: int, M: int, m: int, u: int, p: int, rho_powers, device: int = 0,
-                 row_phase: str = "auto", pass_kind: str = "auto"):
-        """row_phase / pass_kind pick a kernel shape (include/dkss.h dkss_plan_opts); "auto" is the
-        measured-fastest one for the plan, the others exist so every variant can be tested."""
+                 row_phase: str = "auto", pass_kind: str = "auto", twiddle: str = "auto"):
+        """row_phase / pass_kind / twiddle pick a kernel shape (include/dkss.h dkss_plan_opts);
+        "auto" is the measured-fastest one for the plan, the others exist so every variant can be
+        tested (twiddle: "cuda" = IMAD.WIDE ring products, "tensor" = tcgen05 kind::i8)."""
         lib = load()
         self.N, self.M, self.m, self.u, self.p, self.device = N, M, m, u, p, device
         self.L = L = -(-p.bit_length() // 32)
@@ -179,7 +181,7 @@ class DevicePlan:
         rho_l = np.frombuffer(raw, dtype=np.uint32).copy()
         desc = PlanDesc(N, M, m, u, L, _ptr(p_l), _ptr(rho_l))
         h = ctypes.c_void_p()
-        opts = PlanOpts(ROW_PHASES[row_phase], PASS_KINDS[pass_kind])
+        opts = PlanOpts(ROW_PHASES[row_phase], PASS_KINDS[pass_kind], TWIDDLE_ENGINES[twiddle])
         _check(lib.dkss_plan_create_ex(ctypes.byref(desc), ctypes.byref(opts), device, ctypes.byref(h)))
         self._h = h
         self._lib = lib
@@ -246,7 +248,7 @@ class DevicePlan:
         _check(self._lib.dkss_mul_device(self._h, batch, ctypes.c_void_p(a_ptr), ctypes.c_void_p(b_ptr), n_limbs,
                                          ctypes.c_void_p(c_ptr), nc, ctypes.c_void_p(stream)))
 
-    KIND_NAMES = {0: "encode", 1: "fwd_pass", 2: "bottom", 3: "inv_pass", 4: "decode1", 5: "decode2",
+    KIND_NAMES = {0: "encode", 1: "fwd_pass", 2: "bottom", 3: "inv_pass", 4: "decode1", 5: "decode2", 8: "twiddle_tc",
                   6: "transpose", 7: "rows"}
 
     def profile_device(self, batch: int, a_ptr: int, b_ptr: int, n_limbs: int, c_ptr: int, stream: int = 0):

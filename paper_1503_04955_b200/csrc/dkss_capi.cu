@@ -222,6 +222,15 @@ struct GraphKey {
 // re-captures (about 20 us for a two-level plan) instead of growing the cache without bound
 constexpr size_t kGraphCacheCap = 16;
 
+// tensor-core twiddle schedule of one (level, polynomials per launch): tiles of <= 128
+// twiddled elements sharing a table row s, each tile's entries in a 128-slot block
+struct TcSched {
+  uint32_t* d_tiles = nullptr;    // [ntiles][3] s, first entry, count
+  uint32_t* d_entries = nullptr;  // [ntiles][128] (element << 6) | alpha shift
+  int ntiles = 0;
+  long long twiddled = 0;         // elements with s != 0
+};
+
 struct dkss_plan {
   int device = 0;
   long long N = 0;
@@ -243,6 +252,13 @@ struct dkss_plan {
   unsigned* d_dyn = nullptr;        // its ticket + per-row counters (cap_batch rows)
   unsigned long long* d_sglob = nullptr;  // per-limb window sums of a distributed decode
   unsigned* d_tick = nullptr;       // per-launch tile tickets of the CTA kernels, kTickSlots x 2
+  bool tc = false;                  // table twiddles on the tensor cores (dkss_tc.cuh) available
+  bool tc_forced = false;           // DKSS_TWIDDLE_TENSOR: every full-layout launch uses them
+  int tc_grid = 0;                  // SMs (one tensor-core CTA per SM)
+  uint32_t tc_p3 = 0;               // p = 1 + tc_p3 * 2^96
+  uint8_t* d_vtab = nullptr;        // V tables of d_twr rows, [M/m][2m-1][32][16]
+  uint8_t* d_vtab_s = nullptr;      // of the pre-scaled rows d_twr_s (last inverse level)
+  std::map<std::pair<int, int>, TcSched> tc_sched;  // (level, polynomials per launch)
   int tick_next = 0;
   bool dyn_tiles = true;            // DKSS_NO_DYNTILES=1: static round-robin tiles
   void (*rows_fn)(RowsArgs, ModCtx) = nullptr;
@@ -445,6 +461,95 @@ PassArgs pass_args(const dkss_plan* P, const Geom& g, uint32_t* poly, int npoly,
   return A;
 }
 
+// tensor-core twiddle schedule of level lv over `npoly` polynomials of the full layout (built on
+// the host once per (lv, npoly): every element (poly q, instance, j, l) with a table twiddle,
+// e = j l (2m)^lv, s = e mod (M/m) != 0, grouped by s into tiles of <= 128)
+int tc_sched(dkss_plan* P, int lv, int npoly, const TcSched** out) {
+  auto key = std::make_pair(lv, npoly);
+  auto it = P->tc_sched.find(key);
+  if (it != P->tc_sched.end()) {
+    *out = &it->second;
+    return 0;
+  }
+  const long long E = 2LL * P->m, twoM = 2LL * P->M, mu_top = 1LL << P->log_top_mu;
+  const int log_mu = ilog2i(twoM) - P->logE * (lv + 1);
+  const long long mu = 1LL << log_mu, inst = twoM / (E * mu), base_pow = 1LL << (P->logE * lv);
+  if ((long long)npoly * twoM >= (1LL << 26)) return fail(DKSS_EINVAL, "tensor-core schedule: too many elements");
+  std::vector<std::vector<uint32_t>> groups((size_t)mu_top);
+  for (long long q = 0; q < npoly; ++q)
+    for (long long in = 0; in < inst; ++in)
+      for (long long j = 1; j < E; ++j)
+        for (long long l = 1; l < mu; ++l) {
+          const long long e = j * l * base_pow;
+          const long long sr = e & (mu_top - 1);
+          if (!sr) continue;
+          const long long r = (e >> P->log_top_mu) & (E - 1);
+          const long long el = q * twoM + (in << (log_mu + P->logE)) + (j << log_mu) + l;
+          groups[(size_t)sr].push_back((uint32_t)(el << 6 | r));
+        }
+  std::vector<uint32_t> tiles, entries;
+  long long tw = 0;
+  for (long long sr = 1; sr < mu_top; ++sr) {
+    const auto& g = groups[(size_t)sr];
+    tw += (long long)g.size();
+    for (size_t k = 0; k < g.size(); k += kTcRows) {
+      const size_t n = std::min<size_t>(kTcRows, g.size() - k);
+      tiles.push_back((uint32_t)sr);
+      tiles.push_back((uint32_t)entries.size());
+      tiles.push_back((uint32_t)n);
+      entries.insert(entries.end(), g.begin() + (long)k, g.begin() + (long)(k + n));
+      entries.resize(entries.size() + (kTcRows - n), 0u);
+    }
+  }
+  TcSched sc;
+  sc.ntiles = (int)(tiles.size() / 3);
+  sc.twiddled = tw;
+  if (sc.ntiles) {
+    CUCHK(cudaMalloc(&sc.d_tiles, tiles.size() * 4));
+    CUCHK(cudaMalloc(&sc.d_entries, entries.size() * 4));
+    CUCHK(cudaMemcpy(sc.d_tiles, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice));
+    CUCHK(cudaMemcpy(sc.d_entries, entries.data(), entries.size() * 4, cudaMemcpyHostToDevice));
+  }
+  *out = &(P->tc_sched[key] = sc);
+  return 0;
+}
+
+// whether a full-layout launch over `npoly` polynomials takes the tensor-core twiddles: always for
+// m = 32; for m = 16 only from 2^17 elements per launch (2^20 x 2^20, 16384 elements: 96 vs 82 us
+// -- two extra launches per level cost more than the faster products; the 1024 x 2^18 batch:
+// 8.37 vs 11.36 ms)
+constexpr long long kTcMinElems16 = 1LL << 17;
+bool use_tc(const dkss_plan* P, int npoly) {
+  if (!P->tc) return false;
+  return P->tc_forced || P->m >= 32 || (long long)npoly * 2 * P->M >= kTcMinElems16;
+}
+
+// schedules a multiply of `batch` products will use, built before a stream capture starts
+// (their device buffers cannot be allocated inside one)
+int tc_prepare(dkss_plan* P, int batch, bool sq) {
+  const TcSched* sc;
+  int rc;
+  for (int lv = 0; lv < P->levels; ++lv) {
+    if (use_tc(P, (sq ? 1 : 2) * batch) && (rc = tc_sched(P, lv, (sq ? 1 : 2) * batch, &sc))) return rc;
+    if (use_tc(P, batch) && (rc = tc_sched(P, lv, batch, &sc))) return rc;
+  }
+  return 0;
+}
+
+// the table twiddles of level lv on the tensor cores, in place (scaled: the last inverse level)
+int launch_tc(dkss_plan* P, uint32_t* poly, int npoly, int lv, bool scaled, cudaStream_t s) {
+  const TcSched* sc;
+  int rc;
+  if ((rc = tc_sched(P, lv, npoly, &sc))) return rc;
+  if (!sc->ntiles) return 0;
+  TcArgs A{poly, sc->d_tiles, sc->d_entries, scaled ? P->d_vtab_s : P->d_vtab, sc->ntiles, P->tc_p3};
+  const int grid = std::min(sc->ntiles, P->tc_grid);
+  launch_k(P->kt.tc, dim3(grid), dim3(kTcThreads), P->kt.smem_tc, s, A);
+  CUCHK(cudaGetLastError());
+  mark(P, s, DKSS_K_TWIDDLE_TC, rp_work(P, npoly * level_twiddles(P, lv)), 2LL * sc->twiddled * P->m * P->L * 4);
+  return 0;
+}
+
 int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s, const uint32_t* ops_a = nullptr,
                       const uint32_t* ops_b = nullptr, long long na = 0, int enc_split = 0, int lv_lo = 0,
                       int lv_hi = -1, const Geom* geom = nullptr) {
@@ -467,6 +572,11 @@ int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s, c
     // auto mode: the first level (fused encode) runs the CTA-wide kernel, deeper levels may use
     // warp-per-column (batch 1024 x 2^18: forward 6.35 -> 5.95 ms)
     int kind = (lv == 0 && ops_a && !P->pass_mode) ? 1 : pass_kind(P, cols);
+    const bool tc = use_tc(P, npoly) && !geom;  // the four-step layouts keep the CUDA-core twiddles
+    if (tc) {
+      kind = 1;
+      A.tw_skip = 1;
+    }
     if (const char* fk = DKSS_KNOB("DKSS_FWD_KINDS")) {  // experiment: comma-separated kind per level
       int lvl = 0;
       for (const char* c = fk; *c; ++c) {
@@ -495,8 +605,10 @@ int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s, c
       launch_k(P->kt.fwd, dim3(grid), dim3(P->kt.nt), smem_pass(P), s, A, P->mc);
     }
     CUCHK(cudaGetLastError());
-    mark(P, s, DKSS_K_FWD_PASS, (long long)(share * rp_work(P, npoly * level_twiddles(P, lv))),
+    mark(P, s, DKSS_K_FWD_PASS, tc ? 0 : (long long)(share * rp_work(P, npoly * level_twiddles(P, lv))),
          2LL * cols * 2 * P->m * P->m * P->L * 4);
+    int rc;
+    if (tc && (rc = launch_tc(P, poly, npoly, lv, false, s))) return rc;
   }
   return 0;
 }
@@ -513,7 +625,15 @@ int launch_inv_levels(dkss_plan* P, uint32_t* poly, int npoly, bool scale_last, 
     A.scale = (lv == 0 && scale_last) ? 1 : 0;
     // the inverse pass keeps the CTA-wide kernel in auto mode: the warp-per-column inverse needs
     // two column slices per warp (3 CTAs/SM) and measured slower (batch 1024 x 2^18: 4.22 vs 3.89 ms)
-    const int kind = P->pass_mode ? pass_kind(P, cols) : 1;
+    const bool tc = use_tc(P, npoly) && !geom;
+    const int kind = (P->pass_mode && !tc) ? pass_kind(P, cols) : 1;
+    if (tc) {
+      // table twiddles first (the last level with the pre-scaled rows), then the pass multiplies
+      // only the untwiddled elements (scale mode 2) and runs the column DFT
+      int rc;
+      if ((rc = launch_tc(P, poly, npoly, lv, A.scale != 0, s))) return rc;
+      A.tw_skip = 1;
+    }
     if (kind == 1 && A.scale) {
       // CTA-wide kernel: the twiddle products use the scaled rows, only untwiddled elements
       // take an explicit multiply (scale mode 2)
@@ -535,7 +655,7 @@ int launch_inv_levels(dkss_plan* P, uint32_t* poly, int npoly, bool scale_last, 
       launch_k(P->kt.inv, dim3(grid), dim3(P->kt.nt), smem_pass(P), s, A, P->mc);
     }
     CUCHK(cudaGetLastError());
-    mark(P, s, DKSS_K_INV_PASS, (long long)(share * rp_work(P, npoly * level_twiddles(P, lv))),
+    mark(P, s, DKSS_K_INV_PASS, tc ? 0 : (long long)(share * rp_work(P, npoly * level_twiddles(P, lv))),
          2LL * cols * 2 * P->m * P->m * P->L * 4);
   }
   return 0;
@@ -754,8 +874,9 @@ int dkss_plan_create_ex(const dkss_plan_desc* d, const dkss_plan_opts* o, int de
   KTable kt;
   if (!lookup(m, L, &kt)) return fail(DKSS_EINVAL, "no kernels for m=%d, L=%d (m in {8,16,32})", m, L);
   if (opts.row_phase < DKSS_ROWS_AUTO || opts.row_phase > DKSS_ROWS_CLUSTER || opts.pass_kind < DKSS_PASS_AUTO ||
-      opts.pass_kind > DKSS_PASS_SPLIT)
-    return fail(DKSS_EINVAL, "bad plan options (row_phase %d, pass_kind %d)", opts.row_phase, opts.pass_kind);
+      opts.pass_kind > DKSS_PASS_SPLIT || opts.twiddle < DKSS_TWIDDLE_AUTO || opts.twiddle > DKSS_TWIDDLE_TENSOR)
+    return fail(DKSS_EINVAL, "bad plan options (row_phase %d, pass_kind %d, twiddle %d)", opts.row_phase,
+                opts.pass_kind, opts.twiddle);
   CUCHK(cudaSetDevice(device));
   dkss_plan* P = new dkss_plan();
   const int rc = plan_init(P, d, opts, kt, device);
@@ -881,6 +1002,20 @@ int plan_init(dkss_plan* P, const dkss_plan_desc* d, const dkss_plan_opts& opts,
       P->grid_tw = sms * std::max(ot, 1);
     }
     P->pass_mode = opts.pass_kind;
+    // table twiddles on the tensor cores: kernels exist for m in {16, 32} at L = 4, the epilogue
+    // needs a Proth prime p = 1 + p3 2^96, and the split column passes are CTA kernels
+    {
+      const bool tc_ok = kt.tc && L == 4 && P->mc.proth && P->levels >= 1 && d->p[1] == 0 && d->p[2] == 0;
+      if (opts.twiddle == DKSS_TWIDDLE_TENSOR && !tc_ok)
+        return fail(DKSS_EINVAL, "tensor-core twiddles need m in {16, 32}, L = 4 and a Proth prime (m=%d L=%d)", m, L);
+      P->tc = tc_ok && opts.twiddle != DKSS_TWIDDLE_CUDA && P->pass_mode <= DKSS_PASS_CTA;
+      P->tc_forced = P->tc && opts.twiddle == DKSS_TWIDDLE_TENSOR;
+      if (P->tc) {
+        P->tc_p3 = d->p[3];
+        P->tc_grid = sms;
+        CUCHK(cudaFuncSetAttribute((const void*)kt.tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kt.smem_tc));
+      }
+    }
     // row phase in one cluster kernel: two column levels, base length b = cluster size.
     // Opt-in (DKSS_ROWS_CLUSTER): measured slower than the three persistent launches it replaces
     // -- second-level column 0 has no twiddles, so one CTA of every
@@ -888,7 +1023,7 @@ int plan_init(dkss_plan* P, const dkss_plan_desc* d, const dkss_plan_opts& opts,
     // lockstep where the persistent kernels overlap tiles
     const int b = P->base_len;
     const int ri = b == 2 ? 1 : b == 4 ? 2 : b == 8 ? 3 : b == 16 ? 4 : 0;
-    if (P->levels == 2 && ri && kt.rows[ri] && opts.row_phase == DKSS_ROWS_CLUSTER) {
+    if (!P->tc && P->levels == 2 && ri && kt.rows[ri] && opts.row_phase == DKSS_ROWS_CLUSTER) {
       auto fn = kt.rows[ri];
       bool ok = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kt.smem_rows) ==
                 cudaSuccess;
@@ -921,7 +1056,7 @@ int plan_init(dkss_plan* P, const dkss_plan_desc* d, const dkss_plan_opts& opts,
     // measured faster.  DKSS_ROWS_PERSISTENT forces it on, DKSS_ROWS_LAUNCHES off.
     const bool want_dyn = opts.row_phase == DKSS_ROWS_PERSISTENT ||
                           (opts.row_phase == DKSS_ROWS_AUTO && m == 32 && P->base_len >= 4 && P->base_len <= 16);
-    if (!P->rows_cs && P->levels == 2 && kt.dyn && want_dyn &&
+    if (!P->tc && !P->rows_cs && P->levels == 2 && kt.dyn && want_dyn &&
         (1LL << P->log_top_mu) % kt.ne == 0) {
       CUCHK(cudaFuncSetAttribute((const void*)kt.dyn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kt.smem_dyn));
       int od = 0;
@@ -987,6 +1122,28 @@ int plan_init(dkss_plan* P, const dkss_plan_desc* d, const dkss_plan_opts& opts,
         tw_s, P->d_twr_s, (long long)(M / m), m, P->mc);
     e = cudaGetLastError();
   }
+  if (e == cudaSuccess && P->tc) {
+    // V tables of the tensor-core twiddles, from the expanded rows; c160 = 2^160 mod p
+    Limbs c(L, 0);
+    c[0] = 1;
+    for (int i = 0; i < 160; ++i) dbl_mod(c, p);
+    uint32_t* d_c = nullptr;
+    const size_t vbytes = (size_t)(M / m) * kt.tc_vbytes;
+    e = cudaMalloc(&d_c, 4 * L);
+    if (e == cudaSuccess) e = cudaMemcpy(d_c, c.data(), 4 * L, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_vtab, vbytes);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_vtab_s, vbytes);
+    const int gb = (int)std::min<long long>(((long long)(M / m) * (2 * m - 1) + 127) / 128, 4096);
+    if (e == cudaSuccess) {
+      count_launch();
+      kt.tc_build<<<gb, 128, 0, P->stream>>>(P->d_twr, (long long)(M / m), P->d_vtab, P->mc, d_c);
+      count_launch();
+      kt.tc_build<<<gb, 128, 0, P->stream>>>(P->d_twr_s, (long long)(M / m), P->d_vtab_s, P->mc, d_c);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(P->stream);
+    cudaFree(d_c);
+  }
   if (e == cudaSuccess) e = cudaStreamSynchronize(P->stream);
   cudaFree(tw_s);
   if (e != cudaSuccess) return fail(DKSS_ECUDA, "plan upload failed: %s", cudaGetErrorString(e));
@@ -1004,6 +1161,12 @@ void dkss_plan_destroy(dkss_plan* P) {
   cudaFree(P->d_twr);
   cudaFree(P->d_twr_s);
   cudaFree(P->d_tick);
+  cudaFree(P->d_vtab);
+  cudaFree(P->d_vtab_s);
+  for (auto& kv : P->tc_sched) {
+    cudaFree(kv.second.d_tiles);
+    cudaFree(kv.second.d_entries);
+  }
   if (P->h_pin) cudaFreeHost(P->h_pin);
   cudaFree(P->d_stage);
   cudaFree(P->d_sglob);
@@ -1029,7 +1192,8 @@ int dkss_plan_get_info(const dkss_plan* P, dkss_plan_info* o) {
     const bool self = !knob_on(DKSS_KNOB("DKSS_NO_SELFSCAN")) && dec_blocks(P) <= kSelfScanBlocks;
     const int dec = self ? 2 : 3;  // decode1 + (self-scanning apply | scan + apply)
     o->launches_per_mul =
-        (P->rows_cs || P->dyn_grid) ? 1 + 1 + 1 + dec : (P->levels > 0 ? 0 : 2) + P->levels + 1 + P->levels + dec;
+        (P->rows_cs || P->dyn_grid) ? 1 + 1 + 1 + dec
+                                    : (P->levels > 0 ? 0 : 2) + P->levels * (use_tc(P, 2) ? 2 : 1) * 2 + 1 + dec;
   }
   o->workspace_bytes = (int64_t)P->ws_bytes;
   o->footprint_bytes = dkss_footprint_bytes(P->N, P->M, P->m, P->L);
@@ -1047,6 +1211,7 @@ int launch_graph(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, 
   GraphKey key{batch, a, b, c, nl, nc};
   auto* ent = P->graphs.find(key);
   if (!ent) {
+    if ((rc = tc_prepare(P, batch, b == nullptr))) return rc;
     cudaStream_t cap;
     CUCHK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     CUCHK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
@@ -1353,6 +1518,7 @@ int run_digits_graph(dkss_plan* P, int batch, bool sq, int nops, const uint32_t*
   auto key = std::make_tuple(batch, sq, digit_bits);
   auto* ent = P->dgraphs.find(key);
   if (!ent) {
+    if ((rc = tc_prepare(P, batch, sq))) return rc;
     cudaStream_t cap_s;
     CUCHK(cudaStreamCreateWithFlags(&cap_s, cudaStreamNonBlocking));
     CUCHK(cudaStreamBeginCapture(cap_s, cudaStreamCaptureModeThreadLocal));
@@ -1737,6 +1903,8 @@ int dkss_decode_device(dkss_plan* P, const uint32_t* v, uint32_t* out, size_t nc
 namespace {
 int ll_graph(dkss_plan* P, long long p, int k, GraphLru<std::pair<long long, int>>::Ent** out) {
   if ((*out = P->ll_graphs.find({p, k}))) return 0;
+  int rc0;
+  if ((rc0 = tc_prepare(P, 1, true))) return rc0;
   cudaStream_t cap;
   CUCHK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
   CUCHK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));

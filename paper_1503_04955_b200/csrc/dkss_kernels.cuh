@@ -463,6 +463,8 @@ struct PassArgs {
   int M;                 // outer length (elements e >= M are zero)
   int wpc;               // warp-per-column kernels: warps sharing one column (power of 2)
   unsigned* ctr;         // CTA kernels: tile tickets of this launch (null: static round-robin)
+  int tw_skip;           // CTA kernels: elements with a table twiddle (s != 0) pass through
+                         // untouched -- the tensor-core kernel (dkss_tc.cuh) multiplies them
 };
 
 template <int MM>
@@ -512,7 +514,7 @@ __device__ __forceinline__ void issue_pass_tile(const PassArgs& A, long long til
         long long l;
         col_elem(A, cg, 0, LOGE, 0, &l);
         int r;
-        if (tw_exp(A, e % E, l, &r)) bytes += TB;
+        if (!A.tw_skip && tw_exp(A, e % E, l, &r)) bytes += TB;
       }
     }
     bytes = __reduce_add_sync(0xFFFFFFFFu, bytes);
@@ -530,7 +532,7 @@ __device__ __forceinline__ void issue_pass_tile(const PassArgs& A, long long til
       const int slot = FWD ? c * E + bitrev_n(j, LOGE) : e;
       if (load_elems && (part & 2)) bulk_g2s(buf + slot * ES, A.poly + off, EB, bar);
     } else if constexpr (Cfg<MM>::TWS) {
-      if (!(part & 1)) continue;
+      if (!(part & 1) || A.tw_skip) continue;
       int r;
       const long long s = tw_exp(A, j, l, &r);
       if (s) bulk_g2s(tws + e * EST, A.twr + s * (2 * MM * L), TB, bar);
@@ -645,7 +647,8 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArg
       int r;
       const long long s = tw_exp(A, vv, l, &r);
       uint32_t w[kT][L];
-      if (s == 0 || kExpNoMac) {
+      if (s == 0 || kExpNoMac || A.tw_skip) {
+        if (s != 0) r = 0;  // tw_skip: the tensor-core kernel applies rho^e (rotation included)
 #pragma unroll
         for (int t = 0; t < kT; ++t) ld_res<L>(w[t], xv + el * ES + (k0 + t) * L);
       } else {
@@ -712,7 +715,11 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArg
       long long l;
       col_elem(A, cg, 0, LOGE, 0, &l);
       const long long s = tw_exp(A, j, l, &rot[q]);
-      if (s == 0) {
+      if (s != 0 && A.tw_skip) {  // already multiplied (and rotated) by the tensor-core kernel
+        rot[q] = 0;
+#pragma unroll
+        for (int t = 0; t < kT; ++t) ld_res<L>(res[q][t], buf + el * ES + (k0 + t) * L);
+      } else if (s == 0) {
 #pragma unroll
         for (int t = 0; t < kT; ++t) ld_res<L>(res[q][t], buf + el * ES + (k0 + t) * L);
         if (A.scale == 2) {

@@ -5,6 +5,7 @@
 #include "dkss_warp.cuh"
 #include "dkss_rows.cuh"
 #include "dkss_dyn.cuh"
+#include "dkss_tc.cuh"
 
 namespace dkss {
 
@@ -35,6 +36,11 @@ struct KTable {
   // (dkss_dyn.cuh); null for m = 8
   void (*dyn)(DynArgs, ModCtx);
   size_t smem_dyn;
+  // twiddle products on the tensor cores (dkss_tc.cuh): m in {16, 32}, L = 4 only, else null
+  void (*tc)(TcArgs);
+  void (*tc_build)(const uint32_t*, long long, uint8_t*, ModCtx, const uint32_t*);
+  size_t smem_tc;
+  size_t tc_vbytes;  // bytes of one V table row set (per twiddle row s)
 };
 
 template <int MM, int L>
@@ -65,6 +71,12 @@ KTable make_table() {
       t.dyn = k_rows_dyn<MM, L>;
       t.smem_dyn = DynSmem<MM, L>::WORDS * 4;
     }
+  }
+  if constexpr (L == 4 && (MM == 16 || MM == 32)) {
+    t.tc = k_tc_twiddle<MM>;
+    t.tc_build = k_tc_build_v<MM>;
+    t.smem_tc = TcSmem<MM>::BYTES;
+    t.tc_vbytes = TcSmem<MM>::VBYTES;
   }
   t.rmul = k_rmul<MM, L>;
   t.mscale = k_mont_scale<L>;

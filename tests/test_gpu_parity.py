@@ -316,9 +316,11 @@ def test_square_batch_and_all_ones(cuda_ok):
     assert [g.to_int() for g in got] == [x * x for x in xs]
 
 
-@pytest.mark.parametrize("row_phase,pass_kind", [("persistent", "auto"), ("launches", "auto"), ("cluster", "auto"),
-                                                  ("launches", "warp"), ("launches", "split"), ("auto", "cta")])
-def test_kernel_shape_variants(cuda_ok, row_phase, pass_kind):
+@pytest.mark.parametrize("row_phase,pass_kind,twiddle", [
+    ("persistent", "auto", "cuda"), ("launches", "auto", "cuda"), ("cluster", "auto", "cuda"),
+    ("launches", "warp", "cuda"), ("launches", "split", "cuda"), ("auto", "cta", "cuda"),
+    ("auto", "auto", "tensor"), ("auto", "auto", "auto")])
+def test_kernel_shape_variants(cuda_ok, row_phase, pass_kind, twiddle):
     # every kernel shape a plan can be built with (include/dkss.h dkss_plan_opts) gives the same
     # products: two-level sizes of both inner lengths, squares and a batch
     from paper_1503_04955_b200._native import DevicePlan
@@ -329,7 +331,7 @@ def test_kernel_shape_variants(cuda_ok, row_phase, pass_kind):
         N = 1 << e
         pl = P.dkss_select_params(N)
         dp = DevicePlan(plan_capacity(pl), pl.M, pl.m, pl.u, pl.p, pl.rho_powers, 0, row_phase=row_phase,
-                        pass_kind=pass_kind)
+                        pass_kind=pass_kind, twiddle=twiddle)
         nl, npl = dp.info["operand_limbs"], dp.info["product_limbs"]
         a, b = r.getrandbits(N), r.getrandbits(N)
         A, B = int_to_u32(a, nl), int_to_u32(b, nl)
@@ -398,3 +400,32 @@ def test_dmul_beyond_the_configs_residues(cuda_ok, e):
             primes.append(q)
     for q in primes:
         assert c % q == (a % q) * (b % q) % q
+
+
+@pytest.mark.parametrize("e", [16, 18, 20, 22, 24])
+def test_tensor_core_twiddles_match_cuda_cores(cuda_ok, e):
+    # the same transform with the table twiddles on the tensor cores (tcgen05 kind::i8, dkss_tc.cuh)
+    # and on the CUDA cores (IMAD.WIDE ring_mul): identical stage outputs and products
+    from paper_1503_04955_b200._native import DevicePlan
+    from paper_1503_04955_b200.dkss import plan_capacity
+
+    N = 1 << e
+    pl = P.dkss_select_params(N)
+    mk = lambda tw: DevicePlan(plan_capacity(pl), pl.M, pl.m, pl.u, pl.p, pl.rho_powers, 0, twiddle=tw)  # noqa: E731
+    tcp, cup = mk("tensor"), mk("cuda")
+    rng = random.Random(e)
+    nl, npl = tcp.info["operand_limbs"], tcp.info["product_limbs"]
+    a, b = rng.getrandbits(N) | 1 << (N - 1), rng.getrandbits(N) | 1 << (N - 1)
+    ea = tcp.encode(int_to_u32(a, nl))
+    assert np.array_equal(tcp.fft(ea), cup.fft(ea))
+    if e <= 20:
+        o = OraclePlan(pl)
+        assert np.array_equal(tcp.fft(ea), o.fft(ea))
+    A, B = int_to_u32(a, nl), int_to_u32(b, nl)
+    c = tcp.mul_limbs(A, B, npl)
+    assert np.array_equal(c, cup.mul_limbs(A, B, npl))
+    assert u32_to_int(c) == a * b
+    ones = int_to_u32((1 << N) - 1, nl)
+    assert u32_to_int(tcp.mul_limbs(ones, ones, npl)) == ((1 << N) - 1) ** 2
+    tcp.close()
+    cup.close()

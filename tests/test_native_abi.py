@@ -51,7 +51,8 @@ def test_bad_plan_options_rejected_before_any_device_work():
     rho = np.frombuffer(b"".join(c.to_bytes(4 * L, "little") for row in pl.rho_powers for c in row),
                         dtype=np.uint32).copy()
     desc = _native.PlanDesc(pl.N, pl.M, pl.m, pl.u, L, _native._ptr(p), _native._ptr(rho))
-    for opts in (_native.PlanOpts(9, 0), _native.PlanOpts(0, -1), _native.PlanOpts(-1, 0)):
+    for opts in (_native.PlanOpts(9, 0, 0), _native.PlanOpts(0, -1, 0), _native.PlanOpts(-1, 0, 0),
+                 _native.PlanOpts(0, 0, 7)):
         h = ctypes.c_void_p()
         rc = lib.dkss_plan_create_ex(ctypes.byref(desc), ctypes.byref(opts), 0, ctypes.byref(h))
         assert rc == _native.DKSS_EINVAL and not h.value
