@@ -1005,7 +1005,8 @@ int plan_init(dkss_plan* P, const dkss_plan_desc* d, const dkss_plan_opts& opts,
     // table twiddles on the tensor cores: kernels exist for m in {16, 32} at L = 4, the epilogue
     // needs a Proth prime p = 1 + p3 2^96, and the split column passes are CTA kernels
     {
-      const bool tc_ok = kt.tc && L == 4 && P->mc.proth && P->levels >= 1 && d->p[1] == 0 && d->p[2] == 0;
+      const bool tc_ok = kt.tc && L == 4 && P->mc.proth && P->levels >= 1 && d->p[1] == 0 && d->p[2] == 0 &&
+                         d->p[3] >= 64u;  // p > 2^102: the epilogue's single conditional subtraction
       if (opts.twiddle == DKSS_TWIDDLE_TENSOR && !tc_ok)
         return fail(DKSS_EINVAL, "tensor-core twiddles need m in {16, 32}, L = 4 and a Proth prime (m=%d L=%d)", m, L);
       P->tc = tc_ok && opts.twiddle != DKSS_TWIDDLE_CUDA && P->pass_mode <= DKSS_PASS_CTA;

@@ -19,11 +19,12 @@
 // strides (SBO 128 B between 8-row groups, LBO 512 B between K chunks): 32 KB of shared memory
 // for the whole 32m x 16m Toeplitz operand (m = 32).
 //
-// Epilogue (CUDA cores, one thread per element row): tcgen05.ld of the 32 byte-position sums of
-// a coefficient, one 288-bit signed integer, + p 2^160, five Montgomery REDC steps with
-// R = 2^160 using p = 1 + P3 2^96 (Proth: -p^-1 = -1 mod 2^32, q p touches limbs 0, 3, 4),
-// canonical, then stored at (j + r) mod 2m with the negation of alpha^m = -1 -- the same
-// element the CUDA-core kernels' ring_mul + store_rot produce (tests/test_gpu_parity.py).
+// Epilogue (CUDA cores, one thread per element row and coefficient): tcgen05.ld of the 32
+// byte-position sums of a coefficient, folded into a nine-limb non-negative integer with three
+// IMAD.WIDE per limb, five Montgomery REDC steps with R = 2^160 using p = 1 + P3 2^96 (Proth:
+// -p^-1 = -1 mod 2^32, q p touches limbs K, K+3, K+4), one conditional subtraction, then stored
+// at (j + r) mod 2m with the negation of alpha^m = -1 -- the same element the CUDA-core kernels'
+// ring_mul + store_rot produce (tests/test_gpu_parity.py).
 #pragma once
 #include <cstdint>
 #include "dkss_kernels.cuh"
@@ -32,7 +33,9 @@ namespace dkss {
 
 constexpr int kTcRows = 128;     // UMMA M
 constexpr int kTcNChunk = 256;   // UMMA N per instruction and per TMEM buffer
-constexpr int kTcThreads = 256;  // 8 warps: loads and epilogue; thread 0 issues the MMAs
+constexpr int kTcEpiWarps = 16;  // epilogue: 4 per TMEM lane quadrant
+constexpr int kTcProdWarps = 2;  // smem producers (element gather + V bulk copy)
+constexpr int kTcThreads = (kTcEpiWarps + kTcProdWarps + 1) * 32;  // + one MMA-issue warp
 
 struct TcArgs {
   uint32_t* poly;            // element index 0 of the launch (elements of MM * 4 words)
@@ -102,6 +105,27 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* mbar, uint32_t phase)
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
+__device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(mbar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(mbar)), "r"(bytes)
+               : "memory");
+}
+
+// bulk copy global -> shared (TMA engine), completion counted in bytes on mbar
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(sdst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(mbar))
+               : "memory");
+}
+
 __device__ __forceinline__ void cp16(void* sdst, const void* gsrc, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(sdst)), "l"(gsrc),
                "r"(valid ? 16 : 0)
@@ -120,223 +144,258 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
-// z = (sum_d Z[d] 256^d + p 2^160) 2^-160 mod p, canonical, for p = 1 + p3 2^96 (L = 4)
-__device__ __forceinline__ void reduce_coeff(const int32_t (&Z)[32], uint32_t p3, uint32_t (&out)[4]) {
-  long long acc[9];
-#pragma unroll
-  for (int w = 0; w < 9; ++w) acc[w] = 0;
-#pragma unroll
-  for (int d = 0; d < 32; ++d) acc[d >> 2] += (long long)Z[d] << (8 * (d & 3));
-  uint32_t t[10];
-#pragma unroll
-  for (int w = 0; w < 8; ++w) {
-    acc[w + 1] += acc[w] >> 32;  // arithmetic shift: carries and borrows
-    t[w] = (uint32_t)acc[w];
-  }
-  // + p 2^160 = 2^160 + p3 2^256 (limb 5 += 1, limb 8 += p3): non-negative, < 2^288
-  long long top = acc[8] + (long long)p3;
-  {
-    unsigned long long s = (unsigned long long)t[5] + 1u;
-    t[5] = (uint32_t)s;
-    unsigned long long c = s >> 32;
-    s = (unsigned long long)t[6] + c;
-    t[6] = (uint32_t)s;
-    c = s >> 32;
-    s = (unsigned long long)t[7] + c;
-    t[7] = (uint32_t)s;
-    top += (long long)(s >> 32);
-  }
-  t[8] = (uint32_t)top;
-  t[9] = (uint32_t)((unsigned long long)top >> 32);
-#pragma unroll
-  for (int step = 0; step < 5; ++step) {  // REDC: q = -t0, t += q p, t >>= 32
-    const uint32_t q = 0u - t[0];
-    unsigned long long c = (t[0] != 0u) ? 1ull : 0ull;
-    const unsigned long long hq = (unsigned long long)q * p3;
-    unsigned long long s = (unsigned long long)t[1] + c;
-    t[1] = (uint32_t)s;
-    c = s >> 32;
-    s = (unsigned long long)t[2] + c;
-    t[2] = (uint32_t)s;
-    c = s >> 32;
-    s = (unsigned long long)t[3] + (uint32_t)hq + c;
-    t[3] = (uint32_t)s;
-    c = s >> 32;
-    s = (unsigned long long)t[4] + (hq >> 32) + c;
-    t[4] = (uint32_t)s;
-    c = s >> 32;
-#pragma unroll
-    for (int w = 5; w < 10; ++w) {
-      s = (unsigned long long)t[w] + c;
-      t[w] = (uint32_t)s;
-      c = s >> 32;
-    }
-#pragma unroll
-    for (int w = 0; w < 9; ++w) t[w] = t[w + 1];
-    t[9] = 0;
-  }
-  // t < 2^128 + p < 3p: subtract p while that does not borrow
-#pragma unroll
-  for (int it = 0; it < 2; ++it) {
-    uint32_t r[5], b;
-    r[0] = t[0] - 1u;
-    b = t[0] < 1u;
-    r[1] = t[1] - b;
-    b = t[1] < b;
-    r[2] = t[2] - b;
-    b = t[2] < b;
-    r[3] = t[3] - p3 - b;
-    b = (unsigned long long)t[3] < (unsigned long long)p3 + b;
-    r[4] = t[4] - b;
-    b = t[4] < b;
-    if (!b) {
-#pragma unroll
-      for (int q = 0; q < 5; ++q) t[q] = r[q];
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) out[q] = t[q];
+// the same load without the wait (several loads, then one tcgen05.wait::ld)
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, int32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr)
+      : "memory");
 }
 
-// p - z (z canonical; 0 stays 0)
-__device__ __forceinline__ void neg_p(uint32_t (&z)[4], uint32_t p3) {
-  if ((z[0] | z[1] | z[2] | z[3]) == 0u) return;
-  uint32_t b;
-  const uint32_t r0 = 1u - z[0];
-  b = z[0] > 1u;
-  const uint32_t r1 = 0u - z[1] - b;
-  b = (z[1] | b) != 0u;
-  const uint32_t r2 = 0u - z[2] - b;
-  b = (z[2] | b) != 0u;
-  const uint32_t r3 = p3 - z[3] - b;
-  z[0] = r0;
-  z[1] = r1;
-  z[2] = r2;
-  z[3] = r3;
+// the five Montgomery steps of the epilogue REDC (p = 1 + p3 2^96, so -p^-1 = -1 mod 2^32 and
+// q p = q + q p3 2^96): step K adds q = -t[K] at limb K (clearing it) and q p3 at limbs K+3, K+4,
+// with one carry chain through limb 9
+__device__ __forceinline__ void redc5(uint32_t (&t)[10], uint32_t p3) {
+  {  // step 0: limbs 0..9
+    const uint32_t q = 0u - t[0];
+    asm("add.cc.u32 %0, %0, %10;\n\taddc.cc.u32 %1, %1, 0;\n\taddc.cc.u32 %2, %2, 0;\n\tmadc.lo.cc.u32 %3, %10, %11, %3;\n\tmadc.hi.cc.u32 %4, %10, %11, %4;\n\taddc.cc.u32 %5, %5, 0;\n\taddc.cc.u32 %6, %6, 0;\n\taddc.cc.u32 %7, %7, 0;\n\taddc.cc.u32 %8, %8, 0;\n\taddc.u32 %9, %9, 0;\n"
+        : "+r"(t[0]), "+r"(t[1]), "+r"(t[2]), "+r"(t[3]), "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), "+r"(t[8]), "+r"(t[9])
+        : "r"(q), "r"(p3));
+  }
+  {  // step 1: limbs 1..9
+    const uint32_t q = 0u - t[1];
+    asm("add.cc.u32 %0, %0, %9;\n\taddc.cc.u32 %1, %1, 0;\n\taddc.cc.u32 %2, %2, 0;\n\tmadc.lo.cc.u32 %3, %9, %10, %3;\n\tmadc.hi.cc.u32 %4, %9, %10, %4;\n\taddc.cc.u32 %5, %5, 0;\n\taddc.cc.u32 %6, %6, 0;\n\taddc.cc.u32 %7, %7, 0;\n\taddc.u32 %8, %8, 0;\n"
+        : "+r"(t[1]), "+r"(t[2]), "+r"(t[3]), "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), "+r"(t[8]), "+r"(t[9])
+        : "r"(q), "r"(p3));
+  }
+  {  // step 2: limbs 2..9
+    const uint32_t q = 0u - t[2];
+    asm("add.cc.u32 %0, %0, %8;\n\taddc.cc.u32 %1, %1, 0;\n\taddc.cc.u32 %2, %2, 0;\n\tmadc.lo.cc.u32 %3, %8, %9, %3;\n\tmadc.hi.cc.u32 %4, %8, %9, %4;\n\taddc.cc.u32 %5, %5, 0;\n\taddc.cc.u32 %6, %6, 0;\n\taddc.u32 %7, %7, 0;\n"
+        : "+r"(t[2]), "+r"(t[3]), "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), "+r"(t[8]), "+r"(t[9])
+        : "r"(q), "r"(p3));
+  }
+  {  // step 3: limbs 3..9
+    const uint32_t q = 0u - t[3];
+    asm("add.cc.u32 %0, %0, %7;\n\taddc.cc.u32 %1, %1, 0;\n\taddc.cc.u32 %2, %2, 0;\n\tmadc.lo.cc.u32 %3, %7, %8, %3;\n\tmadc.hi.cc.u32 %4, %7, %8, %4;\n\taddc.cc.u32 %5, %5, 0;\n\taddc.u32 %6, %6, 0;\n"
+        : "+r"(t[3]), "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), "+r"(t[8]), "+r"(t[9])
+        : "r"(q), "r"(p3));
+  }
+  {  // step 4: limbs 4..9
+    const uint32_t q = 0u - t[4];
+    asm("add.cc.u32 %0, %0, %6;\n\taddc.cc.u32 %1, %1, 0;\n\taddc.cc.u32 %2, %2, 0;\n\tmadc.lo.cc.u32 %3, %6, %7, %3;\n\tmadc.hi.cc.u32 %4, %6, %7, %4;\n\taddc.u32 %5, %5, 0;\n"
+        : "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), "+r"(t[8]), "+r"(t[9])
+        : "r"(q), "r"(p3));
+  }
 }
+
+// z = (sum_d Z[d] 256^d) 2^-160 mod p, canonical, for p = 1 + p3 2^96 (L = 4), p3 >= 2^6.
+// The sum is the exact integer sum_i x_i T'_i with x_i < 2^128 (the element's bytes, unsigned)
+// and T'_i in [0, p) (the balanced digits only change how T' is written), so it is in
+// [0, m 2^128 p) subset [0, 2^261): nine limbs.  Five REDC steps give r = (V + Q p) / 2^160 <
+// 2^101 + p < min(2p, 2^128): t[9] ends 0 and one conditional subtraction makes r canonical.
+__device__ __forceinline__ void reduce_coeff(const int32_t (&Z)[32], uint32_t p3, bool neg, uint32_t (&out)[4]) {
+  uint32_t t[10];
+  long long c = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {  // 64-bit sums of four byte positions, carried into 32-bit limbs
+    long long a = (long long)Z[4 * k];
+    asm("mad.wide.s32 %0, %1, 256, %0;" : "+l"(a) : "r"(Z[4 * k + 1]));
+    asm("mad.wide.s32 %0, %1, 65536, %0;" : "+l"(a) : "r"(Z[4 * k + 2]));
+    asm("mad.wide.s32 %0, %1, 16777216, %0;" : "+l"(a) : "r"(Z[4 * k + 3]));
+    a += c;
+    t[k] = (uint32_t)a;
+    c = a >> 32;
+  }
+  t[8] = (uint32_t)c;
+  t[9] = 0;
+  redc5(t, p3);
+  // r = t[5..8] < 2^101 + p: subtract p once if r >= p; then p - r when `neg` (alpha^m = -1 wrap)
+  uint32_t r0, r1, r2, r3, bo;
+  asm("sub.cc.u32 %0, %5, 1;\n\tsubc.cc.u32 %1, %6, 0;\n\tsubc.cc.u32 %2, %7, 0;\n\t"
+      "subc.cc.u32 %3, %8, %9;\n\tsubc.u32 %4, 0, 0;\n"
+      : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3), "=r"(bo)
+      : "r"(t[5]), "r"(t[6]), "r"(t[7]), "r"(t[8]), "r"(p3));
+  const bool keep = bo != 0u;  // borrow: r < p
+  const uint32_t c0 = keep ? t[5] : r0, c1 = keep ? t[6] : r1, c2 = keep ? t[7] : r2, c3 = keep ? t[8] : r3;
+  uint32_t e0, e1, e2, e3;
+  asm("sub.cc.u32 %0, 1, %4;\n\tsubc.cc.u32 %1, 0, %5;\n\tsubc.cc.u32 %2, 0, %6;\n\tsubc.u32 %3, %8, %7;\n"
+      : "=r"(e0), "=r"(e1), "=r"(e2), "=r"(e3)
+      : "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(p3));
+  const bool flip = neg && ((c0 | c1 | c2 | c3) != 0u);
+  out[0] = flip ? e0 : c0;
+  out[1] = flip ? e1 : c1;
+  out[2] = flip ? e2 : c2;
+  out[3] = flip ? e3 : c3;
+}
+
 
 }  // namespace tc
 
-// Grouped twiddle products of one level, in place (see the file comment).  Persistent CTAs
-// walk the tile list; tile t + 1's elements, V table and entries are prefetched (cp.async)
-// while tile t multiplies; within a tile the N chunks alternate between two TMEM buffers so
-// the epilogue of chunk c overlaps the MMAs of chunk c + 1.
+// Grouped twiddle products of one level, in place (see the file comment).  Persistent CTAs walk
+// the tile list with warp-specialised roles and mbarrier pipelines (no CTA-wide barriers in the
+// loop):
+//   producer warps (kTcProdWarps): gather tile k's elements into smem stage k & 1 with 16-byte
+//     cp.async (8 rows x 64 contiguous bytes per instruction: coalesced reads, conflict-free
+//     writes), the tile's V table with one bulk copy; stage reuse waits on the MMA's commit;
+//   MMA warp (one thread): per N chunk, waits for a free TMEM buffer, issues the K steps,
+//     commits to the buffer's "full" barrier, and after the tile's last chunk to the stage's
+//     "empty" barrier;
+//   epilogue warps (kTcEpiWarps): per chunk, tcgen05.ld of their coefficient columns, release the
+//     TMEM buffer, then reduce (tc::reduce_coeff) and store.
 template <int MM>
 __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
   griddep_wait();  // PDL: the column pass that produced the elements has completed
   griddep_launch();
   using S = TcSmem<MM>;
   constexpr int K = S::K, NCH = MM * 32 / kTcNChunk, KSTEPS = K / 32;
-  constexpr int SBO_A = MM * 128;  // bytes between 8-row groups of A
+  constexpr int SBO_A = MM * 128;      // bytes between 8-row groups of A
   constexpr int CPC = kTcNChunk / 32;  // coefficients per N chunk
   constexpr int EW = MM * 4;           // words per element
+  constexpr int CPE = CPC / 4;         // coefficients per epilogue warp per chunk (4 lane quadrants)
+  static_assert(kTcEpiWarps == 16 && CPC == 8, "two coefficient columns per epilogue warp per chunk");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t mbar[2];
+  // full[2], empty[2] (smem stages), tfull[2], tempty[2] (TMEM buffers)
+  __shared__ __align__(8) uint64_t bars[8];
   __shared__ uint32_t tmem_sh;
+  uint64_t* full = bars;
+  uint64_t* empty = bars + 2;
+  uint64_t* tfull = bars + 4;
+  uint64_t* tempty = bars + 6;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tc::smem_u32(&tmem_sh)),
                  "r"(2 * kTcNChunk));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(tc::smem_u32(&mbar[0])) : "memory");
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(tc::smem_u32(&mbar[1])) : "memory");
+  if (threadIdx.x == 32) {
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&full[i], kTcProdWarps * 32 + 1);  // every producer lane + the V expect-tx
+      tc::mbar_init(&empty[i], 1);
+      tc::mbar_init(&tfull[i], 1);
+      tc::mbar_init(&tempty[i], kTcEpiWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_sh;
-  const uint32_t idesc = tc::make_idesc(kTcRows, kTcNChunk);
-  uint32_t ph[2] = {0u, 0u};
+  const int G = gridDim.x;
 
-  // stage `st` <- tile t: the elements (reversed coefficient chunks, zero rows past the count),
-  // the tile's V table and its entries
-  auto prefetch = [&](int t, int st) {
-    uint8_t* sA = smem + st * S::STAGE;
-    uint8_t* sV = sA + S::ABYTES;
-    uint32_t* sE = reinterpret_cast<uint32_t*>(sV + S::VPAD);
-    const uint32_t s = A.tiles[3 * t], first = A.tiles[3 * t + 1], cnt = A.tiles[3 * t + 2];
-    for (int i = threadIdx.x; i < kTcRows / 4; i += kTcThreads)
-      tc::cp16(sE + 4 * i, A.entries + first + 4 * i, (uint32_t)(4 * i) < cnt);
-    const uint8_t* vsrc = A.vtab + (size_t)s * S::VBYTES;
-    for (int i = threadIdx.x; i < S::VBYTES / 16; i += kTcThreads) tc::cp16(sV + 16 * i, vsrc + 16 * i, true);
-    for (int i = threadIdx.x; i < kTcRows * MM; i += kTcThreads) {
-      const int r = i / MM, c = i % MM;
-      const bool live = (uint32_t)r < cnt;
-      const uint32_t e = live ? __ldg(A.entries + first + r) >> 6 : 0u;
-      tc::cp16(sA + (r >> 3) * SBO_A + (MM - 1 - c) * 128 + (r & 7) * 16, A.poly + (size_t)e * EW + c * 4, live);
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  };
-
-  int t = blockIdx.x;
-  if (t < A.ntiles) prefetch(t, 0);
-  for (int k = 0; t < A.ntiles; ++k, t += gridDim.x) {
-    const int st = k & 1;
-    const int tn = t + gridDim.x;
-    if (tn < A.ntiles) {
-      prefetch(tn, st ^ 1);  // the other stage's MMAs all completed in the previous tile
-      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    }
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic-proxy writes -> tensor core
-    __syncthreads();
-    tc::fence_after();
-    uint8_t* sA = smem + st * S::STAGE;
-    uint8_t* sV = sA + S::ABYTES;
-    const uint32_t* sE = reinterpret_cast<const uint32_t*>(sV + S::VPAD);
-    const uint32_t cnt = A.tiles[3 * t + 2];
-    const uint32_t a_base = tc::smem_u32(sA), v_base = tc::smem_u32(sV);
-    auto issue = [&](int ch) {
-      const uint32_t tbuf = tmem + (uint32_t)((ch & 1) * kTcNChunk);
-#pragma unroll
-      for (int ks = 0; ks < KSTEPS; ++ks) {
-        const uint64_t da = tc::make_desc(a_base + ks * 256, 128, SBO_A);
-        const uint64_t db = tc::make_desc(v_base + (ch * kTcNChunk / 8) * 128 + ks * 1024, 512, 128);
-        tc::mma_i8(tbuf, da, db, idesc, ks > 0 ? 1u : 0u);
+  if (warp >= kTcEpiWarps && warp < kTcEpiWarps + kTcProdWarps) {
+    // ===== producers =====
+    const int pw = warp - kTcEpiWarps;
+    const int rr = lane & 7, cc = lane >> 3;  // 8 rows x 4 16-byte chunks per instruction
+    int k = 0;
+    for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
+      const int st = k & 1;
+      if (k >= 2) tc::mbar_wait_parity(&empty[st], ((k >> 1) - 1) & 1);
+      uint8_t* sA = smem + st * S::STAGE;
+      uint8_t* sV = sA + S::ABYTES;
+      const uint32_t s = __ldg(A.tiles + 3 * t), first = __ldg(A.tiles + 3 * t + 1), cnt = __ldg(A.tiles + 3 * t + 2);
+      if (pw == 0 && lane == 0) {
+        tc::mbar_arrive_tx(&full[st], S::VBYTES);
+        tc::bulk_g2s(sV, A.vtab + (size_t)s * S::VBYTES, S::VBYTES, &full[st]);
       }
-      tc::mma_commit(&mbar[ch & 1]);
-    };
-    if (threadIdx.x == 0) {
-      issue(0);
-      if (NCH > 1) issue(1);
-    }
-    const int row = 32 * (warp & 3) + lane;
-    const bool live = (uint32_t)row < cnt;
-    const uint32_t ent = live ? sE[row] : 0u;
-    uint32_t* dst = A.poly + (size_t)(ent >> 6) * EW;
-    const int rot = (int)(ent & 63u);
-    for (int ch = 0; ch < NCH; ++ch) {
-      tc::mbar_wait_parity(&mbar[ch & 1], ph[ch & 1]);
-      ph[ch & 1] ^= 1u;
-      tc::fence_after();
-      const uint32_t lane_addr = tmem + (uint32_t)((ch & 1) * kTcNChunk) + ((uint32_t)(32 * (warp & 3)) << 16);
-      for (int cj = warp >> 2; cj < CPC; cj += 2) {
-        int32_t Zv[32];
-        tc::tmem_ld32(lane_addr + cj * 32, Zv);
-        if (live) {
-          uint32_t o[4];
-          tc::reduce_coeff(Zv, A.p3, o);
-          int pos = (ch * CPC + cj + rot) & (2 * MM - 1);
-          if (pos >= MM) {
-            pos -= MM;
-            tc::neg_p(o, A.p3);
-          }
-          *reinterpret_cast<uint4*>(dst + pos * 4) = make_uint4(o[0], o[1], o[2], o[3]);
+      for (int g8 = pw; g8 < kTcRows / 8; g8 += kTcProdWarps) {
+        const int r = g8 * 8 + rr;
+        const bool live = (uint32_t)r < cnt;
+        const uint32_t e = live ? __ldg(A.entries + first + r) >> 6 : 0u;
+        const uint32_t* src = A.poly + (size_t)e * EW;
+        uint8_t* dst = sA + g8 * SBO_A + rr * 16;
+#pragma unroll
+        for (int c0 = 0; c0 < MM; c0 += 4) {
+          const int c = c0 + cc;
+          tc::cp16(dst + (MM - 1 - c) * 128, src + c * 4, live);
         }
       }
-      tc::fence_before();
-      __syncthreads();  // TMEM buffer (ch & 1) drained
-      if (threadIdx.x == 0 && ch + 2 < NCH) {
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      if (k >= 1) {  // the previous tile's copies have landed: publish them to the tensor core
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        tc::mbar_arrive(&full[st ^ 1]);
+      }
+    }
+    if (k >= 1) {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      tc::mbar_arrive(&full[(k - 1) & 1]);
+    }
+  } else if (warp == kTcEpiWarps + kTcProdWarps) {
+    // ===== MMA issuer =====
+    if (lane == 0) {
+      const uint32_t idesc = tc::make_idesc(kTcRows, kTcNChunk);
+      int k = 0, g = 0;
+      for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
+        const int st = k & 1;
+        tc::mbar_wait_parity(&full[st], (k >> 1) & 1);
         tc::fence_after();
-        issue(ch + 2);
+        const uint32_t a_base = tc::smem_u32(smem + st * S::STAGE);
+        const uint32_t v_base = a_base + S::ABYTES;
+        for (int ch = 0; ch < NCH; ++ch, ++g) {
+          const int b = g & 1;
+          if (g >= 2) {
+            tc::mbar_wait_parity(&tempty[b], ((g >> 1) - 1) & 1);
+            tc::fence_after();
+          }
+          const uint32_t tbuf = tmem + (uint32_t)(b * kTcNChunk);
+#pragma unroll
+          for (int ks = 0; ks < KSTEPS; ++ks) {
+            const uint64_t da = tc::make_desc(a_base + ks * 256, 128, SBO_A);
+            const uint64_t db = tc::make_desc(v_base + (ch * kTcNChunk / 8) * 128 + ks * 1024, 512, 128);
+            tc::mma_i8(tbuf, da, db, idesc, ks > 0 ? 1u : 0u);
+          }
+          tc::mma_commit(&tfull[b]);
+        }
+        tc::mma_commit(&empty[st]);
+      }
+    }
+  } else if (warp < kTcEpiWarps) {
+    // ===== epilogue =====
+    const int quad = warp & 3;
+    const int row = 32 * quad + lane;
+    int g = 0;
+    for (int t = blockIdx.x; t < A.ntiles; t += G) {
+      const uint32_t first = __ldg(A.tiles + 3 * t + 1), cnt = __ldg(A.tiles + 3 * t + 2);
+      const bool live = (uint32_t)row < cnt;
+      const bool warp_live = (uint32_t)(32 * quad) < cnt;  // warp-uniform
+      const uint32_t ent = live ? __ldg(A.entries + first + row) : 0u;
+      uint32_t* dst = A.poly + (size_t)(ent >> 6) * EW;
+      const int rot = (int)(ent & 63u);
+      for (int ch = 0; ch < NCH; ++ch, ++g) {
+        const int b = g & 1;
+        tc::mbar_wait_parity(&tfull[b], (g >> 1) & 1);
+        tc::fence_after();
+        int32_t Z0[32], Z1[32];
+        const uint32_t lane_addr = tmem + (uint32_t)(b * kTcNChunk) + ((uint32_t)(32 * quad) << 16);
+        const int cj0 = warp >> 2, cj1 = cj0 + 4;
+        if (warp_live) {
+          tc::tmem_ld32_nowait(lane_addr + cj0 * 32, Z0);
+          tc::tmem_ld32_nowait(lane_addr + cj1 * 32, Z1);
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        }
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[b]);  // this warp's columns of buffer b are read
+        if (live) {
+#pragma unroll
+          for (int h = 0; h < CPE; ++h) {
+            const int pos = (ch * CPC + (h ? cj1 : cj0) + rot) & (2 * MM - 1);
+            uint32_t o[4];
+            tc::reduce_coeff(h ? Z1 : Z0, A.p3, pos >= MM, o);
+            *reinterpret_cast<uint4*>(dst + (pos & (MM - 1)) * 4) = make_uint4(o[0], o[1], o[2], o[3]);
+          }
+        }
       }
     }
   }
+  tc::fence_before();
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * kTcNChunk));
 }

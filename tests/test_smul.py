@@ -113,6 +113,27 @@ def test_smul_equals_product(cuda_ok):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("e", [23, 25, 26])
+def test_smul_large_products_by_residues(cuda_ok, e):
+    # product sizes 2^24, 2^26, 2^27 bits: the Q = 8 / 16 / 32 lane widths of the FFT and
+    # pointwise kernels, the CTA-wide (FULL) variants, and a non-full Q = 32 plan (the odd
+    # operand length below); checked by residues modulo 62-bit primes, as the DKSS 2^26 test
+    from paper_1503_04955_b200.smul import device_plan_for
+
+    rng = random.Random(100 + e)
+    for bits in (1 << e, (1 << e) - 12345):
+        a = rng.getrandbits(bits) | 1 << (bits - 1)
+        b = rng.getrandbits(bits) | 1 << (bits - 1)
+        plan, _ = device_plan_for(2 * bits, 64)
+        c = smul(a, b).to_int()
+        assert c.bit_length() in (2 * bits - 1, 2 * bits), (bits, plan.K)
+        pr = random.Random(54321)
+        for _ in range(16):
+            q = pr.getrandbits(62) | 1 << 61 | 1
+            assert c % q == (a % q) * (b % q) % q, (bits, plan.K, q)
+
+
+@pytest.mark.gpu
 def test_smul_edge_values(cuda_ok):
     for bits in (64, 3000, 1 << 16, 1 << 21):
         ones = (1 << bits) - 1                       # longest carry chains
