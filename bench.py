@@ -145,6 +145,52 @@ def imad_peak():
     return 9.3e12, "fallback: SURVEY.md planning assumption"
 
 
+def tc_i8_peak():
+    """Measured dense int8 tensor-core rate (ops/s) from profiles/tc_i8_peak.json
+    (tools/microbench_tc_i8.cu: tcgen05.mma kind::i8 M128 N256 K32 back to back on every SM)."""
+    path = os.path.join(HERE, "profiles", "tc_i8_peak.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["ops_per_s"]), "tools/microbench_tc_i8.cu (profiles/tc_i8_peak.json)"
+    return 4.5e15, "fallback: nominal dense int8 (2x the 2.25 PFLOP/s bf16 figure)"
+
+
+def hbm_peak():
+    """HBM bytes/s: MEASURED_PEAKS.json (driver-written), else the profiling recipe's fallback."""
+    path = os.path.join(HERE, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]) * 1e9, "MEASURED_PEAKS.json hbm_gbs"
+    return 6.65e12, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+# which roofline bounds each profiled kernel kind (bench's per-launch profile, dkss_profile_device)
+TENSOR_KINDS = {"twiddle_tc"}                            # work = int8 ops of the byte GEMM
+IMAD_KINDS = {"fwd_pass", "inv_pass", "bottom", "rows"}  # work = 32x32->64 limb products
+
+
+def kernel_roofline(kind: str, work: int, nbytes: int, ms: float, peaks) -> dict:
+    """Roofline of one kernel kind over a step: the slower of its compute at the matching peak and
+    its stage bytes at HBM bandwidth; achieved / peak in the binding unit."""
+    (imad, _), (tc, _), (hbm, _) = peaks
+    s = ms * 1e-3
+    if kind in TENSOR_KINDS:
+        t_c, cu, cpk = work / tc, "T int8 ops/s", tc
+    elif kind in IMAD_KINDS and work:
+        t_c, cu, cpk = work / imad, "T limb-products/s (32x32->64)", imad
+    else:
+        t_c, cu, cpk = 0.0, None, None
+    t_m = nbytes / hbm
+    if t_c >= t_m and cu:
+        bound, achieved, peak, unit = ("tensor" if kind in TENSOR_KINDS else "imad"), work / s, cpk, cu
+    else:
+        bound, achieved, peak, unit = "hbm", nbytes / s, hbm, "GB/s"
+    scale = 1e9 if unit == "GB/s" else 1e12
+    return {"bound": bound, "achieved": round(achieved / scale, 4), "peak": round(peak / scale, 4), "unit": unit,
+            "frac": round(achieved / peak, 4), "t_roof_ms": round(max(t_c, t_m) * 1e3, 5)}
+
+
 class ClockSampler:
     """NVML sampling of SM clock + throttle reasons during the timed region."""
 
@@ -539,8 +585,9 @@ def run_local(args, R: Ranks, mode: str):
     nprof = len(prof_runs) - 1
     dom = max(per_kind, key=lambda k: per_kind[k]["ms"])
     dk = per_kind[dom]
-    peak, peak_src = imad_peak()
-    achieved = dk["work"] / (dk["ms"] * 1e-3) if dk["ms"] > 0 else 0.0
+    peaks = (imad_peak(), tc_i8_peak(), hbm_peak())
+    roofs = {k: kernel_roofline(k, v["work"] // nprof, v["bytes"] // nprof, v["ms"] / nprof, peaks)
+             for k, v in per_kind.items()}
     rp = ring_products_per_multiply(plan)
     w_mul = rp * plan.m * plan.m * info["L"] * info["L"]
     traffic, pipe_pct = None, None
@@ -587,18 +634,22 @@ def run_local(args, R: Ranks, mode: str):
 
     if R.rank == 0:
         line = base_line(args, R, mode, ms_per_step, value, clocks, launches)
-        whole = w_mul * products / R.world / (max_ms * 1e-3) / peak
+        # the step's roofline time: every kernel at its own bound (tensor / IMAD / HBM), summed
+        t_roof = sum(r["t_roof_ms"] for r in roofs.values())
+        prof_ms = sum(v["ms"] for v in per_kind.values()) / nprof
+        dr = roofs[dom]
         line.update({
             "plan": plan_desc(plan), "gate": gate,
-            "roofline": {"bound": "imad", "achieved": round(achieved / 1e12, 4), "peak": round(peak / 1e12, 4),
-                         "unit": "T limb-products/s (32x32->64)", "frac": round(achieved / peak, 4),
-                         "traffic": traffic, "kernel": dom, "peak_source": peak_src,
+            "roofline": {"bound": dr["bound"], "achieved": dr["achieved"], "peak": dr["peak"], "unit": dr["unit"],
+                         "frac": dr["frac"], "traffic": traffic, "kernel": dom,
+                         "peak_source": {"imad": peaks[0][1], "tensor": peaks[1][1], "hbm": peaks[2][1]},
                          "ncu_fmaheavy_pct": pipe_pct,  # IMAD.WIDE pipe busy, from the committed ncu capture
                          "work_per_launch": dk["work"] // max(1, dk["launches"]),
-                         "whole_multiply_frac": round(whole, 4)},
+                         "bytes_per_launch": dk["bytes"] // max(1, dk["launches"]),
+                         "step_roofline_ms": round(t_roof, 5),
+                         "step_frac": round(t_roof / prof_ms, 4) if prof_ms > 0 else None},
             "kernels": {k: {"ms_per_step": round(v["ms"] / nprof, 5), "launches_per_step": v["launches"] // nprof,
-                            "work": v["work"] // nprof,
-                            "tput_T_per_s": round(v["work"] / (v["ms"] * 1e-3) / 1e12, 3) if v["work"] else 0}
+                            "work": v["work"] // nprof, "bytes": v["bytes"] // nprof, **roofs[k]}
                         for k, v in per_kind.items()},
             "ring_products_per_mul": rp, "w_mul_limb_products": w_mul,
             "e2e": {"value": round(2 * N * len(pairs) * R.world / e2e_s / 1e9, 4), "unit": "Gbit/s",

@@ -290,24 +290,38 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
 
   if (warp >= kTcEpiWarps && warp < kTcEpiWarps + kTcProdWarps) {
     // ===== producers =====
+    // Each lane gathers rows g8 * 8 + (lane & 7) of the tile (g8 = pw, pw + kTcProdWarps, ...),
+    // 16-byte chunks c = 4 i + (lane >> 3).  The tile header and row entries of tile k + 1 are
+    // loaded while tile k's copies are in flight; a tile's "full" barrier is signalled as soon as
+    // its own copies have landed (wait_group 0, proxy fence, arrive).
+    constexpr int GPW = kTcRows / 8 / kTcProdWarps;  // row groups per producer warp
     const int pw = warp - kTcEpiWarps;
-    const int rr = lane & 7, cc = lane >> 3;  // 8 rows x 4 16-byte chunks per instruction
+    const int rr = lane & 7, cc = lane >> 3;
+    uint32_t hs = 0, hcnt = 0, ent[GPW];
+    auto load_tile = [&](int t) {
+      const uint32_t first = __ldg(A.tiles + 3 * t + 1);
+      hs = __ldg(A.tiles + 3 * t);
+      hcnt = __ldg(A.tiles + 3 * t + 2);
+#pragma unroll
+      for (int i = 0; i < GPW; ++i) ent[i] = __ldg(A.entries + first + (pw + i * kTcProdWarps) * 8 + rr) >> 6;
+    };
     int k = 0;
+    if ((int)blockIdx.x < A.ntiles) load_tile(blockIdx.x);
     for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
       const int st = k & 1;
       if (k >= 2) tc::mbar_wait_parity(&empty[st], ((k >> 1) - 1) & 1);
       uint8_t* sA = smem + st * S::STAGE;
       uint8_t* sV = sA + S::ABYTES;
-      const uint32_t s = __ldg(A.tiles + 3 * t), first = __ldg(A.tiles + 3 * t + 1), cnt = __ldg(A.tiles + 3 * t + 2);
       if (pw == 0 && lane == 0) {
         tc::mbar_arrive_tx(&full[st], S::VBYTES);
-        tc::bulk_g2s(sV, A.vtab + (size_t)s * S::VBYTES, S::VBYTES, &full[st]);
+        tc::bulk_g2s(sV, A.vtab + (size_t)hs * S::VBYTES, S::VBYTES, &full[st]);
       }
-      for (int g8 = pw; g8 < kTcRows / 8; g8 += kTcProdWarps) {
-        const int r = g8 * 8 + rr;
-        const bool live = (uint32_t)r < cnt;
-        const uint32_t e = live ? __ldg(A.entries + first + r) >> 6 : 0u;
-        const uint32_t* src = A.poly + (size_t)e * EW;
+#ifndef DKSS_TC_EXP_NOLOAD  // experiment builds only: time the pipeline without the element gather
+#pragma unroll
+      for (int i = 0; i < GPW; ++i) {
+        const int g8 = pw + i * kTcProdWarps;
+        const bool live = (uint32_t)(g8 * 8 + rr) < hcnt;  // rows past the count: zero-filled
+        const uint32_t* src = A.poly + (size_t)(live ? ent[i] : 0u) * EW;
         uint8_t* dst = sA + g8 * SBO_A + rr * 16;
 #pragma unroll
         for (int c0 = 0; c0 < MM; c0 += 4) {
@@ -315,17 +329,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
           tc::cp16(dst + (MM - 1 - c) * 128, src + c * 4, live);
         }
       }
+#endif
       asm volatile("cp.async.commit_group;\n" ::: "memory");
-      if (k >= 1) {  // the previous tile's copies have landed: publish them to the tensor core
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        tc::mbar_arrive(&full[st ^ 1]);
-      }
-    }
-    if (k >= 1) {
+      if (t + G < A.ntiles) load_tile(t + G);  // next tile's header and rows, under this tile's copies
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      tc::mbar_arrive(&full[(k - 1) & 1]);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic-proxy writes -> tensor core
+      tc::mbar_arrive(&full[st]);
     }
   } else if (warp == kTcEpiWarps + kTcProdWarps) {
     // ===== MMA issuer =====
@@ -383,6 +392,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
         tc::fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&tempty[b]);  // this warp's columns of buffer b are read
+#ifdef DKSS_TC_EXP_NOEPI  // experiment builds only: time the pipeline without the reduction
+        if (live && Z0[0] == 0x7fffffff && Z1[0] == 0x7fffffff) dst[0] = 0u;
+#else
         if (live) {
 #pragma unroll
           for (int h = 0; h < CPE; ++h) {
@@ -392,6 +404,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
             *reinterpret_cast<uint4*>(dst + (pos & (MM - 1)) * 4) = make_uint4(o[0], o[1], o[2], o[3]);
           }
         }
+#endif
       }
     }
   }

@@ -11,7 +11,8 @@ try:
 except Exception as e:
     print(c,'no result',e); sys.exit()
 k=d['kernels']
-print(f"{c:16s} ms/step {d['ms_per_step']:.4f} value {d['value']:.2f} Gbit/s  roofline {d['roofline']['kernel']} frac {d['roofline']['frac']:.3f} whole {d['roofline']['whole_multiply_frac']:.3f} clocks {d['clocks']['sm_mhz']}")
-print('   ', ' '.join(f"{n}:{v['ms_per_mul']*1e3:.1f}us/{v['tput_T_per_s']}T" for n,v in k.items()))
+r=d['roofline']
+print(f"{c:16s} ms/step {d['ms_per_step']:.4f} value {d['value']:.2f} Gbit/s  dominant {r['kernel']} ({r['bound']}) frac {r['frac']:.3f} step_frac {r['step_frac']} e2e {d['e2e']['ms']} ms clocks {d['clocks']['sm_mhz']}")
+print('   ', ' '.join(f"{n}:{v['ms_per_step']*1e3:.1f}us/{v['bound']}:{v['frac']}" for n,v in k.items()))
 PY
 done
