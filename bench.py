@@ -90,7 +90,7 @@ def config_dict(cfg: str, world: int, mode: str) -> dict:
     N, pairs, seed, ones = CONFIGS[cfg]
     par = {
         "single": "1 GPU",
-        "split": f"four-step split of each multiply over {world} GPUs (NCCL all-to-all)",
+        "split": f"four-step split of each multiply over {world} GPUs",
         "shard": f"{pairs} pairs sharded by pair over {world} GPU(s), no data-path collective",
         "replicas": f"{world} independent replicas (one multiply per GPU per step)",
     }[mode]
@@ -449,7 +449,8 @@ def base_line(args, R: Ranks, mode: str, ms_per_step: float, value: float, clock
 
 def run_split(args, R: Ranks):
     from paper_1503_04955_b200.dkss import set_device
-    from paper_1503_04955_b200.fourstep import DistExchange, _operands, dmul_fourstep, make_rank, run_rank
+    from paper_1503_04955_b200.fourstep import (DistExchange, PeerExchange, _operands, dmul_fourstep, make_rank,
+                                                peer_capable, run_rank, run_rank_peer)
     from paper_1503_04955_b200.plan import dkss_select_params, ring_products_per_multiply
 
     torch = R.torch
@@ -457,25 +458,34 @@ def run_split(args, R: Ranks):
     N, _, seed, ones = CONFIGS[args.config]
     a, b = operand_pair(N, seed, 0, ones)  # every rank holds the same operands
     plan = dkss_select_params(N)
-    fs = make_rank(plan, R.rank, R.world, R.dev)
+    fs = make_rank(plan, R.rank, R.world, R.dev, ipc=args.exchange == "peer")
     A, B = _operands(plan, a, b, R.dev)
-    ex = DistExchange()
+    exchange = args.exchange if (args.exchange == "alltoall" or peer_capable(fs)) else "alltoall"
+    if exchange == "peer":
+        px = PeerExchange(fs)
+
+        def split_step():
+            return run_rank_peer(fs, px, A, B)
+    else:
+        ex = DistExchange()
+
+        def split_step():
+            return run_rank(fs, ex, A, B)
     stream = torch.cuda.current_stream(R.dev)
-    prod = run_rank(fs, ex, A, B)
+    prod = split_step()
     torch.cuda.synchronize(R.dev)
     if R.rank == 0:
         c = int.from_bytes(prod.cpu().numpy().view("uint32").tobytes(), "little")
         if not gate_one(c, a, b, N):
             raise SystemExit("split product mismatch")
     R.barrier()
-    max_ms, clocks, launches = timed_steps(R, lambda: run_rank(fs, ex, A, B), args.steps, args.warmup, stream,
-                                           per_step_barrier=True)
+    max_ms, clocks, launches = timed_steps(R, split_step, args.steps, args.warmup, stream, per_step_barrier=True)
     ms_per_step = max_ms / args.steps
     e2e = []
     for _ in range(max(3, args.e2e_steps // 4)):
         R.barrier()
         t0 = time.perf_counter()
-        dmul_fourstep(a, b)
+        dmul_fourstep(a, b, exchange=exchange)
         e2e.append(time.perf_counter() - t0)
     e2e_s = R.max(sorted(e2e)[len(e2e) // 2])
     if R.rank == 0:
@@ -487,6 +497,7 @@ def run_split(args, R: Ranks):
         line = base_line(args, R, "split", ms_per_step, 2 * N / (ms_per_step * 1e-3) / 1e9, clocks, launches)
         line.update({
             "plan": plan_desc(plan),
+            "exchange": exchange,
             "exchange_bytes_per_rank": 3 * 4 * lay["block_words"] * (R.world - 1) // R.world,
             "roofline": {"bound": "imad", "achieved": round(per_gpu / 1e12, 4), "peak": round(peak / 1e12, 4),
                          "unit": "T limb-products/s per GPU", "frac": round(per_gpu / peak, 4), "traffic": None,
@@ -706,6 +717,9 @@ def main():
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--replicas", action="store_true",
                     help="single-multiply configs at N > 1: independent replicas instead of the four-step split")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "alltoall"],
+                    help="four-step split: exchange fused into the phase kernels' stores over CUDA IPC peer "
+                         "memory (default), or NCCL all-to-all + re-layout kernels")
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--ref-budget", type=float, default=150.0, help="seconds of timed oracle work, reference arm")
     ap.add_argument("--no-cpu", action="store_true")

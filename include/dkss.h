@@ -191,6 +191,26 @@ int dkss_fs_decode_partial(dkss_plan* plan, int rank, int world, const uint32_t*
                            void* stream);
 int dkss_fs_decode_finish(dkss_plan* plan, int world, const uint64_t* parts_dev, uint32_t* out_dev, size_t nc,
                           void* stream);
+/* the same two phases with the exchange fused into their stores: instead
+ * of this rank's x (resp. its product rows in z) each output element is written straight into
+ * the buffer of the rank that owns it next -- z_peers[h] = rank h's z = [2][R][mu0] rows,
+ * x_peers[r] = rank r's x = [E][C] columns of the product -- through device-visible peer base
+ * pointers (a device array of `world` uint64 addresses: CUDA IPC mappings of the other GPUs'
+ * buffers over NVLink, or plain pointers for ranks emulated on one GPU).  No all-to-all and no
+ * re-layout; the caller orders the phases across ranks (a stream-ordered barrier such as a
+ * one-element NCCL all-reduce).  The rows phase needs >= 2 transform levels.  x_dev of the
+ * first call is this rank's [2][E][C] scratch: elements whose table twiddles the tensor cores
+ * apply pass through it (the tensor-core kernel stores them to their owners). */
+int dkss_fs_columns_fwd_peer(dkss_plan* plan, int rank, int world, const uint32_t* a_dev, const uint32_t* b_dev,
+                             size_t n_limbs, uint32_t* x_dev, const uint64_t* z_peers_dev, void* stream);
+int dkss_fs_rows_peer(dkss_plan* plan, int rank, int world, uint32_t* z_dev, const uint64_t* x_peers_dev,
+                      void* stream);
+/* device buffers shareable with the other ranks' processes (cudaMalloc + CUDA IPC): handle is a
+ * 64-byte cudaIpcMemHandle_t; dkss_ipc_open maps another process's buffer on `device` */
+int dkss_ipc_alloc(int device, size_t bytes, void** dptr, void* handle);
+int dkss_ipc_open(int device, const void* handle, void** dptr);
+int dkss_ipc_close(void* dptr);
+int dkss_ipc_free(void* dptr);
 /* exchange re-layout: src [n][A][B][run_words] -> dst [n][B][A][run_words] (16-byte aligned,
  * run_words a multiple of 4, n*A*B <= 65535) */
 int dkss_block_transpose(dkss_plan* plan, const uint32_t* src_dev, uint32_t* dst_dev, int n, int A, int B,

@@ -25,7 +25,8 @@ EXPORTS = (
     "dkss_encode_host", "dkss_fft_host", "dkss_rmul_host", "dkss_decode_host",
     "dkss_fs_layout_get", "dkss_fs_columns_fwd", "dkss_fs_rows", "dkss_fs_columns_inv",
     "dkss_block_transpose", "dkss_decode_device", "dkss_lucas_lehmer", "dkss_fs_decode_partial",
-    "dkss_fs_decode_finish",
+    "dkss_fs_decode_finish", "dkss_fs_columns_fwd_peer", "dkss_fs_rows_peer", "dkss_ipc_alloc", "dkss_ipc_open",
+    "dkss_ipc_close", "dkss_ipc_free",
     # include/smul.h
     "smul_plan_create", "smul_plan_destroy", "smul_product_limbs", "smul_mul", "smul_mul_digits", "smul_mul_device",
     "smul_fft_host",
@@ -130,6 +131,12 @@ def load(path: str = LIB_PATH):
         L.dkss_fs_columns_fwd.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t, vp, vp]
         L.dkss_fs_rows.argtypes = [vp, ctypes.c_int, vp, vp]
         L.dkss_fs_columns_inv.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp]
+        L.dkss_fs_columns_fwd_peer.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_size_t, vp, vp, vp]
+        L.dkss_fs_rows_peer.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp, vp]
+        L.dkss_ipc_alloc.argtypes = [ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(vp), vp]
+        L.dkss_ipc_open.argtypes = [ctypes.c_int, vp, ctypes.POINTER(vp)]
+        L.dkss_ipc_close.argtypes = [vp]
+        L.dkss_ipc_free.argtypes = [vp]
         L.dkss_block_transpose.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, vp]
         L.dkss_decode_device.argtypes = [vp, vp, vp, ctypes.c_size_t, vp]
         L.dkss_fs_decode_partial.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp, vp]
@@ -303,6 +310,16 @@ class DevicePlan:
     def fs_rows(self, world: int, z_ptr: int, stream: int = 0):
         _check(self._lib.dkss_fs_rows(self._h, world, ctypes.c_void_p(z_ptr), ctypes.c_void_p(stream)))
 
+    def fs_columns_fwd_peer(self, rank: int, world: int, a_ptr: int, b_ptr: int, n_limbs: int, x_ptr: int,
+                            z_peers_ptr: int, stream: int = 0):
+        _check(self._lib.dkss_fs_columns_fwd_peer(self._h, rank, world, ctypes.c_void_p(a_ptr), ctypes.c_void_p(b_ptr),
+                                                  n_limbs, ctypes.c_void_p(x_ptr), ctypes.c_void_p(z_peers_ptr),
+                                                  ctypes.c_void_p(stream)))
+
+    def fs_rows_peer(self, rank: int, world: int, z_ptr: int, x_peers_ptr: int, stream: int = 0):
+        _check(self._lib.dkss_fs_rows_peer(self._h, rank, world, ctypes.c_void_p(z_ptr), ctypes.c_void_p(x_peers_ptr),
+                                           ctypes.c_void_p(stream)))
+
     def fs_columns_inv(self, rank: int, world: int, x_ptr: int, stream: int = 0):
         _check(self._lib.dkss_fs_columns_inv(self._h, rank, world, ctypes.c_void_p(x_ptr), ctypes.c_void_p(stream)))
 
@@ -418,3 +435,37 @@ def pinned_empty(shape) -> np.ndarray:
     if 4 * int(np.prod(shape)) < _PINNED_MIN_BYTES:
         return np.empty(shape, dtype=np.uint32)
     return np.asarray(_PinnedBlock(shape))
+
+
+IPC_HANDLE_BYTES = 64  # sizeof(cudaIpcMemHandle_t)
+
+
+class IpcBuffer:
+    """A device buffer other processes can map (dkss_ipc_alloc): `ptr`, `nbytes`, `handle` (bytes)."""
+
+    def __init__(self, device: int, nbytes: int):
+        L = load()
+        p = ctypes.c_void_p()
+        h = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+        _check(L.dkss_ipc_alloc(device, nbytes, ctypes.byref(p), h))
+        self.ptr, self.nbytes, self.handle = p.value, nbytes, h.raw
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.dkss_ipc_free(ctypes.c_void_p(self.ptr))
+            self.ptr = None
+
+
+class IpcMapping:
+    """Another process's IpcBuffer mapped into this one (dkss_ipc_open): `ptr`."""
+
+    def __init__(self, device: int, handle: bytes):
+        L = load()
+        p = ctypes.c_void_p()
+        _check(L.dkss_ipc_open(device, ctypes.create_string_buffer(handle, IPC_HANDLE_BYTES), ctypes.byref(p)))
+        self.ptr = p.value
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.dkss_ipc_close(ctypes.c_void_p(self.ptr))
+            self.ptr = None

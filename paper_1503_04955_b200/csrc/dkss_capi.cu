@@ -258,7 +258,7 @@ struct dkss_plan {
   uint32_t tc_p3 = 0;               // p = 1 + tc_p3 * 2^96
   uint8_t* d_vtab = nullptr;        // V tables of d_twr rows, [M/m][2m-1][32][16]
   uint8_t* d_vtab_s = nullptr;      // of the pre-scaled rows d_twr_s (last inverse level)
-  std::map<std::pair<int, int>, TcSched> tc_sched;  // (level, polynomials per launch)
+  std::map<std::tuple<int, long long, bool, int, int>, TcSched> tc_sched;  // by TcLayout
   int tick_next = 0;
   bool dyn_tiles = true;            // DKSS_NO_DYNTILES=1: static round-robin tiles
   void (*rows_fn)(RowsArgs, ModCtx) = nullptr;
@@ -443,9 +443,22 @@ struct Geom {
   int log_cpp;           // log2 columns per polynomial
   long long l_off;       // global column offset (first level of a column shard)
   int log_mu0;           // column stride at level 0 in this layout (-1: 2M/2m)
+  // fused four-step exchange (PassArgs::peer_mode): applied to the last level the call runs
+  const unsigned long long* peer = nullptr;
+  int peer_mode = 0, peer_log_r = 0, peer_log_c = 0, peer_log_mu0 = 0;
+  long long peer_row0 = 0;
 };
 
 Geom full_geom(const dkss_plan* P) { return Geom{P->poly_words, P->log_top_mu, 0, -1}; }
+
+void set_peer(PassArgs& A, const Geom& g) {
+  A.peer = g.peer;
+  A.peer_mode = g.peer_mode;
+  A.peer_log_r = g.peer_log_r;
+  A.peer_log_c = g.peer_log_c;
+  A.peer_log_mu0 = g.peer_log_mu0;
+  A.peer_row0 = g.peer_row0;
+}
 
 PassArgs pass_args(const dkss_plan* P, const Geom& g, uint32_t* poly, int npoly, int lv) {
   PassArgs A{};
@@ -465,32 +478,75 @@ PassArgs pass_args(const dkss_plan* P, const Geom& g, uint32_t* poly, int npoly,
   return A;
 }
 
-// tensor-core twiddle schedule of level lv over `npoly` polynomials of the full layout (built on
-// the host once per (lv, npoly): every element (poly q, instance, j, l) with a table twiddle,
-// e = j l (2m)^lv, s = e mod (M/m) != 0, grouped by s into tiles of <= 128)
-int tc_sched(dkss_plan* P, int lv, int npoly, const TcSched** out) {
-  auto key = std::make_pair(lv, npoly);
+// Which elements one tensor-core launch covers (the layouts of the pass kernels):
+//   full layout, level 0: `count` polynomials of 2M elements;
+//   rows layout, level >= 1: `count` rows of mu0 = M/m elements (a full-layout launch over n
+//     polynomials at level >= 1 is the rows layout over n E rows: levels >= 1 act inside a row);
+//   columns layout, level 0 (four-step split): `count` polynomials of E x C
+//     elements, this rank's columns [col_rank C, (col_rank + 1) C), C = mu0 / col_world.
+struct TcLayout {
+  int lv = 0;
+  long long count = 0;
+  bool rows = false;
+  int col_rank = 0, col_world = 0;
+};
+
+TcLayout tc_full(const dkss_plan* P, int lv, int npoly) {
+  TcLayout t;
+  t.lv = lv;
+  t.count = npoly;
+  if (lv >= 1) {
+    t.rows = true;
+    t.count = (long long)npoly * 2 * P->m;
+  }
+  return t;
+}
+
+// tensor-core twiddle schedule of one launch (built on the host once per layout): every element
+// with a table twiddle, e = j l (2m)^lv, s = e mod (M/m) != 0, grouped by s into tiles of <= 128
+int tc_sched(dkss_plan* P, const TcLayout& lay, const TcSched** out) {
+  const auto key = std::make_tuple(lay.lv, lay.count, lay.rows, lay.col_rank, lay.col_world);
   auto it = P->tc_sched.find(key);
   if (it != P->tc_sched.end()) {
     *out = &it->second;
     return 0;
   }
-  const long long E = 2LL * P->m, twoM = 2LL * P->M, mu_top = 1LL << P->log_top_mu;
+  const long long E = 2LL * P->m, twoM = 2LL * P->M, mu_top = 1LL << P->log_top_mu, mu0 = mu_top;
+  const int lv = lay.lv;
   const int log_mu = ilog2i(twoM) - P->logE * (lv + 1);
-  const long long mu = 1LL << log_mu, inst = twoM / (E * mu), base_pow = 1LL << (P->logE * lv);
-  if ((long long)npoly * twoM >= (1LL << 26)) return fail(DKSS_EINVAL, "tensor-core schedule: too many elements");
+  const long long mu = 1LL << log_mu, base_pow = 1LL << (P->logE * lv);
   std::vector<std::vector<uint32_t>> groups((size_t)mu_top);
-  for (long long q = 0; q < npoly; ++q)
-    for (long long in = 0; in < inst; ++in)
-      for (long long j = 1; j < E; ++j)
-        for (long long l = 1; l < mu; ++l) {
-          const long long e = j * l * base_pow;
-          const long long sr = e & (mu_top - 1);
-          if (!sr) continue;
-          const long long r = (e >> P->log_top_mu) & (E - 1);
-          const long long el = q * twoM + (in << (log_mu + P->logE)) + (j << log_mu) + l;
-          groups[(size_t)sr].push_back((uint32_t)(el << 6 | r));
-        }
+  long long total = 0;
+  auto add = [&](long long el, long long j, long long l) {
+    const long long e = j * l * base_pow;
+    const long long sr = e & (mu_top - 1);
+    if (!sr) return;
+    const long long r = (e >> P->log_top_mu) & (E - 1);
+    groups[(size_t)sr].push_back((uint32_t)(el << 6 | r));
+  };
+  if (lay.rows) {
+    total = lay.count * mu0;
+    const long long inst = mu0 / (E * mu);
+    if (total < (1LL << 26))
+      for (long long u = 0; u < lay.count; ++u)
+        for (long long in = 0; in < inst; ++in)
+          for (long long j = 1; j < E; ++j)
+            for (long long l = 1; l < mu; ++l) add(u * mu0 + (in << (log_mu + P->logE)) + (j << log_mu) + l, j, l);
+  } else if (lay.col_world) {
+    const long long C = mu0 / lay.col_world;
+    total = lay.count * E * C;
+    if (total < (1LL << 26))
+      for (long long q = 0; q < lay.count; ++q)
+        for (long long j = 1; j < E; ++j)
+          for (long long c = 0; c < C; ++c) add(q * E * C + j * C + c, j, (long long)lay.col_rank * C + c);
+  } else {
+    total = lay.count * twoM;
+    if (total < (1LL << 26))
+      for (long long q = 0; q < lay.count; ++q)
+        for (long long j = 1; j < E; ++j)
+          for (long long l = 1; l < mu0; ++l) add(q * twoM + (j << P->log_top_mu) + l, j, l);
+  }
+  if (total >= (1LL << 26)) return fail(DKSS_EINVAL, "tensor-core schedule: too many elements");
   std::vector<uint32_t> tiles, entries;
   long long tw = 0;
   for (long long sr = 1; sr < mu_top; ++sr) {
@@ -518,15 +574,16 @@ int tc_sched(dkss_plan* P, int lv, int npoly, const TcSched** out) {
   return 0;
 }
 
-// whether a full-layout launch over `npoly` polynomials takes the tensor-core twiddles: always for
-// m = 32; for m = 16 only from 2^17 elements per launch (2^20 x 2^20, 16384 elements: 96 vs 82 us
-// -- two extra launches per level cost more than the faster products; the 1024 x 2^18 batch:
-// 8.37 vs 11.36 ms)
+// whether a launch over `elems` elements takes the tensor-core twiddles: always for m = 32; for
+// m = 16 only from 2^17 elements per launch (2^20 x 2^20, 16384 elements: 96 vs 82 us -- two
+// extra launches per level cost more than the faster products; the 1024 x 2^18 batch: 8.37 vs
+// 11.36 ms)
 constexpr long long kTcMinElems16 = 1LL << 17;
-bool use_tc(const dkss_plan* P, int npoly) {
+bool use_tc_elems(const dkss_plan* P, long long elems) {
   if (!P->tc) return false;
-  return P->tc_forced || P->m >= 32 || (long long)npoly * 2 * P->M >= kTcMinElems16;
+  return P->tc_forced || P->m >= 32 || elems >= kTcMinElems16;
 }
+bool use_tc(const dkss_plan* P, int npoly) { return use_tc_elems(P, (long long)npoly * 2 * P->M); }
 
 // schedules a multiply of `batch` products will use, built before a stream capture starts
 // (their device buffers cannot be allocated inside one)
@@ -534,19 +591,30 @@ int tc_prepare(dkss_plan* P, int batch, bool sq) {
   const TcSched* sc;
   int rc;
   for (int lv = 0; lv < P->levels; ++lv) {
-    if (use_tc(P, (sq ? 1 : 2) * batch) && (rc = tc_sched(P, lv, (sq ? 1 : 2) * batch, &sc))) return rc;
-    if (use_tc(P, batch) && (rc = tc_sched(P, lv, batch, &sc))) return rc;
+    if (use_tc(P, (sq ? 1 : 2) * batch) && (rc = tc_sched(P, tc_full(P, lv, (sq ? 1 : 2) * batch), &sc))) return rc;
+    if (use_tc(P, batch) && (rc = tc_sched(P, tc_full(P, lv, batch), &sc))) return rc;
   }
   return 0;
 }
 
-// the table twiddles of level lv on the tensor cores, in place (scaled: the last inverse level)
-int launch_tc(dkss_plan* P, uint32_t* poly, int npoly, int lv, bool scaled, cudaStream_t s) {
+// the table twiddles of one launch on the tensor cores, in place (scaled: the last inverse
+// level); with g->peer_mode == 1 (the fused four-step exchange of the first level) the products
+// are stored into the row owners' buffers instead
+int launch_tc_layout(dkss_plan* P, uint32_t* poly, const TcLayout& lay, bool scaled, cudaStream_t s,
+                     const Geom* peer = nullptr) {
   const TcSched* sc;
   int rc;
-  if ((rc = tc_sched(P, lv, npoly, &sc))) return rc;
+  if ((rc = tc_sched(P, lay, &sc))) return rc;
   if (!sc->ntiles) return 0;
   TcArgs A{poly, sc->d_tiles, sc->d_entries, scaled ? P->d_vtab_s : P->d_vtab, sc->ntiles, P->tc_p3};
+  if (peer && peer->peer_mode == 1) {
+    A.peer = peer->peer;
+    A.peer_log_r = peer->peer_log_r;
+    A.peer_log_c = peer->peer_log_c;
+    A.peer_log_mu0 = peer->peer_log_mu0;
+    A.peer_log_poly = P->logE + peer->peer_log_c;
+    A.l_off = peer->l_off;
+  }
   const int grid = std::min(sc->ntiles, P->tc_grid);
   launch_k(P->kt.tc, dim3(grid), dim3(kTcThreads), P->kt.smem_tc, s, A);
   CUCHK(cudaGetLastError());
@@ -555,6 +623,44 @@ int launch_tc(dkss_plan* P, uint32_t* poly, int npoly, int lv, bool scaled, cuda
   mark(P, s, DKSS_K_TWIDDLE_TC, 2LL * sc->twiddled * (16LL * P->m) * (32LL * P->m),
        2LL * sc->twiddled * P->m * P->L * 4 + (long long)sc->ntiles * (long long)P->kt.tc_vbytes);
   return 0;
+}
+
+int launch_tc(dkss_plan* P, uint32_t* poly, int npoly, int lv, bool scaled, cudaStream_t s) {
+  return launch_tc_layout(P, poly, tc_full(P, lv, npoly), scaled, s);
+}
+
+// the tensor-core layout of a pass launch over `npoly` polynomials of geometry g at level lv;
+// false: CUDA-core twiddles (layout not covered, too few elements, or -- for the four-step
+// layouts -- tiles too sparse: a rank holds 1/world of every twiddle group, and at an eighth of
+// a tile per group the fixed cost per tile loses to the CUDA cores -- 2^26 on 8 ranks, first
+// level, fill 0.125 / 0.062: 0.207 vs 0.194 ms forward, 0.228 vs 0.167 ms inverse -- while at a
+// quarter it still wins: 2^24 on 2 ranks, inverse first level, fill 0.245: 0.118 vs 0.166 ms)
+constexpr double kTcMinFill = 0.2;
+bool tc_layout_of(dkss_plan* P, const Geom* g, int npoly, int lv, TcLayout* out) {
+  if (!g) {
+    *out = tc_full(P, lv, npoly);
+    return use_tc(P, npoly);
+  }
+  bool ok = false;
+  if (g->log_mu0 < 0 && lv >= 1) {  // rows layout: npoly rows of mu0 elements
+    out->lv = lv;
+    out->count = npoly;
+    out->rows = true;
+    ok = use_tc_elems(P, (long long)npoly << P->log_top_mu);
+  } else if (g->log_mu0 >= 0 && lv == 0) {  // columns layout of a four-step rank
+    out->lv = 0;
+    out->count = npoly;
+    out->col_world = 1 << (P->log_top_mu - g->log_cpp);
+    out->col_rank = (int)(g->l_off >> g->log_cpp);
+    ok = use_tc_elems(P, (long long)npoly * 2 * P->m << g->log_cpp);
+  }
+  if (!ok) return false;
+  const TcSched* sc;
+  if (tc_sched(P, *out, &sc)) {
+    g_err.clear();
+    return false;
+  }
+  return sc->ntiles == 0 || (double)sc->twiddled >= kTcMinFill * kTcRows * sc->ntiles;
 }
 
 // tc_npoly: polynomials the tensor-core decision is made for (default npoly); tc_launch = false
@@ -581,7 +687,13 @@ int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s, c
     // auto mode: the first level (fused encode) runs the CTA-wide kernel, deeper levels may use
     // warp-per-column (batch 1024 x 2^18: forward 6.35 -> 5.95 ms)
     int kind = (lv == 0 && ops_a && !P->pass_mode) ? 1 : pass_kind(P, cols);
-    const bool tc = use_tc(P, tc_npoly > 0 ? tc_npoly : npoly) && !geom;  // four-step layouts: CUDA cores
+    if (g.peer_mode && lv == lv_hi - 1) {  // fused exchange: CTA kernel, stores to the owning ranks
+      set_peer(A, g);
+      kind = 1;
+    }
+    TcLayout tl;
+    const bool tc = tc_layout_of(P, geom, tc_npoly > 0 ? tc_npoly : npoly, lv, &tl);
+    if (tc) tc_layout_of(P, geom, npoly, lv, &tl);
     if (tc) {
       kind = 1;
       A.tw_skip = 1;
@@ -617,7 +729,9 @@ int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s, c
     mark(P, s, DKSS_K_FWD_PASS, tc ? 0 : (long long)(share * rp_work(P, npoly * level_twiddles(P, lv))),
          2LL * cols * 2 * P->m * P->m * P->L * 4);
     int rc;
-    if (tc && tc_launch && (rc = launch_tc(P, poly, npoly, lv, false, s))) return rc;
+    if (tc && tc_launch &&
+        (rc = launch_tc_layout(P, poly, tl, false, s, (g.peer_mode && lv == lv_hi - 1) ? &g : nullptr)))
+      return rc;
   }
   return 0;
 }
@@ -634,13 +748,18 @@ int launch_inv_levels(dkss_plan* P, uint32_t* poly, int npoly, bool scale_last, 
     A.scale = (lv == 0 && scale_last) ? 1 : 0;
     // the inverse pass keeps the CTA-wide kernel in auto mode: the warp-per-column inverse needs
     // two column slices per warp (3 CTAs/SM) and measured slower (batch 1024 x 2^18: 4.22 vs 3.89 ms)
-    const bool tc = use_tc(P, npoly) && !geom;
-    const int kind = (P->pass_mode && !tc) ? pass_kind(P, cols) : 1;
+    TcLayout tl;
+    const bool tc = tc_layout_of(P, geom, npoly, lv, &tl);
+    int kind = (P->pass_mode && !tc) ? pass_kind(P, cols) : 1;
+    if (g.peer_mode && lv == lv_lo) {  // fused exchange: CTA kernel, stores to the owning ranks
+      set_peer(A, g);
+      kind = 1;
+    }
     if (tc) {
       // table twiddles first (the last level with the pre-scaled rows), then the pass multiplies
       // only the untwiddled elements (scale mode 2) and runs the column DFT
       int rc;
-      if ((rc = launch_tc(P, poly, npoly, lv, A.scale != 0, s))) return rc;
+      if ((rc = launch_tc_layout(P, poly, tl, A.scale != 0, s))) return rc;
       A.tw_skip = 1;
     }
     if (kind == 1 && A.scale) {
@@ -1935,8 +2054,9 @@ int dkss_fs_decode_finish(dkss_plan* P, int world, const uint64_t* parts, uint32
   return DKSS_OK;
 }
 
-int dkss_fs_columns_fwd(dkss_plan* P, int rank, int world, const uint32_t* a, const uint32_t* b, size_t nl,
-                        uint32_t* x, void* stream) {
+namespace {
+int fs_columns_fwd(dkss_plan* P, int rank, int world, const uint32_t* a, const uint32_t* b, size_t nl, uint32_t* x,
+                   const uint64_t* z_peers, void* stream) {
   int rc;
   if ((rc = fs_check(P, rank, world))) return rc;
   if (!a || !b || !x) return fail(DKSS_EINVAL, "bad argument");
@@ -1944,13 +2064,20 @@ int dkss_fs_columns_fwd(dkss_plan* P, int rank, int world, const uint32_t* a, co
   std::lock_guard<std::mutex> lk(P->mu);
   CUCHK(cudaSetDevice(P->device));
   const int logC = P->log_top_mu - ilog2i(world);
-  const Geom g{P->poly_words / world, logC, (long long)rank << logC, logC};
+  Geom g{P->poly_words / world, logC, (long long)rank << logC, logC};
+  if (z_peers) {  // outputs straight into the row owners' [2][R][mu0] buffers
+    g.peer = reinterpret_cast<const unsigned long long*>(z_peers);
+    g.peer_mode = 1;
+    g.peer_log_r = ilog2i(2LL * P->m / world);
+    g.peer_log_c = logC;
+    g.peer_log_mu0 = P->log_top_mu;
+  }
   return launch_fwd_levels(P, x, 2, (cudaStream_t)stream, a, b, (long long)nl, 1, 0, 1, &g);
 }
 
-int dkss_fs_rows(dkss_plan* P, int world, uint32_t* z, void* stream) {
+int fs_rows(dkss_plan* P, int rank, int world, uint32_t* z, const uint64_t* x_peers, void* stream) {
   int rc;
-  if ((rc = fs_check(P, 0, world))) return rc;
+  if ((rc = fs_check(P, rank, world))) return rc;
   if (!z) return fail(DKSS_EINVAL, "bad argument");
   std::lock_guard<std::mutex> lk(P->mu);
   CUCHK(cudaSetDevice(P->device));
@@ -1958,14 +2085,14 @@ int dkss_fs_rows(dkss_plan* P, int world, uint32_t* z, void* stream) {
   const int rows = 2 * P->m / world;
   const long long row_words = P->poly_words / (2LL * P->m);
   const long long f_items = 2LL * rows << (P->log_top_mu - P->logE);
-  if (P->dyn_grid && f_items >= 2LL * P->dyn_grid) {
+  if (!x_peers && P->dyn_grid && f_items >= 2LL * P->dyn_grid) {
     // the persistent row-phase kernel on this rank's R rows of a and b when there are enough
     // column items to keep its grid busy (2^26 on 8 ranks: 0.43 vs 0.50 ms; 2^24 on 8 ranks,
     // 256 items: the three launches win); its counters live in the plan workspace
     if ((rc = ensure_ws(P, 1))) return rc;
     return launch_dyn(P, z, z + (size_t)rows * row_words, 1, false, s, rows);
   }
-  const Geom g{row_words, P->log_top_mu - P->logE, 0, -1};
+  Geom g{row_words, P->log_top_mu - P->logE, 0, -1};
   if ((rc = launch_fwd_levels(P, z, 2 * rows, s, nullptr, nullptr, 0, 0, 1, P->levels, &g))) return rc;
   BottomArgs A{};
   A.a = z;
@@ -1981,7 +2108,69 @@ int dkss_fs_rows(dkss_plan* P, int world, uint32_t* z, void* stream) {
   launch_k(P->kt.bottom, dim3(grid), dim3(P->kt.nt), smem_two(P), s, A, P->mc);
   CUCHK(cudaGetLastError());
   mark(P, s, DKSS_K_BOTTOM, rp_work(P, A.total_elems), 3LL * A.total_elems * P->m * P->L * 4);
+  if (x_peers) {  // the last inverse level stores the product rows into the column owners' [E][C]
+    g.peer = reinterpret_cast<const unsigned long long*>(x_peers);
+    g.peer_mode = 2;
+    g.peer_log_c = P->log_top_mu - ilog2i(world);
+    g.peer_row0 = (long long)rank * rows;
+  }
   return launch_inv_levels(P, z, rows, false, s, 1, P->levels, &g);
+}
+}  // namespace
+
+int dkss_fs_columns_fwd(dkss_plan* P, int rank, int world, const uint32_t* a, const uint32_t* b, size_t nl,
+                        uint32_t* x, void* stream) {
+  return fs_columns_fwd(P, rank, world, a, b, nl, x, nullptr, stream);
+}
+
+int dkss_fs_columns_fwd_peer(dkss_plan* P, int rank, int world, const uint32_t* a, const uint32_t* b, size_t nl,
+                             uint32_t* x, const uint64_t* z_peers, void* stream) {
+  if (!z_peers) return fail(DKSS_EINVAL, "bad argument");
+  return fs_columns_fwd(P, rank, world, a, b, nl, x, z_peers, stream);
+}
+
+int dkss_fs_rows(dkss_plan* P, int world, uint32_t* z, void* stream) { return fs_rows(P, 0, world, z, nullptr, stream); }
+
+int dkss_fs_rows_peer(dkss_plan* P, int rank, int world, uint32_t* z, const uint64_t* x_peers, void* stream) {
+  if (!x_peers) return fail(DKSS_EINVAL, "bad argument");
+  if (P && P->levels < 2) return fail(DKSS_EINVAL, "fused exchange needs two or more transform levels");
+  return fs_rows(P, rank, world, z, x_peers, stream);
+}
+
+int dkss_ipc_alloc(int device, size_t bytes, void** dptr, void* handle) {
+  if (!dptr || !handle || !bytes) return fail(DKSS_EINVAL, "bad argument");
+  CUCHK(cudaSetDevice(device));
+  CUCHK(cudaMalloc(dptr, bytes));
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, *dptr);
+  if (e != cudaSuccess) {
+    cudaFree(*dptr);
+    *dptr = nullptr;
+    return fail(DKSS_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+  }
+  memcpy(handle, &h, sizeof h);
+  return DKSS_OK;
+}
+
+int dkss_ipc_open(int device, const void* handle, void** dptr) {
+  if (!dptr || !handle) return fail(DKSS_EINVAL, "bad argument");
+  CUCHK(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  CUCHK(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return DKSS_OK;
+}
+
+int dkss_ipc_close(void* dptr) {
+  if (!dptr) return DKSS_OK;
+  CUCHK(cudaIpcCloseMemHandle(dptr));
+  return DKSS_OK;
+}
+
+int dkss_ipc_free(void* dptr) {
+  if (!dptr) return DKSS_OK;
+  CUCHK(cudaFree(dptr));
+  return DKSS_OK;
 }
 
 int dkss_fs_columns_inv(dkss_plan* P, int rank, int world, uint32_t* x, void* stream) {

@@ -465,7 +465,42 @@ struct PassArgs {
   unsigned* ctr;         // CTA kernels: tile tickets of this launch (null: static round-robin)
   int tw_skip;           // CTA kernels: elements with a table twiddle (s != 0) pass through
                          // untouched -- the tensor-core kernel (dkss_tc.cuh) multiplies them
+  // four-step split with the exchange fused into the stores (CTA kernels):
+  // every output element goes straight to the rank that owns it next, through the peer base
+  // pointers peer[world] (CUDA IPC mappings over NVLink, or plain pointers for emulated ranks)
+  //   peer_mode 1 (first forward level, launch layout [2][E][C]): element (q, j, c) -> rank
+  //     j >> peer_log_r, at ((q R + (j & (R-1))) mu0 + l_off + c) in that rank's [2][R][mu0] rows
+  //   peer_mode 2 (last inverse level of the rows, launch layout [R][mu0], one row per launch
+  //     polynomial jr): element (jr, global column l) -> rank l >> peer_log_c, at
+  //     ((peer_row0 + jr) C + (l & (C-1))) in that rank's [E][C] columns
+  const unsigned long long* peer;
+  int peer_mode;
+  int peer_log_r, peer_log_c, peer_log_mu0;
+  long long peer_row0;
 };
+
+// destination of output element `pos` (element index inside launch polynomial `poly`) under a
+// fused-exchange store (peer_mode != 0); elem_words per element
+__device__ __forceinline__ uint32_t* peer_dst(const PassArgs& A, long long poly, long long pos, int elem_words) {
+  const long long C = 1LL << A.peer_log_c;
+  if (A.peer_mode == 1) {
+    const long long j = pos >> A.peer_log_c, c = pos & (C - 1);
+    const long long R = 1LL << A.peer_log_r;
+    uint32_t* base = reinterpret_cast<uint32_t*>(A.peer[j >> A.peer_log_r]);
+    return base + (((poly * R + (j & (R - 1))) << A.peer_log_mu0) + A.l_off + c) * elem_words;
+  }
+  uint32_t* base = reinterpret_cast<uint32_t*>(A.peer[pos >> A.peer_log_c]);
+  return base + ((A.peer_row0 + poly) * C + (pos & (C - 1))) * elem_words;
+}
+
+// the global word offset col_elem gives, or the fused-exchange destination
+__device__ __forceinline__ uint32_t* out_elem(const PassArgs& A, long long cg, int j, int loge, int elem_words) {
+  const long long poly = cg >> A.log_cpp, cc = cg & ((1LL << A.log_cpp) - 1);
+  const long long inst = cc >> A.log_mu, l = cc & ((1LL << A.log_mu) - 1);
+  const long long pos = (inst << (A.log_mu + loge)) + ((long long)j << A.log_mu) + l;
+  if (A.peer_mode) return peer_dst(A, poly, pos, elem_words);
+  return A.poly + poly * A.poly_words + pos * elem_words;
+}
 
 template <int MM>
 struct Geo {
@@ -643,9 +678,12 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArg
       const long long cg = tile * COLS + c;
       if (cg >= A.total_cols) continue;
       long long l;
-      uint32_t* dst = A.poly + col_elem(A, cg, vv, LOGE, MM * L, &l);
+      const long long off = col_elem(A, cg, vv, LOGE, MM * L, &l);
       int r;
       const long long s = tw_exp(A, vv, l, &r);
+      // fused exchange: elements the tensor-core kernel still multiplies stay local (it stores
+      // them to their owners)
+      uint32_t* dst = (A.peer_mode && !(A.tw_skip && s != 0)) ? out_elem(A, cg, vv, LOGE, MM * L) : A.poly + off;
       uint32_t w[kT][L];
       if (s == 0 || kExpNoMac || A.tw_skip) {
         if (s != 0) r = 0;  // tw_skip: the tensor-core kernel applies rho^e (rotation included)
@@ -661,6 +699,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArg
     TRACE_MARK
     tile = nxt;
   }
+  if (A.peer_mode) __threadfence_system();  // fused exchange: stores to other GPUs performed
   release_tiles(A.ctr);
   TRACE_DUMP(enc ? "fwd0" : "fwd")
 }
@@ -746,8 +785,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArg
       const int c = el / E, vv = el % E;
       const long long cg = tile * COLS + c;
       if (cg >= A.total_cols) continue;
-      long long l;
-      const long long off = col_elem(A, cg, vv, LOGE, MM * L, &l);
+      uint32_t* dst = out_elem(A, cg, vv, LOGE, MM * L);
       uint32_t v[L];
       ld_res<L>(v, ov + el * ES + kk * L);
       if (A.scale == 1) {
@@ -756,13 +794,14 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArg
         for (int q = 0; q < L; ++q) ks[q] = mc.kscale[q];
         mont_mul<L>(v, v, ks, mc);
       }
-      st_res<L>(A.poly + off + kk * L, v);
+      st_res<L>(dst + kk * L, v);
     }
     fence_proxy_async();
     __syncthreads();
     TRACE_MARK
     tile = nxt;
   }
+  if (A.peer_mode) __threadfence_system();  // fused exchange: stores to other GPUs performed
   release_tiles(A.ctr);
   TRACE_DUMP("inv")
 }
@@ -1365,6 +1404,7 @@ __global__ void k_decode_partial(PartialArgs A) {
     }
     A.s_out[idx] = S;
   }
+  __threadfence_system();  // s_out may be rank 0's gather buffer on another GPU (fused exchange)
 }
 
 struct AssembleArgs {

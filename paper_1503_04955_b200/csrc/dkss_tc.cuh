@@ -44,7 +44,21 @@ struct TcArgs {
   const uint8_t* vtab;       // [M/m][2m - 1][32][16] s8 digits, from the (scaled) twiddle rows
   int ntiles;
   uint32_t p3;               // p = 1 + p3 * 2^96
+  // fused four-step exchange of the first level (PassArgs::peer_mode 1): element el = q E C + pos
+  // (q = el >> peer_log_poly) is stored into its row owner's [2][R][mu0] buffer
+  const unsigned long long* peer = nullptr;
+  int peer_log_r = 0, peer_log_c = 0, peer_log_mu0 = 0, peer_log_poly = 0;
+  long long l_off = 0;
 };
+
+__device__ __forceinline__ uint32_t* tc_dst(const TcArgs& A, uint32_t el, int ew) {
+  if (!A.peer) return A.poly + (size_t)el * ew;
+  const long long q = (long long)el >> A.peer_log_poly, pos = (long long)el & ((1LL << A.peer_log_poly) - 1);
+  const long long j = pos >> A.peer_log_c, c = pos & ((1LL << A.peer_log_c) - 1);
+  const long long R = 1LL << A.peer_log_r;
+  uint32_t* base = reinterpret_cast<uint32_t*>(A.peer[j >> A.peer_log_r]);
+  return base + (((q * R + (j & (R - 1))) << A.peer_log_mu0) + A.l_off + c) * ew;
+}
 
 template <int MM>
 struct TcSmem {
@@ -375,7 +389,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
       const bool live = (uint32_t)row < cnt;
       const bool warp_live = (uint32_t)(32 * quad) < cnt;  // warp-uniform
       const uint32_t ent = live ? __ldg(A.entries + first + row) : 0u;
-      uint32_t* dst = A.poly + (size_t)(ent >> 6) * EW;
+      uint32_t* dst = tc_dst(A, ent >> 6, EW);
       const int rot = (int)(ent & 63u);
       for (int ch = 0; ch < NCH; ++ch, ++g) {
         const int b = g & 1;
@@ -408,6 +422,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
       }
     }
   }
+  if (A.peer) __threadfence_system();  // fused exchange: stores to other GPUs performed
   tc::fence_before();
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * kTcNChunk));

@@ -154,3 +154,77 @@ def test_two_rank_gloo_fourstep_exchange(distd):
         assert calls[:3] == ["columns_fwd", "rows", "columns_inv"]
     assert res[0][1] == [1, 1, 1, 1] and res[0][2][-1] == "decode"
     assert res[1][1] is None
+
+
+# --- the fused exchange (peer stores), CPU stand-in -----------------------------------------
+# The device kernels store each output element at the address peer_dst() computes
+# (csrc/dkss_kernels.cuh: out_elem / peer_dst).  The stand-in below restates that formula in
+# Python and scatters tagged elements with it; TagStages then checks that every rank's rows and
+# columns hold exactly the elements the all-to-all path delivers.
+
+def peer_index(mode, world, rank, q_or_row, pos):
+    """(destination rank, element index) of output element `pos` of launch polynomial
+    `q_or_row` -- the Python restatement of csrc/dkss_kernels.cuh peer_dst()."""
+    C, R = MU0 // world, E // world
+    if mode == 1:  # columns [2][E][C] -> rows [2][R][MU0]
+        j, c = pos // C, pos % C
+        return j // R, (q_or_row * R + j % R) * MU0 + rank * C + c
+    return pos // C, (rank * R + q_or_row) * C + pos % C  # rows [R][MU0] -> columns [E][C]
+
+
+class TagPeerStages(TagStages):
+    """TagStages with the fused-exchange entry points (peer tables map data_ptr -> tensor)."""
+
+    def __init__(self):
+        super().__init__(dist=True)
+        self.by_ptr = {}
+
+    def register(self, ranks):
+        for fs in ranks:
+            for t in (fs.z, fs.x, fs.gath):
+                self.by_ptr[t.data_ptr()] = t
+
+    def columns_fwd_peer(self, rank, world, a, b, x, z_peers):
+        self.columns_fwd(rank, world, a, b, x)  # the tagged outputs of this rank's columns
+        C = MU0 // world
+        xv = x.view(2, E * C, EW)
+        dst = [self.by_ptr[p].view(-1, EW) for p in z_peers.tolist()]
+        for q in range(2):
+            for pos in range(E * C):
+                h, i = peer_index(1, world, rank, q, pos)
+                dst[h][i] = xv[q, pos]
+
+    def rows_peer(self, rank, world, z, x_peers):
+        self.rows(rank, world, z)  # checks the rows arrived, tags the product rows
+        R = E // world
+        zv = z.view(2, R, MU0, EW)
+        dst = [self.by_ptr[p].view(-1, EW) for p in x_peers.tolist()]
+        for jr in range(R):
+            for pos in range(MU0):
+                h, i = peer_index(2, world, rank, jr, pos)
+                dst[h][i] = zv[0, jr, pos]
+
+    def decode_partial_ptr(self, rank, world, x, s_ptr):
+        # s_ptr: rank 0's gather buffer + this rank's slot
+        base = max(p for p in self.by_ptr if p <= s_ptr)
+        g = self.by_ptr[base]
+        n = (E + 1) * SEG
+        off = (s_ptr - base) // 8
+        self.decode_partial(rank, world, x, g[off:off + n])
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_virtual_ranks_fused_exchange_places_every_element(world):
+    from paper_1503_04955_b200.fourstep import run_virtual_peer
+
+    st = TagPeerStages()
+    ranks = [FourStepRank(st, r, world, M, MM, torch.device("cpu"), 4) for r in range(world)]
+    st.register(ranks)
+    for fs in ranks:  # nothing may be read before the peers wrote it
+        fs.z.fill_(-1)
+        fs.x.fill_(-1)
+    a = torch.zeros(4, dtype=torch.int32)
+    out = run_virtual_peer(ranks, a, a)
+    assert out.tolist() == [1, 1, 1, 1]
+    assert st.calls.count("rows") == world and st.calls.count("columns_inv") == world
+    assert st.calls[-1] == "decode"

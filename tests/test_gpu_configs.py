@@ -53,7 +53,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _split_worker(rank, world, port, N, seed, q):
+def _split_worker(rank, world, port, N, seed, q, exchange):
     import torch
     import torch.distributed as dist
 
@@ -65,7 +65,9 @@ def _split_worker(rank, world, port, N, seed, q):
 
     a, b = _pair(N, seed, 0)
     try:
-        c = dmul_fourstep(a, b)  # DeviceStages + DistExchange (gloo stages through host memory)
+        # "peer": the fused exchange over CUDA IPC mappings of the other process's buffers;
+        # "alltoall": DeviceStages + DistExchange (gloo stages through host memory)
+        c = dmul_fourstep(a, b, exchange=exchange)
         q.put((rank, None if rank else (c == a * b), c is None))
     except Exception as e:  # noqa: BLE001
         q.put((rank, repr(e), False))
@@ -73,14 +75,15 @@ def _split_worker(rank, world, port, N, seed, q):
 
 
 @pytest.mark.timeout(900)
+@pytest.mark.parametrize("exchange", ["peer", "alltoall"])
 @pytest.mark.parametrize("e", [20, 24])
-def test_fourstep_two_processes(cuda_ok, e):
+def test_fourstep_two_processes(cuda_ok, e, exchange):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_split_worker, args=(r, 2, port, 1 << e, 40 + e, q)) for r in range(2)]
+    procs = [ctx.Process(target=_split_worker, args=(r, 2, port, 1 << e, 40 + e, q, exchange)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted(q.get(timeout=850) for _ in procs)

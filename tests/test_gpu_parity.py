@@ -241,6 +241,28 @@ def test_fourstep_virtual_ranks(cuda_ok, e, world, dist_decode):
     assert dmul_fourstep_virtual(a, b, world, distributed_decode=dist_decode) == a * b
 
 
+@pytest.mark.parametrize("e,world", [(18, 4), (20, 2), (20, 8), (22, 4), (24, 8), (24, 32)])
+def test_fourstep_virtual_fused_exchange(cuda_ok, e, world):
+    # the exchange fused into the phase kernels' stores (dkss_fs_*_peer), emulated ranks' buffers
+    # as the peer table: equal to a*b and to the all-to-all path
+    from paper_1503_04955_b200.fourstep import dmul_fourstep_virtual
+
+    rng = random.Random(300 + e + world)
+    N = 1 << e
+    a = rng.getrandbits(N) | 1 << (N - 1)
+    b = rng.getrandbits(N) | 1 << (N - 1)
+    c = dmul_fourstep_virtual(a, b, world, exchange="peer")
+    if e <= 22:
+        assert c == a * b
+    else:
+        assert c == dmul_fourstep_virtual(a, b, world)
+        for q in (2**61 - 1, 2**62 - 57, 2**59 - 55):
+            assert c % q == (a % q) * (b % q) % q
+    ones = (1 << N) - 1
+    if e <= 20:
+        assert dmul_fourstep_virtual(ones, ones, world, exchange="peer") == ones * ones
+
+
 def test_fourstep_virtual_all_ones(cuda_ok):
     from paper_1503_04955_b200.fourstep import dmul_fourstep_virtual
 
