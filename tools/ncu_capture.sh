@@ -12,6 +12,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
   > gpurun_out/ncu_launches.log 2>&1
 echo "launch list rc=$?"
 $CMD > gpurun_out/plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"${KREGEX:-k_fwd_pass|k_bottom|k_inv_pass}" -c ${KCOUNT:-5} \
+ncu --set full --clock-control none --import-source on -k regex:"${KREGEX:-k_fwd_pass|k_bottom|k_inv_pass|k_tc_twiddle}" -c ${KCOUNT:-9} \
   -o gpurun_out/full_$TAG $CMD > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?"

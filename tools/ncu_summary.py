@@ -15,7 +15,7 @@ import subprocess
 import sys
 from collections import defaultdict
 
-KIND = {"k_rows_dyn": "rows", "k_rows": "rows", "k_fwd_pass": "fwd_pass", "k_fwd_warp": "fwd_pass", "k_dft_cols": "fwd_pass", "k_inv_pass": "inv_pass",
+KIND = {"k_tc_twiddle": "twiddle_tc", "k_rows_dyn": "rows", "k_rows": "rows", "k_fwd_pass": "fwd_pass", "k_fwd_warp": "fwd_pass", "k_dft_cols": "fwd_pass", "k_inv_pass": "inv_pass",
         "k_inv_warp": "inv_pass", "k_bottom": "bottom", "k_decode1": "decode1", "k_decode2": "decode2",
         "k_decode_scan": "decode_scan", "k_encode": "encode"}
 

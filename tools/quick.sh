@@ -1,7 +1,7 @@
 #!/bin/bash
 # parity report + short benches of the main configs (used for iteration on the GPU box)
 python tools/gpu_check.py > gpurun_out/gpu_check.log 2>&1; tail -1 gpurun_out/gpu_check.log
-for c in mul2^20 batch1024x2^18 mul2^24 ${EXTRA_CONFIGS}; do
+for c in mul2^20 batch1024x2^18 mul2^24 mul2^26 mul2^16 ones2^20 ${EXTRA_CONFIGS:-}; do
   python bench.py --config $c --steps ${STEPS:-20} --warmup 3 --no-cpu --e2e-steps 3 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err || tail -5 gpurun_out/bench_$c.err
   python - "$c" <<'PY'
 import json,sys
