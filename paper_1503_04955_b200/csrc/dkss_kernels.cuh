@@ -401,6 +401,87 @@ __device__ __forceinline__ uint32_t* dft_pingpong(uint32_t* buf, uint32_t* alt, 
 }
 
 // ---------------------------------------------------------------------------
+// The same 2m-point DFT for m = 32 with the data in registers: lane k of a warp holds
+// coefficient k of 8 elements, the rotation by alpha^r of a butterfly's second operand is a warp
+// shuffle (lane k reads lane (k - r) mod m) and its negation of the wrapped lanes (k < r) swaps
+// the two outputs.  Eight warps: stages 1-3 on slots [8w, 8w + 8), one exchange through shared
+// memory, stages 4-6 on slots {w + 8i}; in place in `buf` (NE = 64 elements in bit-reversed
+// slots, as dft_pingpong), two shared-memory round trips instead of six and no per-item index
+// arithmetic.
+template <int L, bool R0>
+__device__ __forceinline__ void bfly_reg(uint32_t (&u)[L], uint32_t (&v)[L], int r, int k, const ModCtx& mc) {
+  uint32_t x[L], sm[L], df[L];
+  if constexpr (R0) {
+#pragma unroll
+    for (int q = 0; q < L; ++q) x[q] = v[q];
+  } else {
+    const int src = (k - r) & 31;
+#pragma unroll
+    for (int q = 0; q < L; ++q) x[q] = __shfl_sync(0xFFFFFFFFu, v[q], src);
+  }
+  add_mod<L>(sm, u, x, mc);
+  sub_mod<L>(df, u, x, mc);
+  const bool neg = !R0 && k < r;
+#pragma unroll
+  for (int q = 0; q < L; ++q) {
+    u[q] = neg ? df[q] : sm[q];
+    v[q] = neg ? sm[q] : df[q];
+  }
+}
+
+template <int L>
+__device__ __forceinline__ void dft64_regs(uint32_t* buf, const ModCtx& mc) {
+  constexpr int ES = Smem<32, L>::ES;
+  const int w = threadIdx.x >> 5, k = threadIdx.x & 31;
+  uint32_t x[8][L];
+  // stages 1-3: butterflies inside the slot block [8w, 8w + 8); root alpha^(kk * 64 / size)
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ld_res<L>(x[i], buf + (8 * w + i) * ES + k * L);
+#pragma unroll
+  for (int a = 0; a < 8; a += 2) bfly_reg<L, true>(x[a], x[a + 1], 0, k, mc);  // size 2: kk = 0
+#pragma unroll
+  for (int a = 0; a < 8; a += 4) {  // size 4: kk in {0, 1}, rootstep 16
+    bfly_reg<L, true>(x[a], x[a + 2], 0, k, mc);
+    bfly_reg<L, false>(x[a + 1], x[a + 3], 16, k, mc);
+  }
+  bfly_reg<L, true>(x[0], x[4], 0, k, mc);  // size 8: kk in 0..3, rootstep 8
+  bfly_reg<L, false>(x[1], x[5], 8, k, mc);
+  bfly_reg<L, false>(x[2], x[6], 16, k, mc);
+  bfly_reg<L, false>(x[3], x[7], 24, k, mc);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) st_res<L>(buf + (8 * w + i) * ES + k * L, x[i]);
+  __syncthreads();
+  // stages 4-6: slots w + 8i; size 16 (rootstep 4): kk = w; size 32 (rootstep 2): kk = w + 8 (i & 1);
+  // size 64 (rootstep 1): kk = w + 8 (i & 3)
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ld_res<L>(x[i], buf + (w + 8 * i) * ES + k * L);
+#pragma unroll
+  for (int i = 0; i < 8; i += 2) bfly_reg<L, false>(x[i], x[i + 1], 4 * w, k, mc);
+#pragma unroll
+  for (int i = 0; i < 8; i += 4) {
+    bfly_reg<L, false>(x[i], x[i + 2], 2 * w, k, mc);
+    bfly_reg<L, false>(x[i + 1], x[i + 3], 2 * (w + 8), k, mc);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) bfly_reg<L, false>(x[i], x[i + 4], w + 8 * i, k, mc);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) st_res<L>(buf + (w + 8 * i) * ES + k * L, x[i]);
+  __syncthreads();
+}
+
+// the column DFT of a pass tile: registers for m = 32 (one 64-element column, 8 warps), the
+// shared-memory ping-pong otherwise; returns the buffer holding the result
+template <int MM, int L, int NE>
+__device__ __forceinline__ uint32_t* column_dft(uint32_t* buf, uint32_t* alt, int logn, const ModCtx& mc) {
+  if constexpr (MM == 32 && NE == 64 && Cfg<MM>::NT == 256) {
+    dft64_regs<L>(buf, mc);
+    return buf;
+  } else {
+    return dft_pingpong<MM, L, NE>(buf, alt, logn, mc);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // timing experiments only (tools/exp_build.sh): drop the column DFT or the twiddle products
 #ifdef DKSS_EXP_NODFT
 constexpr bool kExpNoDft = true;
@@ -670,7 +751,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArg
     TRACE_MARK
     mbar_wait(&bar[st], (k >> 1) & 1);
     TRACE_MARK
-    const uint32_t* xv = kExpNoDft ? buf : dft_pingpong<MM, L, NE>(buf, smem + 2 * STAGE, LOGE, mc);
+    const uint32_t* xv = kExpNoDft ? buf : column_dft<MM, L, NE>(buf, smem + 2 * STAGE, LOGE, mc);
     TRACE_MARK
     for (int it = threadIdx.x; it < NE * TPE; it += NT) {
       const int el = it / TPE, k0 = (it % TPE) * kT;
@@ -779,7 +860,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArg
       if (dsl[q] >= 0) store_rot<MM, L, kT>(buf + dsl[q], res[q], ((threadIdx.x + q * NT) % TPE) * kT, rot[q], mc);
     __syncthreads();
     TRACE_MARK
-    const uint32_t* ov = dft_pingpong<MM, L, NE>(buf, smem + 2 * STAGE, LOGE, mc);
+    const uint32_t* ov = column_dft<MM, L, NE>(buf, smem + 2 * STAGE, LOGE, mc);
     for (int it = threadIdx.x; it < NE * MM; it += NT) {
       const int el = it / MM, kk = it % MM;
       const int c = el / E, vv = el % E;
