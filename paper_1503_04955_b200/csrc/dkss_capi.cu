@@ -244,6 +244,7 @@ struct dkss_plan {
   uint32_t* d_twr = nullptr;  // twiddle rows [M/m][2m][L]: Montgomery-form rho^s, then W_s
   uint32_t* d_twr_s = nullptr;  // the same rows times (2M)^-1 R: the last inverse level scales for free
   int grid_pass = 0, grid_bot = 0;  // persistent grid sizes (SMs x resident CTAs)
+  int grid_pass_do = 0;             // DFT-only passes (kt.fwd_do / inv_do), 0 = not used
   int grid_fw = 0, grid_iw = 0;     // warp-per-column kernels (0 = not used)
   int grid_dft = 0, grid_tw = 0;    // split passes (column DFT kernel + elementwise twiddles)
   int pass_mode = 0;                // 0 auto, 1 CTA-fused, 2 warp-fused, 3 split
@@ -721,6 +722,10 @@ int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s, c
       A.wpc = wpc;
       const int gw = (int)std::min<long long>(P->grid_fw, (cols * wpc + kWarpsPerCta - 1) / kWarpsPerCta);
       launch_k(P->kt.fwd_w, dim3(gw), dim3(kWarpsPerCta * 32), P->kt.smem_fwd_w, s, A, P->mc);
+    } else if (A.tw_skip && P->grid_pass_do) {  // DFT only: three CTAs per SM
+      const int gd = (int)std::min<long long>((cols + P->kt.cols - 1) / P->kt.cols, P->grid_pass_do);
+      A.ctr = next_tick(P, (cols + P->kt.cols - 1) / P->kt.cols, gd);
+      launch_k(P->kt.fwd_do, dim3(gd), dim3(P->kt.nt), P->kt.smem_pass_do, s, A, P->mc);
     } else {
       A.ctr = next_tick(P, (cols + P->kt.cols - 1) / P->kt.cols, grid);
       launch_k(P->kt.fwd, dim3(grid), dim3(P->kt.nt), smem_pass(P), s, A, P->mc);
@@ -778,6 +783,10 @@ int launch_inv_levels(dkss_plan* P, uint32_t* poly, int npoly, bool scale_last, 
       A.wpc = 1;
       const int gw = (int)std::min<long long>(P->grid_iw, (cols + kWarpsPerCta - 1) / kWarpsPerCta);
       launch_k(P->kt.inv_w, dim3(gw), dim3(kWarpsPerCta * 32), P->kt.smem_inv_w, s, A, P->mc);
+    } else if (A.tw_skip && P->grid_pass_do) {  // DFT only: three CTAs per SM
+      const int gd = (int)std::min<long long>((cols + P->kt.cols - 1) / P->kt.cols, P->grid_pass_do);
+      A.ctr = next_tick(P, (cols + P->kt.cols - 1) / P->kt.cols, gd);
+      launch_k(P->kt.inv_do, dim3(gd), dim3(P->kt.nt), P->kt.smem_pass_do, s, A, P->mc);
     } else {
       A.ctr = next_tick(P, (cols + P->kt.cols - 1) / P->kt.cols, grid);
       launch_k(P->kt.inv, dim3(grid), dim3(P->kt.nt), smem_pass(P), s, A, P->mc);
@@ -1126,6 +1135,16 @@ int plan_init(dkss_plan* P, const dkss_plan_desc* d, const dkss_plan_opts& opts,
     if (occ_f < 1 || occ_i < 1 || occ_b < 1) return fail(DKSS_EINVAL, "kernels for m=%d L=%d do not fit an SM", m, L);
     P->grid_pass = sms * std::min(occ_f, occ_i);
     P->grid_bot = sms * occ_b;
+    if (kt.fwd_do && !knob_on(DKSS_KNOB("DKSS_NO_DFT_ONLY"))) {
+      int od_f = 0, od_i = 0;
+      for (const void* f : {(const void*)kt.fwd_do, (const void*)kt.inv_do}) {
+        CUCHK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kt.smem_pass_do));
+        CUCHK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      }
+      CUCHK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&od_f, kt.fwd_do, kt.nt, kt.smem_pass_do));
+      CUCHK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&od_i, kt.inv_do, kt.nt, kt.smem_pass_do));
+      P->grid_pass_do = sms * std::min(od_f, od_i);
+    }
     if (kt.fwd_w && !knob_on(DKSS_KNOB("DKSS_NO_WARP_PASS"))) {
       int ofw = 0, oiw = 0;
       CUCHK(cudaFuncSetAttribute((const void*)kt.fwd_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kt.smem_fwd_w));

@@ -709,8 +709,11 @@ __device__ __forceinline__ void cta_encode_tile(const PassArgs& A, long long til
 
 // forward column pass (one level of dkss_fft): column DFT, then twiddle ring product
 // rho^(vv*l*base_pow) = alpha^r * rho_table[s] (bigmul/dkss.py:480-492)
-template <int MM, int L>
-__global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArgs A, ModCtx mc) {
+// DO (DFT only): the table twiddles are the tensor cores' (tw_skip), so no ring products are
+// compiled in -- fewer registers, three CTAs per SM (m = 32: the column DFT in registers needs
+// no ping-pong buffer either)
+template <int MM, int L, bool DO = false>
+__global__ void __launch_bounds__(Cfg<MM>::NT, DO ? 3 : Cfg<MM>::MINB) k_fwd_pass(PassArgs A, ModCtx mc) {
   griddep_launch();
   constexpr int kT = Cfg<MM>::T;
   constexpr int ES = Smem<MM, L>::ES, EST = Smem<MM, L>::EST;
@@ -766,11 +769,11 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArg
       // them to their owners)
       uint32_t* dst = (A.peer_mode && !(A.tw_skip && s != 0)) ? out_elem(A, cg, vv, LOGE, MM * L) : A.poly + off;
       uint32_t w[kT][L];
-      if (s == 0 || kExpNoMac || A.tw_skip) {
+      if (DO || s == 0 || kExpNoMac || A.tw_skip) {
         if (s != 0) r = 0;  // tw_skip: the tensor-core kernel applies rho^e (rotation included)
 #pragma unroll
         for (int t = 0; t < kT; ++t) ld_res<L>(w[t], xv + el * ES + (k0 + t) * L);
-      } else {
+      } else if constexpr (!DO) {
         twiddle_mul<MM, L, kT>(A, xv + el * ES, tws + el * EST, s, k0, mc, w);
       }
       store_rot<MM, L, kT>(dst, w, k0, r, mc);
@@ -786,8 +789,8 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_fwd_pass(PassArg
 }
 
 // inverse (transposed) column pass: twiddle ring product, then column DFT
-template <int MM, int L>
-__global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArgs A, ModCtx mc) {
+template <int MM, int L, bool DO = false>
+__global__ void __launch_bounds__(Cfg<MM>::NT, DO ? 3 : Cfg<MM>::MINB) k_inv_pass(PassArgs A, ModCtx mc) {
   griddep_launch();
   constexpr int kT = Cfg<MM>::T;
   constexpr int ES = Smem<MM, L>::ES, EST = Smem<MM, L>::EST;
@@ -835,7 +838,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArg
       long long l;
       col_elem(A, cg, 0, LOGE, 0, &l);
       const long long s = tw_exp(A, j, l, &rot[q]);
-      if (s != 0 && A.tw_skip) {  // already multiplied (and rotated) by the tensor-core kernel
+      if (s != 0 && (DO || A.tw_skip)) {  // already multiplied (and rotated) by the tensor-core kernel
         rot[q] = 0;
 #pragma unroll
         for (int t = 0; t < kT; ++t) ld_res<L>(res[q][t], buf + el * ES + (k0 + t) * L);
@@ -849,7 +852,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_inv_pass(PassArg
 #pragma unroll
           for (int t = 0; t < kT; ++t) mont_mul<L>(res[q][t], res[q][t], ks, mc);
         }
-      } else {
+      } else if constexpr (!DO) {
         twiddle_mul<MM, L, kT>(A, buf + el * ES, tws + el * EST, s, k0, mc, res[q]);
       }
       dsl[q] = (c * E + bitrev_n(j, LOGE)) * ES;

@@ -12,6 +12,10 @@ namespace dkss {
 struct KTable {
   void (*fwd)(PassArgs, ModCtx);
   void (*inv)(PassArgs, ModCtx);
+  // DFT-only passes (table twiddles on the tensor cores), m = 32; else null
+  void (*fwd_do)(PassArgs, ModCtx);
+  void (*inv_do)(PassArgs, ModCtx);
+  size_t smem_pass_do;
   void (*fwd_w)(PassArgs, ModCtx);  // warp-per-column variants (m <= 16), else null
   void (*inv_w)(PassArgs, ModCtx);
   size_t smem_fwd_w, smem_inv_w;    // dynamic shared memory per CTA (kWarpsPerCta warps)
@@ -48,6 +52,11 @@ KTable make_table() {
   KTable t{};
   t.fwd = k_fwd_pass<MM, L>;
   t.inv = k_inv_pass<MM, L>;
+  if constexpr (MM == 32 && !Cfg<MM>::TWS) {
+    t.fwd_do = k_fwd_pass<MM, L, true>;
+    t.inv_do = k_inv_pass<MM, L, true>;
+    t.smem_pass_do = 2 * SmemPlan<MM, L>::STAGE_PASS * 4;  // two stages, no ping-pong buffer
+  }
   t.tw = k_twiddle<MM, L>;
   if constexpr (MM <= 16) {
     t.fwd_w = k_fwd_warp<MM, L>;
