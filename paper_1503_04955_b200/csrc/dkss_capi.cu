@@ -1696,29 +1696,30 @@ int run_digits_split(dkss_plan* P, const std::vector<size_t>& nd, const uint32_t
   auto* g1 = P->dgraphs.find(key_of(1));
   if (!g0 || !g1) return fail(DKSS_ECUDA, "split graphs evicted");
   long long* off = reinterpret_cast<long long*>(P->h_pin);
-  uint32_t* dig = P->h_pin + head;
   off[0] = 0;
   off[1] = (long long)nd[0];
   off[2] = (long long)(nd[0] + nd[1]);
-  // timing study (experiment builds, DKSS_HOST_TIMING=1): device-side event times of the pieces
+  // the operands go to the device straight from the caller's (pageable) digits: the driver's
+  // pageable path pipelines its own staging with the DMA -- 138 us for a 2^24-bit operand against
+  // 216 us for a copy into our page-locked buffer followed by the transfer (tools/hostreg_probe.py).
+  // Each pageable copy returns once staged, so b's transfer runs while part 0 computes.  (Issuing
+  // the two from two host threads on two streams serialises them in the driver: 130 + 250 us.)
+  // timing study (experiment builds, DKSS_HOST_TIMING=1): device-side events of the pieces
   const bool tev = g_ht && g_ht->on;
   cudaEvent_t te[6] = {};
   if (tev)
     for (auto& e : te) cudaEventCreate(&e);
-  if (nd[0]) par_memcpy(dig, ptrs[0], nd[0] * 4);
   if (tev) cudaEventRecord(te[0], P->cstream);
-  CUCHK(cudaMemcpyAsync(P->d_stage, P->h_pin, (head + nd[0]) * 4, cudaMemcpyHostToDevice, P->cstream));
+  CUCHK(cudaMemcpyAsync(P->d_stage, P->h_pin, head * 4, cudaMemcpyHostToDevice, P->cstream));
+  if (nd[0]) CUCHK(cudaMemcpyAsync(P->d_stage + head, ptrs[0], nd[0] * 4, cudaMemcpyHostToDevice, P->cstream));
   CUCHK(cudaEventRecord(P->ev_ops[0], P->cstream));
   if (tev) cudaEventRecord(te[1], P->cstream);
   CUCHK(cudaStreamWaitEvent(P->stream, P->ev_ops[0], 0));
   CUCHK(P->dgraphs.launch(g0, P->stream));
   if (tev) cudaEventRecord(te[2], P->stream);
   ht_mark("stage_launch_a");
-  if (nd[1]) {
-    par_memcpy(dig + nd[0], ptrs[1], nd[1] * 4);
-    if (tev) cudaEventRecord(te[3], P->cstream);
-    CUCHK(cudaMemcpyAsync(P->d_stage + head + nd[0], dig + nd[0], nd[1] * 4, cudaMemcpyHostToDevice, P->cstream));
-  }
+  if (tev) cudaEventRecord(te[3], P->cstream);
+  if (nd[1]) CUCHK(cudaMemcpyAsync(P->d_stage + head + nd[0], ptrs[1], nd[1] * 4, cudaMemcpyHostToDevice, P->cstream));
   CUCHK(cudaEventRecord(P->ev_ops[1], P->cstream));
   if (tev) cudaEventRecord(te[4], P->cstream);
   CUCHK(cudaStreamWaitEvent(P->stream, P->ev_ops[1], 0));
@@ -1817,18 +1818,12 @@ int run_digits_graph(dkss_plan* P, int batch, bool sq, int nops, const uint32_t*
     }
     off[nops] = o;
     if (nops <= 4) {
-      // one product: each operand's digits are copied in chunks over the host pool, and its H2D
-      // is issued as soon as it is staged, so operand q's transfer overlaps operand q+1's copy
-      size_t sent = 0;  // words of the staging buffer (offsets header + digits) already in flight
-      for (int q = 0; q < nops; ++q) {
-        if (nd[q]) par_memcpy(dig + off[q], ptrs[q], nd[q] * 4);
-        const size_t upto = head + (size_t)off[q + 1];
-        if (upto > sent || q + 1 == nops) {
-          CUCHK(cudaMemcpyAsync(P->d_stage + sent, P->h_pin + sent, (upto - sent) * 4, cudaMemcpyHostToDevice,
-                                P->stream));
-          sent = upto;
-        }
-      }
+      // few operands: the header from the staging buffer, the digits straight from the caller's
+      // pageable memory (the driver pipelines its own staging with the DMA, run_digits_split)
+      CUCHK(cudaMemcpyAsync(P->d_stage, P->h_pin, head * 4, cudaMemcpyHostToDevice, P->stream));
+      for (int q = 0; q < nops; ++q)
+        if (nd[q])
+          CUCHK(cudaMemcpyAsync(P->d_stage + head + off[q], ptrs[q], nd[q] * 4, cudaMemcpyHostToDevice, P->stream));
     } else {
       host_par((size_t)nops, (size_t)o * 4, [&](size_t q) {
         if (nd[q]) memcpy(dig + off[q], ptrs[q], nd[q] * 4);
