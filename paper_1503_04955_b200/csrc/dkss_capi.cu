@@ -723,8 +723,9 @@ int launch_fwd_levels(dkss_plan* P, uint32_t* poly, int npoly, cudaStream_t s, c
       const int gw = (int)std::min<long long>(P->grid_fw, (cols * wpc + kWarpsPerCta - 1) / kWarpsPerCta);
       launch_k(P->kt.fwd_w, dim3(gw), dim3(kWarpsPerCta * 32), P->kt.smem_fwd_w, s, A, P->mc);
     } else if (A.tw_skip && P->grid_pass_do) {  // DFT only: three CTAs per SM
-      const int gd = (int)std::min<long long>((cols + P->kt.cols - 1) / P->kt.cols, P->grid_pass_do);
-      A.ctr = next_tick(P, (cols + P->kt.cols - 1) / P->kt.cols, gd);
+      const long long tiles = (cols + P->kt.cols_do - 1) / P->kt.cols_do;
+      const int gd = (int)std::min<long long>(tiles, P->grid_pass_do);
+      A.ctr = next_tick(P, tiles, gd);
       launch_k(P->kt.fwd_do, dim3(gd), dim3(P->kt.nt), P->kt.smem_pass_do, s, A, P->mc);
     } else {
       A.ctr = next_tick(P, (cols + P->kt.cols - 1) / P->kt.cols, grid);
@@ -784,8 +785,9 @@ int launch_inv_levels(dkss_plan* P, uint32_t* poly, int npoly, bool scale_last, 
       const int gw = (int)std::min<long long>(P->grid_iw, (cols + kWarpsPerCta - 1) / kWarpsPerCta);
       launch_k(P->kt.inv_w, dim3(gw), dim3(kWarpsPerCta * 32), P->kt.smem_inv_w, s, A, P->mc);
     } else if (A.tw_skip && P->grid_pass_do) {  // DFT only: three CTAs per SM
-      const int gd = (int)std::min<long long>((cols + P->kt.cols - 1) / P->kt.cols, P->grid_pass_do);
-      A.ctr = next_tick(P, (cols + P->kt.cols - 1) / P->kt.cols, gd);
+      const long long tiles = (cols + P->kt.cols_do - 1) / P->kt.cols_do;
+      const int gd = (int)std::min<long long>(tiles, P->grid_pass_do);
+      A.ctr = next_tick(P, tiles, gd);
       launch_k(P->kt.inv_do, dim3(gd), dim3(P->kt.nt), P->kt.smem_pass_do, s, A, P->mc);
     } else {
       A.ctr = next_tick(P, (cols + P->kt.cols - 1) / P->kt.cols, grid);

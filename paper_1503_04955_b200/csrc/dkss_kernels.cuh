@@ -82,6 +82,18 @@ struct Cfg<32> {
   static constexpr bool TWS = false;
 };
 
+// column-pass shape: Cfg<MM>, except the DFT-only passes (table twiddles on the tensor cores,
+// DO) at m = 16 take four columns per tile -- 128 elements, 32 KB: a 32-element tile kept too few
+// bytes in flight (the 1024 x 2^18 batch's passes ran at 0.9-2.1 TB/s) -- and run the column DFT
+// in registers (dft32x4_regs)
+template <int MM, bool DO>
+struct PCfg : Cfg<MM> {};
+template <>
+struct PCfg<16, true> {
+  static constexpr int NT = 256, COLS = 4, NE = 128, MINB = 3, T = 2;
+  static constexpr bool TWS = false;
+};
+
 // shared-memory words per CTA, by kernel kind (host uses the same formulas)
 template <int MM, int L>
 struct SmemPlan {
@@ -469,12 +481,86 @@ __device__ __forceinline__ void dft64_regs(uint32_t* buf, const ModCtx& mc) {
   __syncthreads();
 }
 
+// m = 16, four 32-element columns per tile (PCfg<16, true>): half-warp h of warp w holds
+// coefficient k = lane & 15 of 8 elements of column c = 2 (w >> 2) + h; rotations are shuffles
+// inside the half-warp.  Stages 1-3 on slots [8b, 8b + 8), b = w & 3; one exchange through shared
+// memory; stages 4-5 on slots {b' + 8i}, b' in {2 (w & 3), 2 (w & 3) + 1}, i < 4.
+template <int L, bool R0>
+__device__ __forceinline__ void bfly_reg16(uint32_t (&u)[L], uint32_t (&v)[L], int r, int k, int h,
+                                           const ModCtx& mc) {
+  uint32_t x[L], sm[L], df[L];
+  if constexpr (R0) {
+#pragma unroll
+    for (int q = 0; q < L; ++q) x[q] = v[q];
+  } else {
+    const int src = (h << 4) | ((k - r) & 15);
+#pragma unroll
+    for (int q = 0; q < L; ++q) x[q] = __shfl_sync(0xFFFFFFFFu, v[q], src);
+  }
+  add_mod<L>(sm, u, x, mc);
+  sub_mod<L>(df, u, x, mc);
+  const bool neg = !R0 && k < r;
+#pragma unroll
+  for (int q = 0; q < L; ++q) {
+    u[q] = neg ? df[q] : sm[q];
+    v[q] = neg ? sm[q] : df[q];
+  }
+}
+
+template <int L>
+__device__ __forceinline__ void dft32x4_regs(uint32_t* buf, const ModCtx& mc) {
+  constexpr int ES = Smem<16, L>::ES;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, h = lane >> 4, k = lane & 15;
+  uint32_t* col = buf + (2 * (w >> 2) + h) * 32 * ES;
+  const int b = w & 3;
+  uint32_t x[8][L];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ld_res<L>(x[i], col + (8 * b + i) * ES + k * L);
+  // size 2: kk = 0; size 4 (rootstep 8): kk in {0, 1}; size 8 (rootstep 4): kk in 0..3
+#pragma unroll
+  for (int a = 0; a < 8; a += 2) bfly_reg16<L, true>(x[a], x[a + 1], 0, k, h, mc);
+#pragma unroll
+  for (int a = 0; a < 8; a += 4) {
+    bfly_reg16<L, true>(x[a], x[a + 2], 0, k, h, mc);
+    bfly_reg16<L, false>(x[a + 1], x[a + 3], 8, k, h, mc);
+  }
+  bfly_reg16<L, true>(x[0], x[4], 0, k, h, mc);
+  bfly_reg16<L, false>(x[1], x[5], 4, k, h, mc);
+  bfly_reg16<L, false>(x[2], x[6], 8, k, h, mc);
+  bfly_reg16<L, false>(x[3], x[7], 12, k, h, mc);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) st_res<L>(col + (8 * b + i) * ES + k * L, x[i]);
+  __syncthreads();
+  // x[2 g + i'] = slot b' + 8 i', b' = 2 b + g: size 16 (rootstep 2): pairs i' (0, 1), (2, 3), kk =
+  // b'; size 32 (rootstep 1): pairs i' (0, 2), (1, 3), kk = b' + 8 i'
+#pragma unroll
+  for (int g = 0; g < 2; ++g)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ld_res<L>(x[4 * g + i], col + (2 * b + g + 8 * i) * ES + k * L);
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    const int bp = 2 * b + g;
+    bfly_reg16<L, false>(x[4 * g + 0], x[4 * g + 1], 2 * bp, k, h, mc);
+    bfly_reg16<L, false>(x[4 * g + 2], x[4 * g + 3], 2 * bp, k, h, mc);
+    bfly_reg16<L, false>(x[4 * g + 0], x[4 * g + 2], bp, k, h, mc);
+    bfly_reg16<L, false>(x[4 * g + 1], x[4 * g + 3], bp + 8, k, h, mc);
+  }
+#pragma unroll
+  for (int g = 0; g < 2; ++g)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) st_res<L>(col + (2 * b + g + 8 * i) * ES + k * L, x[4 * g + i]);
+  __syncthreads();
+}
+
 // the column DFT of a pass tile: registers for m = 32 (one 64-element column, 8 warps), the
 // shared-memory ping-pong otherwise; returns the buffer holding the result
 template <int MM, int L, int NE>
 __device__ __forceinline__ uint32_t* column_dft(uint32_t* buf, uint32_t* alt, int logn, const ModCtx& mc) {
   if constexpr (MM == 32 && NE == 64 && Cfg<MM>::NT == 256) {
     dft64_regs<L>(buf, mc);
+    return buf;
+  } else if constexpr (MM == 16 && NE == 128) {
+    dft32x4_regs<L>(buf, mc);
     return buf;
   } else {
     return dft_pingpong<MM, L, NE>(buf, alt, logn, mc);
@@ -612,12 +698,12 @@ __device__ __forceinline__ long long tw_exp(const PassArgs& A, int j, long long 
 // warp, so 2*NE copies from one warp cost microseconds)
 // part: 3 = everything; 1 = arm the barrier + twiddle rows (independent of the previous
 // kernel's output, issued before griddep_wait); 2 = the column elements
-template <int MM, int L, bool FWD>
+template <int MM, int L, bool FWD, class C = Cfg<MM>>
 __device__ __forceinline__ void issue_pass_tile(const PassArgs& A, long long tile, uint64_t* bar, uint32_t* buf,
                                                 uint32_t* tws, bool load_elems = true, int part = 3) {
   constexpr int ES = Smem<MM, L>::ES, EST = Smem<MM, L>::EST;
-  constexpr int NE = Cfg<MM>::NE, COLS = Cfg<MM>::COLS, E = 2 * MM, LOGE = Geo<MM>::LOGE;
-  constexpr int NW = kSpreadIssue ? Cfg<MM>::NT / 32 : 1;
+  constexpr int NE = C::NE, COLS = C::COLS, E = 2 * MM, LOGE = Geo<MM>::LOGE;
+  constexpr int NW = kSpreadIssue ? C::NT / 32 : 1;
   constexpr uint32_t EB = MM * L * 4, TB = 2 * MM * L * 4;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (warp == 0 && (part & 1)) {
@@ -626,7 +712,7 @@ __device__ __forceinline__ void issue_pass_tile(const PassArgs& A, long long til
       const long long cg = tile * COLS + e / E;
       if (cg >= A.total_cols) continue;
       if (load_elems) bytes += EB;
-      if constexpr (Cfg<MM>::TWS) {
+      if constexpr (C::TWS) {
         long long l;
         col_elem(A, cg, 0, LOGE, 0, &l);
         int r;
@@ -647,7 +733,7 @@ __device__ __forceinline__ void issue_pass_tile(const PassArgs& A, long long til
     if (q < NE) {
       const int slot = FWD ? c * E + bitrev_n(j, LOGE) : e;
       if (load_elems && (part & 2)) bulk_g2s(buf + slot * ES, A.poly + off, EB, bar);
-    } else if constexpr (Cfg<MM>::TWS) {
+    } else if constexpr (C::TWS) {
       if (!(part & 1) || A.tw_skip) continue;
       int r;
       const long long s = tw_exp(A, j, l, &r);
@@ -671,9 +757,9 @@ __device__ __forceinline__ void twiddle_mul(const PassArgs& A, const uint32_t* x
 // fused dkss_encode (bigmul/dkss.py:381-398) for the first forward level: coefficient k of
 // element pos is bits [u(pos*m/2 + k), +u) of the operand for pos < M, k < m/2, else 0;
 // written straight into the column buffer at the bit-reversed slot
-template <int MM, int L>
+template <int MM, int L, class C = Cfg<MM>>
 __device__ __forceinline__ void cta_encode_tile(const PassArgs& A, long long tile, uint32_t* buf) {
-  constexpr int ES = Smem<MM, L>::ES, NT = Cfg<MM>::NT, NE = Cfg<MM>::NE, COLS = Cfg<MM>::COLS;
+  constexpr int ES = Smem<MM, L>::ES, NT = C::NT, NE = C::NE, COLS = C::COLS;
   constexpr int E = 2 * MM, LOGE = Geo<MM>::LOGE, HALF = MM / 2;
   for (int it = threadIdx.x; it < NE * MM; it += NT) {
     const int el = it / MM, k = it % MM;
@@ -715,10 +801,11 @@ __device__ __forceinline__ void cta_encode_tile(const PassArgs& A, long long til
 template <int MM, int L, bool DO = false>
 __global__ void __launch_bounds__(Cfg<MM>::NT, DO ? 3 : Cfg<MM>::MINB) k_fwd_pass(PassArgs A, ModCtx mc) {
   griddep_launch();
-  constexpr int kT = Cfg<MM>::T;
+  using C = PCfg<MM, DO>;
+  constexpr int kT = C::T;
   constexpr int ES = Smem<MM, L>::ES, EST = Smem<MM, L>::EST;
-  constexpr int NT = Cfg<MM>::NT, NE = Cfg<MM>::NE, COLS = Cfg<MM>::COLS, E = 2 * MM, LOGE = Geo<MM>::LOGE;
-  constexpr int STAGE = SmemPlan<MM, L>::STAGE_PASS;
+  constexpr int NT = C::NT, NE = C::NE, COLS = C::COLS, E = 2 * MM, LOGE = Geo<MM>::LOGE;
+  constexpr int STAGE = NE * ES + (C::TWS ? NE * EST : 0);
   constexpr int TPE = MM / kT;
   extern __shared__ __align__(16) uint32_t smem[];
   __shared__ __align__(8) uint64_t bar[2];
@@ -735,20 +822,20 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, DO ? 3 : Cfg<MM>::MINB) k_fwd_pas
   // PDL: the twiddle rows do not depend on the previous kernel; the elements (and, for the
   // fused encode, the operands) do
   if (tile < ntiles && (kSpreadIssue || threadIdx.x < 32))
-    issue_pass_tile<MM, L, true>(A, tile, &bar[0], smem, smem + NE * ES, !enc, 1);
+    issue_pass_tile<MM, L, true, C>(A, tile, &bar[0], smem, smem + NE * ES, !enc, 1);
   griddep_wait();
   if (tile < ntiles && (kSpreadIssue || threadIdx.x < 32))
-    issue_pass_tile<MM, L, true>(A, tile, &bar[0], smem, smem + NE * ES, !enc, 2);
+    issue_pass_tile<MM, L, true, C>(A, tile, &bar[0], smem, smem + NE * ES, !enc, 2);
   for (int k = 0; tile < ntiles; ++k) {
     const int st = k & 1;
     uint32_t* buf = smem + st * STAGE;
     uint32_t* tws = buf + NE * ES;
     const long long nxt = grab_tile(A.ctr, tile, &s_tile);
     if (nxt < ntiles && (kSpreadIssue || threadIdx.x < 32))
-      issue_pass_tile<MM, L, true>(A, nxt, &bar[st ^ 1], smem + (st ^ 1) * STAGE, smem + (st ^ 1) * STAGE + NE * ES,
+      issue_pass_tile<MM, L, true, C>(A, nxt, &bar[st ^ 1], smem + (st ^ 1) * STAGE, smem + (st ^ 1) * STAGE + NE * ES,
                                    !enc);
     if (enc) {
-      cta_encode_tile<MM, L>(A, tile, buf);
+      cta_encode_tile<MM, L, C>(A, tile, buf);
       __syncthreads();
     }
     TRACE_MARK
@@ -792,10 +879,11 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, DO ? 3 : Cfg<MM>::MINB) k_fwd_pas
 template <int MM, int L, bool DO = false>
 __global__ void __launch_bounds__(Cfg<MM>::NT, DO ? 3 : Cfg<MM>::MINB) k_inv_pass(PassArgs A, ModCtx mc) {
   griddep_launch();
-  constexpr int kT = Cfg<MM>::T;
+  using C = PCfg<MM, DO>;
+  constexpr int kT = C::T;
   constexpr int ES = Smem<MM, L>::ES, EST = Smem<MM, L>::EST;
-  constexpr int NT = Cfg<MM>::NT, NE = Cfg<MM>::NE, COLS = Cfg<MM>::COLS, E = 2 * MM, LOGE = Geo<MM>::LOGE;
-  constexpr int STAGE = SmemPlan<MM, L>::STAGE_PASS;
+  constexpr int NT = C::NT, NE = C::NE, COLS = C::COLS, E = 2 * MM, LOGE = Geo<MM>::LOGE;
+  constexpr int STAGE = NE * ES + (C::TWS ? NE * EST : 0);
   constexpr int TPE = MM / kT;
   constexpr int PER = (NE * TPE + NT - 1) / NT;
   extern __shared__ __align__(16) uint32_t smem[];
@@ -810,17 +898,17 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, DO ? 3 : Cfg<MM>::MINB) k_inv_pas
   __shared__ long long s_tile;
   long long tile = grab_tile(A.ctr, -1, &s_tile);
   if (tile < ntiles && (kSpreadIssue || threadIdx.x < 32))
-    issue_pass_tile<MM, L, false>(A, tile, &bar[0], smem, smem + NE * ES, true, 1);
+    issue_pass_tile<MM, L, false, C>(A, tile, &bar[0], smem, smem + NE * ES, true, 1);
   griddep_wait();  // PDL: twiddle rows above are independent of the previous kernel
   if (tile < ntiles && (kSpreadIssue || threadIdx.x < 32))
-    issue_pass_tile<MM, L, false>(A, tile, &bar[0], smem, smem + NE * ES, true, 2);
+    issue_pass_tile<MM, L, false, C>(A, tile, &bar[0], smem, smem + NE * ES, true, 2);
   for (int k = 0; tile < ntiles; ++k) {
     const int st = k & 1;
     uint32_t* buf = smem + st * STAGE;
     uint32_t* tws = buf + NE * ES;
     const long long nxt = grab_tile(A.ctr, tile, &s_tile);
     if (nxt < ntiles && (kSpreadIssue || threadIdx.x < 32))
-      issue_pass_tile<MM, L, false>(A, nxt, &bar[st ^ 1], smem + (st ^ 1) * STAGE, smem + (st ^ 1) * STAGE + NE * ES);
+      issue_pass_tile<MM, L, false, C>(A, nxt, &bar[st ^ 1], smem + (st ^ 1) * STAGE, smem + (st ^ 1) * STAGE + NE * ES);
     TRACE_MARK
     mbar_wait(&bar[st], (k >> 1) & 1);
     TRACE_MARK

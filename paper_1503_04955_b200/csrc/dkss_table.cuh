@@ -12,10 +12,11 @@ namespace dkss {
 struct KTable {
   void (*fwd)(PassArgs, ModCtx);
   void (*inv)(PassArgs, ModCtx);
-  // DFT-only passes (table twiddles on the tensor cores), m = 32; else null
+  // DFT-only passes (table twiddles on the tensor cores), m in {16, 32}; else null
   void (*fwd_do)(PassArgs, ModCtx);
   void (*inv_do)(PassArgs, ModCtx);
   size_t smem_pass_do;
+  int cols_do;  // columns per tile of the DFT-only passes (PCfg)
   void (*fwd_w)(PassArgs, ModCtx);  // warp-per-column variants (m <= 16), else null
   void (*inv_w)(PassArgs, ModCtx);
   size_t smem_fwd_w, smem_inv_w;    // dynamic shared memory per CTA (kWarpsPerCta warps)
@@ -52,10 +53,13 @@ KTable make_table() {
   KTable t{};
   t.fwd = k_fwd_pass<MM, L>;
   t.inv = k_inv_pass<MM, L>;
-  if constexpr (MM == 32 && !Cfg<MM>::TWS) {
+  if constexpr (MM == 32 || MM == 16) {
+    using PC = PCfg<MM, true>;
+    static_assert(!PC::TWS, "DFT-only passes stage no twiddle rows");
     t.fwd_do = k_fwd_pass<MM, L, true>;
     t.inv_do = k_inv_pass<MM, L, true>;
-    t.smem_pass_do = 2 * SmemPlan<MM, L>::STAGE_PASS * 4;  // two stages, no ping-pong buffer
+    t.smem_pass_do = 2 * PC::NE * Smem<MM, L>::ES * 4;  // two stages; the register DFT needs no ping-pong
+    t.cols_do = PC::COLS;
   }
   t.tw = k_twiddle<MM, L>;
   if constexpr (MM <= 16) {

@@ -451,3 +451,15 @@ def test_tensor_core_twiddles_match_cuda_cores(cuda_ok, e):
     assert u32_to_int(tcp.mul_limbs(ones, ones, npl)) == ((1 << N) - 1) ** 2
     tcp.close()
     cup.close()
+
+
+def test_dmul_without_cpython_digit_layout(cuda_ok, rng, monkeypatch):
+    # the e2e path's fallback when the interpreter's int layout is not the checked one: operands
+    # go to the C ABI as 32-bit limbs (int_to_u32) instead of CPython's 30-bit digits
+    from paper_1503_04955_b200 import words
+
+    monkeypatch.setattr(words, "_PYLONG_OK", False)
+    for e in (12, 20, 24):
+        a = rng.getrandbits(1 << e) | 1 << ((1 << e) - 1)
+        b = rng.getrandbits((1 << e) - 7) | 1
+        assert dmul(a, b).to_int() == a * b

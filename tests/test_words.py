@@ -59,3 +59,28 @@ def test_scratch_arena_peak():
             a.alloc_words(5)
         a.alloc_words(1)
     assert a.pos == 0 and a.peak_words == 15
+
+
+def test_pylong_digits_layout_and_fallback(monkeypatch):
+    # e2e hands CPython's own 30-bit int digits to the C ABI (words.pylong_digits, checked
+    # against the interpreter's int layout at import); without that layout (another
+    # interpreter, a layout change) the operand goes as 32-bit limbs instead -- same product
+    import ctypes
+
+    import numpy as np
+
+    from paper_1503_04955_b200 import dkss, words
+
+    x = (1 << 1000) + 12345678901234567890
+    d = words.pylong_digits(x)
+    if d is not None:  # CPython >= 3.12: the digits read back are the int's base-2^30 digits
+        ptr, n = d
+        got = np.ctypeslib.as_array((ctypes.c_uint32 * n).from_address(ptr)).copy()
+        want = [(x >> (30 * i)) & ((1 << 30) - 1) for i in range(n)]
+        assert got.tolist() == want
+        keep, p, cnt, bits = dkss._digits(x, x)
+        assert (p, cnt) == (ptr, n) and bits & 0xFF == words.PYLONG_DIGIT_BITS
+    monkeypatch.setattr(words, "_PYLONG_OK", False)
+    assert words.pylong_digits(x) is None
+    keep, p, cnt, bits = dkss._digits(x, x)
+    assert bits == 32 and np.array_equal(keep, words.int_to_u32(x, cnt))
