@@ -481,6 +481,64 @@ __device__ __forceinline__ void dft64_regs(uint32_t* buf, const ModCtx& mc) {
   __syncthreads();
 }
 
+// the base-case DFT of the bottom kernel for m = 32, b = 16 (2^24: four groups of 16 elements per
+// 64-element tile, root alpha^4): stages 1-3 exactly as dft64_regs's (same roots), then stage 4
+// (pairs (16g + i, 16g + 8 + i), root alpha^(4i)) after one exchange through shared memory
+template <int L>
+__device__ __forceinline__ void dft16x4_regs(uint32_t* buf, const ModCtx& mc) {
+  constexpr int ES = Smem<32, L>::ES;
+  const int w = threadIdx.x >> 5, k = threadIdx.x & 31;
+  uint32_t x[8][L];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ld_res<L>(x[i], buf + (8 * w + i) * ES + k * L);
+#pragma unroll
+  for (int a = 0; a < 8; a += 2) bfly_reg<L, true>(x[a], x[a + 1], 0, k, mc);
+#pragma unroll
+  for (int a = 0; a < 8; a += 4) {
+    bfly_reg<L, true>(x[a], x[a + 2], 0, k, mc);
+    bfly_reg<L, false>(x[a + 1], x[a + 3], 16, k, mc);
+  }
+  bfly_reg<L, true>(x[0], x[4], 0, k, mc);
+  bfly_reg<L, false>(x[1], x[5], 8, k, mc);
+  bfly_reg<L, false>(x[2], x[6], 16, k, mc);
+  bfly_reg<L, false>(x[3], x[7], 24, k, mc);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) st_res<L>(buf + (8 * w + i) * ES + k * L, x[i]);
+  __syncthreads();
+  // warp w: group g = w >> 1, i in [4 (w & 1), 4 (w & 1) + 4): x[2t] = slot 16g + i, x[2t+1] = +8
+  const int g = w >> 1, i0 = 4 * (w & 1);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    ld_res<L>(x[2 * t], buf + (16 * g + i0 + t) * ES + k * L);
+    ld_res<L>(x[2 * t + 1], buf + (16 * g + 8 + i0 + t) * ES + k * L);
+  }
+#pragma unroll
+  for (int t = 0; t < 4; ++t) bfly_reg<L, false>(x[2 * t], x[2 * t + 1], 4 * (i0 + t), k, mc);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    st_res<L>(buf + (16 * g + i0 + t) * ES + k * L, x[2 * t]);
+    st_res<L>(buf + (16 * g + 8 + i0 + t) * ES + k * L, x[2 * t + 1]);
+  }
+  __syncthreads();
+}
+
+// base-case DFT of a bottom tile: registers where a version exists (m = 32, b = 64 or 16), else
+// the shared-memory ping-pong; returns the buffer holding the result
+template <int MM, int L, int NE>
+__device__ __forceinline__ uint32_t* base_dft(uint32_t* buf, uint32_t* alt, int logb, const ModCtx& mc) {
+  if constexpr (MM == 32 && NE == 64 && Cfg<MM>::NT == 256) {
+    if (logb == 6) {
+      dft64_regs<L>(buf, mc);
+      return buf;
+    }
+    if (logb == 4) {
+      dft16x4_regs<L>(buf, mc);
+      return buf;
+    }
+  }
+  return dft_pingpong<MM, L, NE>(buf, alt, logb, mc);
+}
+
 // m = 16, four 32-element columns per tile (PCfg<16, true>): half-warp h of warp w holds
 // coefficient k = lane & 15 of 8 elements of column c = 2 (w >> 2) + h; rotations are shuffles
 // inside the half-warp.  Stages 1-3 on slots [8b, 8b + 8), b = w & 3; one exchange through shared
@@ -1058,10 +1116,10 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_bottom(BottomArg
     mbar_wait(&bar[st], NS == 2 ? ((k >> 1) & 1) : (k & 1));
     const long long e0 = tile * NE;
     // three NE-element buffers {sa, sb, wr} serve as DFT ping-pong space and results
-    uint32_t* ra = dft_pingpong<MM, L, NE>(sa, wr, A.logb, mc);
+    uint32_t* ra = base_dft<MM, L, NE>(sa, wr, A.logb, mc);
     uint32_t* out = ra;
     if (two) {
-      uint32_t* rb = dft_pingpong<MM, L, NE>(sb, ra == sa ? wr : sa, A.logb, mc);
+      uint32_t* rb = base_dft<MM, L, NE>(sb, ra == sa ? wr : sa, A.logb, mc);
       __syncthreads();
       uint32_t res[PER][kT][L];
       int dsts[PER];
@@ -1084,7 +1142,7 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, Cfg<MM>::MINB) k_bottom(BottomArg
           for (int t = 0; t < kT; ++t) st_res<L>(ra + dsts[q] + t * L, res[q][t]);
         }
       __syncthreads();
-      out = dft_pingpong<MM, L, NE>(ra, rb, A.logb, mc);
+      out = base_dft<MM, L, NE>(ra, rb, A.logb, mc);
     }
     for (int it = threadIdx.x; it < NE * MM; it += NT) {
       const int el = it / MM, kk = it % MM;
