@@ -263,7 +263,8 @@ __device__ __forceinline__ void reduce_coeff(const int32_t (&Z)[32], uint32_t p3
 //     TMEM buffer, then reduce (tc::reduce_coeff) and store.
 template <int MM>
 __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
-  griddep_wait();  // PDL: the column pass that produced the elements has completed
+  // PDL: the set-up, the first tile's schedule entries and V table (constants of the plan) overlap
+  // the tail of the column pass; only the element gather waits for it (griddep_wait below)
   griddep_launch();
   using S = TcSmem<MM>;
   constexpr int K = S::K, NCH = MM * 32 / kTcNChunk, KSTEPS = K / 32;
@@ -330,6 +331,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
         tc::mbar_arrive_tx(&full[st], S::VBYTES);
         tc::bulk_g2s(sV, A.vtab + (size_t)hs * S::VBYTES, S::VBYTES, &full[st]);
       }
+      if (k == 0) griddep_wait();  // the column pass that produced the elements has completed
 #ifndef DKSS_TC_EXP_NOLOAD  // experiment builds only: time the pipeline without the element gather
 #pragma unroll
       for (int i = 0; i < GPW; ++i) {
@@ -381,6 +383,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
     }
   } else if (warp < kTcEpiWarps) {
     // ===== epilogue =====
+    griddep_wait();  // its stores overwrite elements the previous kernel wrote
     const int quad = warp & 3;
     const int row = 32 * quad + lane;
     int g = 0;

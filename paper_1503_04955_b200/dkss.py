@@ -213,6 +213,10 @@ def _deliver(n: Natural, cls):
 def _as_int_len(x, w: int):
     """(value, word length at word size w) exactly as as_natural(x) would give
     (bigmul/words.py:112-117); a foreign Natural's words are read at its own word size w."""
+    if type(x) is int:  # the common case first
+        if x < 0:
+            raise ValueError("Natural is nonnegative")
+        return x, max(1, -(-x.bit_length() // w))
     if isinstance(x, Natural):
         return x.to_int(w), len(x)
     if foreign_natural(x) is not None:
