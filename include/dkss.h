@@ -139,7 +139,7 @@ int dkss_mul_device(dkss_plan* plan, int batch, const uint32_t* a_dev, const uin
  * a CUDA event is recorded on `stream` after every kernel; for launch i, kinds[i] is a
  * DKSS_K_* id, ms[i] its event-to-event duration, work[i] the algorithmic 32x32->64 limb
  * products it performs (ring products x m^2 L^2) -- for DKSS_K_TWIDDLE_TC the
- * int8 operations of its byte GEMM on the live rows (rows x 16m x 32m x 2) -- and bytes[i] the
+ * int8 operations of its byte GEMM on the live rows (rows x 16m x 16m x 2) -- and bytes[i] the
  * stage-boundary HBM bytes of the §8(d) model.  c_dev receives the product (product_limbs). */
 #define DKSS_K_ENCODE 0
 #define DKSS_K_FWD_PASS 1

@@ -257,7 +257,7 @@ struct dkss_plan {
   bool tc_forced = false;           // DKSS_TWIDDLE_TENSOR: every full-layout launch uses them
   int tc_grid = 0;                  // SMs (one tensor-core CTA per SM)
   uint32_t tc_p3 = 0;               // p = 1 + tc_p3 * 2^96
-  uint8_t* d_vtab = nullptr;        // V tables of d_twr rows, [M/m][2m-1][32][16]
+  uint8_t* d_vtab = nullptr;        // V tables of d_twr rows, [M/m][2m-1][16][16]
   uint8_t* d_vtab_s = nullptr;      // of the pre-scaled rows d_twr_s (last inverse level)
   std::map<std::tuple<int, long long, bool, int, int>, TcSched> tc_sched;  // by TcLayout
   int tick_next = 0;
@@ -621,7 +621,7 @@ int launch_tc_layout(dkss_plan* P, uint32_t* poly, const TcLayout& lay, bool sca
   CUCHK(cudaGetLastError());
   // work: the byte-GEMM's int8 operations on the live rows (rows x K x N x 2, K = 16m, N = 32m);
   // bytes: elements read and written once, one V table per tile
-  mark(P, s, DKSS_K_TWIDDLE_TC, 2LL * sc->twiddled * (16LL * P->m) * (32LL * P->m),
+  mark(P, s, DKSS_K_TWIDDLE_TC, 2LL * sc->twiddled * (16LL * P->m) * (16LL * P->m),
        2LL * sc->twiddled * P->m * P->L * 4 + (long long)sc->ntiles * (long long)P->kt.tc_vbytes);
   return 0;
 }
@@ -850,7 +850,18 @@ int launch_decode(dkss_plan* P, const uint32_t* v, uint32_t* out, int npoly, cud
   A.L = P->L;
   A.u = P->u;
   const int grid = A.blocks_per_poly * npoly;
-  launch_k(k_decode1, dim3(grid), dim3(kDecThreads), 0, s, A);
+  void (*k1)(DecodeArgs) = k_decode1;
+  if (!sglob && A.u == 32) {
+    switch (A.L) {
+      case 2: k1 = k_decode1_u32<2>; break;
+      case 3: k1 = k_decode1_u32<3>; break;
+      case 4: k1 = k_decode1_u32<4>; break;
+      case 5: k1 = k_decode1_u32<5>; break;
+      case 6: k1 = k_decode1_u32<6>; break;
+      default: break;
+    }
+  }
+  launch_k(k1, dim3(grid), dim3(kDecThreads), 0, s, A);
   CUCHK(cudaGetLastError());
   mark(P, s, DKSS_K_DECODE1, 0, npoly * (P->poly_words * 4 + P->prod_limbs * 4));
   launch_carry_tail(A, npoly, s);
@@ -1173,8 +1184,10 @@ int plan_init(dkss_plan* P, const dkss_plan_desc* d, const dkss_plan_opts& opts,
     // table twiddles on the tensor cores: kernels exist for m in {16, 32} at L = 4, the epilogue
     // needs a Proth prime p = 1 + p3 2^96, and the split column passes are CTA kernels
     {
+      // epilogue bounds (dkss_tc.cuh reduce_coeff16): p in (2^127, 2^128 - 2^113), and p / 2 within
+      // the range of 16 balanced base-256 digits
       const bool tc_ok = kt.tc && L == 4 && P->mc.proth && P->levels >= 1 && d->p[1] == 0 && d->p[2] == 0 &&
-                         d->p[3] >= 64u;  // p > 2^102: the epilogue's single conditional subtraction
+                         d->p[3] >= 0x80000000u && d->p[3] <= 0xFEFEFEFEu;
       if (opts.twiddle == DKSS_TWIDDLE_TENSOR && !tc_ok)
         return fail(DKSS_EINVAL, "tensor-core twiddles need m in {16, 32}, L = 4 and a Proth prime (m=%d L=%d)", m, L);
       P->tc = tc_ok && opts.twiddle != DKSS_TWIDDLE_CUDA && P->pass_mode <= DKSS_PASS_CTA;
@@ -1292,14 +1305,21 @@ int plan_init(dkss_plan* P, const dkss_plan_desc* d, const dkss_plan_opts& opts,
     e = cudaGetLastError();
   }
   if (e == cudaSuccess && P->tc) {
-    // V tables of the tensor-core twiddles, from the expanded rows; c160 = 2^160 mod p
-    Limbs c(L, 0);
-    c[0] = 1;
-    for (int i = 0; i < 160; ++i) dbl_mod(c, p);
+    // V tables of the tensor-core twiddles, from the expanded rows; ck[k] = 2^(32 + 8k) mod p
+    std::vector<uint32_t> ck;
+    {
+      Limbs c(L, 0);
+      c[0] = 1;
+      for (int i = 0; i < 32; ++i) dbl_mod(c, p);
+      for (int k = 0; k < 16; ++k) {
+        ck.insert(ck.end(), c.begin(), c.end());
+        for (int i = 0; i < 8; ++i) dbl_mod(c, p);
+      }
+    }
     uint32_t* d_c = nullptr;
     const size_t vbytes = (size_t)(M / m) * kt.tc_vbytes;
-    e = cudaMalloc(&d_c, 4 * L);
-    if (e == cudaSuccess) e = cudaMemcpy(d_c, c.data(), 4 * L, cudaMemcpyHostToDevice);
+    e = cudaMalloc(&d_c, 4 * ck.size());
+    if (e == cudaSuccess) e = cudaMemcpy(d_c, ck.data(), 4 * ck.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&P->d_vtab, vbytes);
     if (e == cudaSuccess) e = cudaMalloc(&P->d_vtab_s, vbytes);
     const int gb = (int)std::min<long long>(((long long)(M / m) * (2 * m - 1) + 127) / 128, 4096);

@@ -1463,6 +1463,65 @@ __global__ void __launch_bounds__(kDecThreads) k_decode1(DecodeArgs A) {
   });
 }
 
+// decode1 for u = 32 with the residues staged: slot s = l*m/2 + k holds residue k of element l
+// and residue k + m/2 of element l - 1, and limb q of slot s lands on output limb s + q.  The
+// block's 256 + L slots are read once, each residue as one vector load (consecutive slots are
+// consecutive residues: coalesced), their per-limb pair sums go to shared memory, and
+// S_t = sum_q P[t - q][q] is summed from there -- instead of L dependent strided scalar loads
+// per limb (window_sum)
+template <int L>
+__global__ void __launch_bounds__(kDecThreads) k_decode1_u32(DecodeArgs A) {
+  griddep_wait();  // PDL: predecessor grid complete, its writes visible
+  griddep_launch();
+  __shared__ unsigned long long sP[(kDecThreads + L) * L];
+  const int pidx = blockIdx.x / A.blocks_per_poly;
+  const long long t0 = (long long)(blockIdx.x % A.blocks_per_poly) * kDecThreads;
+  const uint32_t* v = A.v + (long long)pidx * A.poly_words;
+  const long long twoM = 2LL * A.M;
+  const int half = A.MM / 2, lh = __ffs(half) - 1;
+  for (int i = threadIdx.x; i < kDecThreads + L; i += kDecThreads) {
+    const long long s = t0 - L + i;
+    unsigned long long acc[L];
+#pragma unroll
+    for (int q = 0; q < L; ++q) acc[q] = 0;
+    if (s >= 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const long long l = (s >> lh) - h;
+        if (l < 0 || l >= twoM) continue;
+        const long long src = (twoM - l) & (twoM - 1);
+        const uint32_t* c = v + (src * A.MM + (s & (half - 1)) + h * half) * L;
+        uint32_t w[L];
+        if constexpr (L == 4) {
+          const uint4 x = __ldg(reinterpret_cast<const uint4*>(c));
+          w[0] = x.x, w[1] = x.y, w[2] = x.z, w[3] = x.w;
+        } else if constexpr (L % 2 == 0) {
+#pragma unroll
+          for (int q = 0; q < L; q += 2) {
+            const uint2 x = __ldg(reinterpret_cast<const uint2*>(c + q));
+            w[q] = x.x, w[q + 1] = x.y;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < L; ++q) w[q] = __ldg(c + q);
+        }
+#pragma unroll
+        for (int q = 0; q < L; ++q) acc[q] += w[q];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < L; ++q) sP[i * L + q] = acc[q];
+  }
+  __syncthreads();
+  decode1_body(A, [&](int, long long t) {
+    const int i = (int)(t - t0) + L;  // slot index of t inside sP (t >= t0 - 1)
+    unsigned long long S = 0;
+#pragma unroll
+    for (int q = 0; q < L; ++q) S += sP[(i - q) * L + q];
+    return S;
+  });
+}
+
 // phase 2: one CTA per product turns the block carry functions into block carry-ins
 // (bit 2 of bstat).  Carry functions of a block are kill (c0=c1=0), propagate (c0=0,c1=1)
 // or generate (c0=c1=1); thread chunks are composed sequentially, the 1024 chunk results
@@ -1532,8 +1591,9 @@ __device__ __forceinline__ void decode2_body(const DecodeArgs& A, int pidx, int 
   const unsigned G = A.gmask[wi], P = A.pmask[wi];
   const unsigned long long a = (unsigned long long)(G | P), b = G;
   const unsigned long long carries = (a + b + s_wcin[warp]) ^ a ^ b;
-  const unsigned c = (unsigned)((carries >> lane) & 1ull);
-  A.out[(long long)pidx * A.nout + t] += c;
+  // a carry into a limb is rare (w_t's high word is set only when lo(S_t) + hi(S_(t-1))
+  // overflows), so the limbs decode1 wrote are rewritten only where one arrives
+  if ((carries >> lane) & 1ull) A.out[(long long)pidx * A.nout + t] += 1u;
 }
 
 __global__ void __launch_bounds__(kDecThreads) k_decode2(DecodeArgs A) {

@@ -4,27 +4,32 @@
 // A level multiplies element (j, l) of every column by rho^e, e = j * l * base_pow
 // (bigmul/dkss.py:480-492), = alpha^r * rho_table[s] with s = e mod (M/m).  Every element with
 // the same s is multiplied by the SAME ring element t = rho_table[s], and over bytes that is a
-// dense integer matrix product:
+// dense integer matrix product.  Multiplication by a constant mod p is
+// linear in the bytes of the other factor, so the constant is spread over them:
 //
-//   x_i = sum_k X[i][k] 256^k          -- u8 digits: the element's own little-endian bytes
-//   T_l = t_l 2^160 mod p              -- balanced signed base-256 digits D_l[0..16] (s8)
-//   Z[j][d] = sum_{i,k} X[i][k] D_{+-(j-i) mod m}[d-k]      (|Z| < 2^25)
-//   z_j = (sum_d Z[j][d] 256^d) 2^-160 mod p = (x t)_j        (negacyclic: the wrapped terms use
-//                                                              p - T, alpha^m = -1)
+//   x_i = sum_k X[i][k] 256^k                 -- u8 digits: the element's own little-endian bytes
+//   C_l,k = +-t_l 256^k 2^32 mod p            -- in (-p/2, p/2), balanced signed base-256 digits
+//                                                D_l,k[0..15] (s8); the wrapped terms of the
+//                                                negacyclic product are negated (alpha^m = -1)
+//   Z[j][d] = sum_{i,k} X[i][k] D_{j-i,k}[d]  (|Z| < 16 m 255 128 <= 2^24)
+//   z_j = (sum_d Z[j][d] 256^d) 2^-32 mod p = (x t)_j
 //
-// One CTA tile = up to 128 elements sharing s: D[128][32m] (s32, TMEM) += A[128][16m] (u8)
-// x B[32m][16m] (s8).  B is never materialised: with A's 16-byte K chunks in reversed
+// so one ring product is a 16m x 16m byte matrix with no structural zeros (a byte Toeplitz
+// formulation with T = t 2^160 needs 32m output positions, half of them zero bands).
+//
+// One CTA tile = up to 128 elements sharing s: D[128][16m] (s32, TMEM) += A[128][16m] (u8)
+// x B[16m][16m] (s8).  B is never materialised: with A's 16-byte K chunks in reversed
 // coefficient order (chunk i' holds x_{m-1-i'}), B row (j, d), K chunk i' is the 16-byte unit
-// V[j + i'][d] of a per-s table V[2m-1][32][16], so the UMMA descriptor of B is just V read with
-// strides (SBO 128 B between 8-row groups, LBO 512 B between K chunks): 32 KB of shared memory
-// for the whole 32m x 16m Toeplitz operand (m = 32).
+// V[j + i'][d] = (D_{j+i'-m+1,k}[d])_{k<16} of a per-s table V[2m-1][16][16], so the UMMA
+// descriptor of B is just V read with strides (SBO 128 B between 8-row groups, LBO 256 B between
+// K chunks): 16 KB of shared memory for the whole 16m x 16m operand (m = 32).
 //
-// Epilogue (CUDA cores, one thread per element row and coefficient): tcgen05.ld of the 32
-// byte-position sums of a coefficient, folded into a nine-limb non-negative integer with three
-// IMAD.WIDE per limb, five Montgomery REDC steps with R = 2^160 using p = 1 + P3 2^96 (Proth:
-// -p^-1 = -1 mod 2^32, q p touches limbs K, K+3, K+4), one conditional subtraction, then stored
-// at (j + r) mod 2m with the negation of alpha^m = -1 -- the same element the CUDA-core kernels'
-// ring_mul + store_rot produce (tests/test_gpu_parity.py).
+// Epilogue (CUDA cores, one thread per element row and coefficient): tcgen05.ld of the 16
+// byte-position sums of a coefficient, folded into a signed five-limb integer with three
+// IMAD.WIDE per limb, + p 2^17 (non-negative), one Montgomery REDC step with R = 2^32 using
+// p = 1 + P3 2^96 (Proth: -p^-1 = -1 mod 2^32, q p touches limbs 0, 3, 4), one conditional
+// subtraction, then stored at (j + r) mod 2m with the negation of alpha^m = -1 -- the same
+// element the CUDA-core kernels' ring_mul + store_rot produce (tests/test_gpu_parity.py).
 #pragma once
 #include <cstdint>
 #include "dkss_kernels.cuh"
@@ -41,7 +46,7 @@ struct TcArgs {
   uint32_t* poly;            // element index 0 of the launch (elements of MM * 4 words)
   const uint32_t* tiles;     // [ntiles][3]: s, first entry, entry count (<= 128)
   const uint32_t* entries;   // (element index << 6) | alpha shift r (mod 2m)
-  const uint8_t* vtab;       // [M/m][2m - 1][32][16] s8 digits, from the (scaled) twiddle rows
+  const uint8_t* vtab;       // [M/m][2m - 1][16][16] s8 digits, from the (scaled) twiddle rows
   int ntiles;
   uint32_t p3;               // p = 1 + p3 * 2^96
   // fused four-step exchange of the first level (PassArgs::peer_mode 1): element el = q E C + pos
@@ -64,7 +69,7 @@ template <int MM>
 struct TcSmem {
   static constexpr int K = MM * 16;                    // bytes per element (A row)
   static constexpr int ABYTES = kTcRows * K;           // A tile
-  static constexpr int VBYTES = (2 * MM - 1) * 32 * 16;
+  static constexpr int VBYTES = (2 * MM - 1) * 16 * 16;
   static constexpr int VPAD = (VBYTES + 1023) / 1024 * 1024;
   static constexpr int STAGE = ABYTES + VPAD + kTcRows * 4;  // + entries
   static constexpr int BYTES = 2 * STAGE + 1024;             // two stages + alignment slack
@@ -171,71 +176,47 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, int32_t (&v)[32
       : "memory");
 }
 
-// the five Montgomery steps of the epilogue REDC (p = 1 + p3 2^96, so -p^-1 = -1 mod 2^32 and
-// q p = q + q p3 2^96): step K adds q = -t[K] at limb K (clearing it) and q p3 at limbs K+3, K+4,
-// with one carry chain through limb 9
-__device__ __forceinline__ void redc5(uint32_t (&t)[10], uint32_t p3) {
-  {  // step 0: limbs 0..9
-    const uint32_t q = 0u - t[0];
-    asm("add.cc.u32 %0, %0, %10;\n\taddc.cc.u32 %1, %1, 0;\n\taddc.cc.u32 %2, %2, 0;\n\tmadc.lo.cc.u32 %3, %10, %11, %3;\n\tmadc.hi.cc.u32 %4, %10, %11, %4;\n\taddc.cc.u32 %5, %5, 0;\n\taddc.cc.u32 %6, %6, 0;\n\taddc.cc.u32 %7, %7, 0;\n\taddc.cc.u32 %8, %8, 0;\n\taddc.u32 %9, %9, 0;\n"
-        : "+r"(t[0]), "+r"(t[1]), "+r"(t[2]), "+r"(t[3]), "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), "+r"(t[8]), "+r"(t[9])
-        : "r"(q), "r"(p3));
-  }
-  {  // step 1: limbs 1..9
-    const uint32_t q = 0u - t[1];
-    asm("add.cc.u32 %0, %0, %9;\n\taddc.cc.u32 %1, %1, 0;\n\taddc.cc.u32 %2, %2, 0;\n\tmadc.lo.cc.u32 %3, %9, %10, %3;\n\tmadc.hi.cc.u32 %4, %9, %10, %4;\n\taddc.cc.u32 %5, %5, 0;\n\taddc.cc.u32 %6, %6, 0;\n\taddc.cc.u32 %7, %7, 0;\n\taddc.u32 %8, %8, 0;\n"
-        : "+r"(t[1]), "+r"(t[2]), "+r"(t[3]), "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), "+r"(t[8]), "+r"(t[9])
-        : "r"(q), "r"(p3));
-  }
-  {  // step 2: limbs 2..9
-    const uint32_t q = 0u - t[2];
-    asm("add.cc.u32 %0, %0, %8;\n\taddc.cc.u32 %1, %1, 0;\n\taddc.cc.u32 %2, %2, 0;\n\tmadc.lo.cc.u32 %3, %8, %9, %3;\n\tmadc.hi.cc.u32 %4, %8, %9, %4;\n\taddc.cc.u32 %5, %5, 0;\n\taddc.cc.u32 %6, %6, 0;\n\taddc.u32 %7, %7, 0;\n"
-        : "+r"(t[2]), "+r"(t[3]), "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), "+r"(t[8]), "+r"(t[9])
-        : "r"(q), "r"(p3));
-  }
-  {  // step 3: limbs 3..9
-    const uint32_t q = 0u - t[3];
-    asm("add.cc.u32 %0, %0, %7;\n\taddc.cc.u32 %1, %1, 0;\n\taddc.cc.u32 %2, %2, 0;\n\tmadc.lo.cc.u32 %3, %7, %8, %3;\n\tmadc.hi.cc.u32 %4, %7, %8, %4;\n\taddc.cc.u32 %5, %5, 0;\n\taddc.u32 %6, %6, 0;\n"
-        : "+r"(t[3]), "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), "+r"(t[8]), "+r"(t[9])
-        : "r"(q), "r"(p3));
-  }
-  {  // step 4: limbs 4..9
-    const uint32_t q = 0u - t[4];
-    asm("add.cc.u32 %0, %0, %6;\n\taddc.cc.u32 %1, %1, 0;\n\taddc.cc.u32 %2, %2, 0;\n\tmadc.lo.cc.u32 %3, %6, %7, %3;\n\tmadc.hi.cc.u32 %4, %6, %7, %4;\n\taddc.u32 %5, %5, 0;\n"
-        : "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), "+r"(t[8]), "+r"(t[9])
-        : "r"(q), "r"(p3));
-  }
-}
-
-// z = (sum_d Z[d] 256^d) 2^-160 mod p, canonical, for p = 1 + p3 2^96 (L = 4), p3 >= 2^6.
-// The sum is the exact integer sum_i x_i T'_i with x_i < 2^128 (the element's bytes, unsigned)
-// and T'_i in [0, p) (the balanced digits only change how T' is written), so it is in
-// [0, m 2^128 p) subset [0, 2^261): nine limbs.  Five REDC steps give r = (V + Q p) / 2^160 <
-// 2^101 + p < min(2p, 2^128): t[9] ends 0 and one conditional subtraction makes r canonical.
-__device__ __forceinline__ void reduce_coeff(const int32_t (&Z)[32], uint32_t p3, bool neg, uint32_t (&out)[4]) {
-  uint32_t t[10];
-  long long c = 0;
+// z = (sum_{d<16} Z[d] 256^d) 2^-32 mod p, canonical, for p = 1 + p3 2^96 (L = 4) with
+// 2^31 <= p3 < 2^32 - 2^17 (p in (2^127, 2^128 - 2^113)).  |Z[d]| <= 16 m 255 128, so
+// |sum| <= 16 m 128 (256^16 - 1) < m 2^139 <= 2^144 < p 2^17: adding p 2^17 makes it
+// non-negative and < 2^145 (five limbs).  One REDC step (q = -t0, since -p^-1 = -1 mod 2^32;
+// q p = q + q p3 2^96) gives r = (V + q p) / 2^32 < 2^113 + p < min(2p, 2^128), so one
+// conditional subtraction makes r canonical.  `Z` points at 16 consecutive sums.
+template <class Arr>
+__device__ __forceinline__ void reduce_coeff16(const Arr& Z, int z0, uint32_t p3, bool neg, uint32_t (&out)[4]) {
+  uint32_t t0, t1, t2, t3, t4;
+  {
+    long long c = 0;
+    uint32_t t[4];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {  // 64-bit sums of four byte positions, carried into 32-bit limbs
-    long long a = (long long)Z[4 * k];
-    asm("mad.wide.s32 %0, %1, 256, %0;" : "+l"(a) : "r"(Z[4 * k + 1]));
-    asm("mad.wide.s32 %0, %1, 65536, %0;" : "+l"(a) : "r"(Z[4 * k + 2]));
-    asm("mad.wide.s32 %0, %1, 16777216, %0;" : "+l"(a) : "r"(Z[4 * k + 3]));
-    a += c;
-    t[k] = (uint32_t)a;
-    c = a >> 32;
+    for (int k = 0; k < 4; ++k) {  // 64-bit sums of four byte positions, carried into 32-bit limbs
+      long long a = (long long)Z[z0 + 4 * k];
+      asm("mad.wide.s32 %0, %1, 256, %0;" : "+l"(a) : "r"(Z[z0 + 4 * k + 1]));
+      asm("mad.wide.s32 %0, %1, 65536, %0;" : "+l"(a) : "r"(Z[z0 + 4 * k + 2]));
+      asm("mad.wide.s32 %0, %1, 16777216, %0;" : "+l"(a) : "r"(Z[z0 + 4 * k + 3]));
+      a += c;
+      t[k] = (uint32_t)a;
+      c = a >> 32;
+    }
+    t0 = t[0], t1 = t[1], t2 = t[2], t3 = t[3];
+    t4 = (uint32_t)c;  // two's complement top limb (|c| < 2^16)
   }
-  t[8] = (uint32_t)c;
-  t[9] = 0;
-  redc5(t, p3);
-  // r = t[5..8] < 2^101 + p: subtract p once if r >= p; then p - r when `neg` (alpha^m = -1 wrap)
+  // + p 2^17 = 2^17 + p3 2^113: limbs (2^17, 0, 0, p3 << 17, p3 >> 15); then the REDC step
+  const uint32_t q = 0u - (t0 + 0x20000u);
+  asm("add.cc.u32 %0, %0, 0x20000;\n\taddc.cc.u32 %1, %1, 0;\n\taddc.cc.u32 %2, %2, 0;\n\t"
+      "addc.cc.u32 %3, %3, %5;\n\taddc.u32 %4, %4, %6;\n\t"
+      "add.cc.u32 %0, %0, %7;\n\taddc.cc.u32 %1, %1, 0;\n\taddc.cc.u32 %2, %2, 0;\n\t"
+      "madc.lo.cc.u32 %3, %7, %8, %3;\n\tmadc.hi.u32 %4, %7, %8, %4;\n"
+      : "+r"(t0), "+r"(t1), "+r"(t2), "+r"(t3), "+r"(t4)
+      : "r"(p3 << 17), "r"(p3 >> 15), "r"(q), "r"(p3));
+  // r = t1..t4 < 2^113 + p: subtract p once if r >= p; then p - r when `neg` (alpha^m = -1 wrap)
   uint32_t r0, r1, r2, r3, bo;
   asm("sub.cc.u32 %0, %5, 1;\n\tsubc.cc.u32 %1, %6, 0;\n\tsubc.cc.u32 %2, %7, 0;\n\t"
       "subc.cc.u32 %3, %8, %9;\n\tsubc.u32 %4, 0, 0;\n"
       : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3), "=r"(bo)
-      : "r"(t[5]), "r"(t[6]), "r"(t[7]), "r"(t[8]), "r"(p3));
+      : "r"(t1), "r"(t2), "r"(t3), "r"(t4), "r"(p3));
   const bool keep = bo != 0u;  // borrow: r < p
-  const uint32_t c0 = keep ? t[5] : r0, c1 = keep ? t[6] : r1, c2 = keep ? t[7] : r2, c3 = keep ? t[8] : r3;
+  const uint32_t c0 = keep ? t1 : r0, c1 = keep ? t2 : r1, c2 = keep ? t3 : r2, c3 = keep ? t4 : r3;
   uint32_t e0, e1, e2, e3;
   asm("sub.cc.u32 %0, 1, %4;\n\tsubc.cc.u32 %1, 0, %5;\n\tsubc.cc.u32 %2, 0, %6;\n\tsubc.u32 %3, %8, %7;\n"
       : "=r"(e0), "=r"(e1), "=r"(e2), "=r"(e3)
@@ -246,7 +227,6 @@ __device__ __forceinline__ void reduce_coeff(const int32_t (&Z)[32], uint32_t p3
   out[2] = flip ? e2 : c2;
   out[3] = flip ? e3 : c3;
 }
-
 
 }  // namespace tc
 
@@ -260,19 +240,19 @@ __device__ __forceinline__ void reduce_coeff(const int32_t (&Z)[32], uint32_t p3
 //     commits to the buffer's "full" barrier, and after the tile's last chunk to the stage's
 //     "empty" barrier;
 //   epilogue warps (kTcEpiWarps): per chunk, tcgen05.ld of their coefficient columns, release the
-//     TMEM buffer, then reduce (tc::reduce_coeff) and store.
+//     TMEM buffer, then reduce (tc::reduce_coeff16) and store.
 template <int MM>
 __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
   // PDL: the set-up, the first tile's schedule entries and V table (constants of the plan) overlap
   // the tail of the column pass; only the element gather waits for it (griddep_wait below)
   griddep_launch();
   using S = TcSmem<MM>;
-  constexpr int K = S::K, NCH = MM * 32 / kTcNChunk, KSTEPS = K / 32;
+  constexpr int K = S::K, NCH = MM * 16 / kTcNChunk, KSTEPS = K / 32;
   constexpr int SBO_A = MM * 128;      // bytes between 8-row groups of A
-  constexpr int CPC = kTcNChunk / 32;  // coefficients per N chunk
+  constexpr int CPC = kTcNChunk / 16;  // coefficients per N chunk (16 byte positions each)
   constexpr int EW = MM * 4;           // words per element
   constexpr int CPE = CPC / 4;         // coefficients per epilogue warp per chunk (4 lane quadrants)
-  static_assert(kTcEpiWarps == 16 && CPC == 8, "two coefficient columns per epilogue warp per chunk");
+  static_assert(kTcEpiWarps == 16 && CPC == 16 && CPE == 4, "two coefficient pairs per epilogue warp per chunk");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // full[2], empty[2] (smem stages), tfull[2], tempty[2] (TMEM buffers)
@@ -373,7 +353,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
 #pragma unroll
           for (int ks = 0; ks < KSTEPS; ++ks) {
             const uint64_t da = tc::make_desc(a_base + ks * 256, 128, SBO_A);
-            const uint64_t db = tc::make_desc(v_base + (ch * kTcNChunk / 8) * 128 + ks * 1024, 512, 128);
+            const uint64_t db = tc::make_desc(v_base + (ch * kTcNChunk / 8) * 128 + ks * 512, 256, 128);
             tc::mma_i8(tbuf, da, db, idesc, ks > 0 ? 1u : 0u);
           }
           tc::mma_commit(&tfull[b]);
@@ -400,10 +380,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
         tc::fence_after();
         int32_t Z0[32], Z1[32];
         const uint32_t lane_addr = tmem + (uint32_t)(b * kTcNChunk) + ((uint32_t)(32 * quad) << 16);
-        const int cj0 = warp >> 2, cj1 = cj0 + 4;
+        const int pp0 = warp >> 2, pp1 = pp0 + 4;  // coefficient pairs (2 x 16 columns) of this warp
         if (warp_live) {
-          tc::tmem_ld32_nowait(lane_addr + cj0 * 32, Z0);
-          tc::tmem_ld32_nowait(lane_addr + cj1 * 32, Z1);
+          tc::tmem_ld32_nowait(lane_addr + pp0 * 32, Z0);
+          tc::tmem_ld32_nowait(lane_addr + pp1 * 32, Z1);
           asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
         }
         tc::fence_before();
@@ -415,9 +395,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
         if (live) {
 #pragma unroll
           for (int h = 0; h < CPE; ++h) {
-            const int pos = (ch * CPC + (h ? cj1 : cj0) + rot) & (2 * MM - 1);
+            const int cj = 2 * (h < 2 ? pp0 : pp1) + (h & 1);
+            const int pos = (ch * CPC + cj + rot) & (2 * MM - 1);
             uint32_t o[4];
-            tc::reduce_coeff(h ? Z1 : Z0, A.p3, pos >= MM, o);
+            if (h < 2)
+              tc::reduce_coeff16(Z0, 16 * (h & 1), A.p3, pos >= MM, o);
+            else
+              tc::reduce_coeff16(Z1, 16 * (h & 1), A.p3, pos >= MM, o);
             *reinterpret_cast<uint4*>(dst + (pos & (MM - 1)) * 4) = make_uint4(o[0], o[1], o[2], o[3]);
           }
         }
@@ -432,12 +416,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
 }
 
 // V tables of the tensor-core twiddle products: for every table row s, the effective twiddle
-// t = w R^-1 of the stored (Montgomery-form) row w (ring_mul computes REDC(x w)), scaled to
-// T = t 2^160 = w 2^32 = mont_mul(w, 2^160 mod p); V[s][l'][d] = 16 bytes k = 0..15 of the digit
-// at position d - k of (l' >= m-1 ? T_{l'-m+1} : p - T_{l'+1}) in balanced base 256.
+// t = w R^-1 of the stored (Montgomery-form) row w (ring_mul computes REDC(x w)); with
+// ck[k] = 2^(32 + 8k) mod p, C_l,k = t_l 256^k 2^32 = mont_mul(w_l, ck[k]).  V[s][l'][d] = the
+// 16 bytes k = 0..15 of digit d of (l' >= m-1 ? C_{l'-m+1,k} : p - C_{l'+1,k}) written in
+// (-p/2, p/2) with balanced base-256 digits (16 suffice: p/2 < 127 (256^16 - 1) / 255).
 template <int MM>
 __global__ void k_tc_build_v(const uint32_t* __restrict__ twr, long long nrows, uint8_t* __restrict__ vtab, ModCtx mc,
-                             const uint32_t* __restrict__ c160) {
+                             const uint32_t* __restrict__ ck) {
   constexpr int L = 4, LP = 2 * MM - 1;
   const long long n = nrows * LP;
   for (long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x; it < n; it += (long long)gridDim.x * blockDim.x) {
@@ -445,39 +430,52 @@ __global__ void k_tc_build_v(const uint32_t* __restrict__ twr, long long nrows, 
     const int lp = (int)(it % LP);
     const bool pos = lp >= MM - 1;
     const int l = pos ? lp - (MM - 1) : lp + 1;
-    uint32_t w[L], K[L], T[L];
+    uint32_t w[L];
 #pragma unroll
-    for (int q = 0; q < L; ++q) {
-      w[q] = twr[(s * 2 * MM + l) * L + q];
-      K[q] = c160[q];
-    }
-    mont_mul<L>(T, w, K, mc);  // canonical
-    if (!pos) neg_mod_canon<L>(T, T, mc);
-    int8_t dig[17];
-    int carry = 0;
+    for (int q = 0; q < L; ++q) w[q] = twr[(s * 2 * MM + l) * L + q];
+    uint32_t unit[16][4];  // unit[d] = bytes k = 0..15 of digit d
 #pragma unroll
+    for (int d = 0; d < 16; ++d)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) unit[d][q] = 0;
+#pragma unroll 1
     for (int k = 0; k < 16; ++k) {
-      int v = (int)((T[k >> 2] >> (8 * (k & 3))) & 0xFFu) + carry;
-      carry = v >= 128;
-      dig[k] = (int8_t)(v - (carry ? 256 : 0));
-    }
-    dig[16] = (int8_t)carry;
-    uint8_t* out = vtab + (size_t)it * 32 * 16;
-    for (int d = 0; d < 32; ++d) {
-      uint32_t wd[4];
+      uint32_t K[L], T[L];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint32_t v = 0;
+      for (int q = 0; q < L; ++q) K[q] = ck[4 * k + q];
+      mont_mul<L>(T, w, K, mc);  // canonical
+      if (!pos) neg_mod_canon<L>(T, T, mc);
+      // 2T > p (T > (p - 1) / 2): write T - p (two's complement) instead
+      bool gt = (T[L - 1] >> 31) != 0u, decided = gt;  // 2T >= 2^128 > p
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int k = 4 * q + b, x = d - k;
-          const uint32_t byte = (x >= 0 && x <= 16) ? (uint8_t)dig[x] : 0u;
-          v |= byte << (8 * b);
+      for (int q = L - 1; q >= 0; --q) {
+        const uint32_t t2 = (T[q] << 1) | (q ? T[q - 1] >> 31 : 0u);  // limb q of 2T
+        if (!decided && t2 != mc.p[q]) {
+          gt = t2 > mc.p[q];
+          decided = true;
         }
-        wd[q] = v;
       }
-      *reinterpret_cast<uint4*>(out + d * 16) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+      if (gt) {  // T - p mod 2^128
+        unsigned long long br = 0;
+#pragma unroll
+        for (int q = 0; q < L; ++q) {
+          const unsigned long long v = (unsigned long long)T[q] - mc.p[q] - br;
+          T[q] = (uint32_t)v;
+          br = (v >> 63) & 1ull;
+        }
+      }
+      int carry = 0;
+#pragma unroll
+      for (int d = 0; d < 16; ++d) {
+        int v = (int)((T[d >> 2] >> (8 * (d & 3))) & 0xFFu) + carry;
+        carry = v >= 128;
+        const uint32_t byte = (uint8_t)(int8_t)(v - (carry ? 256 : 0));
+        unit[d][k >> 2] |= byte << (8 * (k & 3));
+      }
     }
+    uint4* out = reinterpret_cast<uint4*>(vtab + (size_t)it * 16 * 16);
+#pragma unroll
+    for (int d = 0; d < 16; ++d) out[d] = make_uint4(unit[d][0], unit[d][1], unit[d][2], unit[d][3]);
   }
 }
 
