@@ -1,5 +1,6 @@
 // dkss_capi.cu -- libdkss: plan upload, device workspace, launch sequence, C ABI.
 // See include/dkss.h for the contract and DESIGN.md for the kernel/roofline story.
+#include <cuda.h>  // CUtensorMap types only: the encoder is fetched through cudaGetDriverEntryPoint
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -257,6 +258,7 @@ struct dkss_plan {
   bool tc_forced = false;           // DKSS_TWIDDLE_TENSOR: every full-layout launch uses them
   int tc_grid = 0;                  // SMs (one tensor-core CTA per SM)
   uint32_t tc_p3 = 0;               // p = 1 + tc_p3 * 2^96
+  std::map<const void*, TcTensorMap> tc_tmaps;  // TMA descriptors of the element buffers seen (tc_tensor_map)
   uint8_t* d_vtab = nullptr;        // V tables of d_twr rows, [M/m][2m-1][16][16]
   uint8_t* d_vtab_s = nullptr;      // of the pre-scaled rows d_twr_s (last inverse level)
   std::map<std::tuple<int, long long, bool, int, int>, TcSched> tc_sched;  // by TcLayout
@@ -601,13 +603,58 @@ int tc_prepare(dkss_plan* P, int batch, bool sq) {
 // the table twiddles of one launch on the tensor cores, in place (scaled: the last inverse
 // level); with g->peer_mode == 1 (the fused four-step exchange of the first level) the products
 // are stored into the row owners' buffers instead
+// The tensor-core kernel gathers its element rows with TMA (cp.async.bulk.tensor ... tile::gather4):
+// a 2-D byte tensor [rows][16 m] over the launch's elements, box 128 B x 1 row, 128-byte swizzle.
+// The row bound is nominal (the schedule's entries index inside the caller's buffer).
+int tc_tensor_map(dkss_plan* P, uint32_t* poly, TcTensorMap* out) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode enc = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return (Encode)fn;
+  }();
+  if (!enc) return fail(DKSS_ECUDA, "cuTensorMapEncodeTiled is not available from this driver");
+  static_assert(sizeof(TcTensorMap) == sizeof(CUtensorMap), "tensor map size");
+  auto it = P->tc_tmaps.find(poly);
+  if (it != P->tc_tmaps.end()) {
+    *out = it->second;
+    return 0;
+  }
+  const cuuint64_t row_bytes = (cuuint64_t)P->m * P->L * 4;
+  const cuuint64_t gdim[2] = {row_bytes, (cuuint64_t)1 << 26};
+  const cuuint64_t gstride[1] = {row_bytes};
+  const cuuint32_t box[2] = {128, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  CUtensorMap tm;
+  const CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, poly, gdim, gstride, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DKSS_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  memcpy(out, &tm, sizeof(tm));
+  if (P->tc_tmaps.size() >= 64) P->tc_tmaps.clear();
+  P->tc_tmaps[poly] = *out;
+  return 0;
+}
+
 int launch_tc_layout(dkss_plan* P, uint32_t* poly, const TcLayout& lay, bool scaled, cudaStream_t s,
                      const Geom* peer = nullptr) {
   const TcSched* sc;
   int rc;
   if ((rc = tc_sched(P, lay, &sc))) return rc;
   if (!sc->ntiles) return 0;
-  TcArgs A{poly, sc->d_tiles, sc->d_entries, scaled ? P->d_vtab_s : P->d_vtab, sc->ntiles, P->tc_p3};
+  TcArgs A{};
+  if ((rc = tc_tensor_map(P, poly, &A.tmap))) return rc;
+  A.poly = poly;
+  A.tiles = sc->d_tiles;
+  A.entries = sc->d_entries;
+  A.vtab = scaled ? P->d_vtab_s : P->d_vtab;
+  A.ntiles = sc->ntiles;
+  A.p3 = P->tc_p3;
   if (peer && peer->peer_mode == 1) {
     A.peer = peer->peer;
     A.peer_log_r = peer->peer_log_r;

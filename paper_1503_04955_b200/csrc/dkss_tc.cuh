@@ -39,10 +39,17 @@ namespace dkss {
 constexpr int kTcRows = 128;     // UMMA M
 constexpr int kTcNChunk = 256;   // UMMA N per instruction and per TMEM buffer
 constexpr int kTcEpiWarps = 16;  // epilogue: 4 per TMEM lane quadrant
-constexpr int kTcProdWarps = 2;  // smem producers (element gather + V bulk copy)
+constexpr int kTcProdWarps = 4;  // smem producers (TMA row gather of the elements + V bulk copy)
 constexpr int kTcThreads = (kTcEpiWarps + kTcProdWarps + 1) * 32;  // + one MMA-issue warp
 
+// CUtensorMap of the launch's elements as a 2-D byte tensor [elements][16 m], box 128 B x 1 row,
+// 128-byte swizzle (encoded on the host, csrc/dkss_capi.cu tc_tensor_map)
+struct alignas(64) TcTensorMap {
+  unsigned long long v[16];
+};
+
 struct TcArgs {
+  TcTensorMap tmap;          // over `poly`
   uint32_t* poly;            // element index 0 of the launch (elements of MM * 4 words)
   const uint32_t* tiles;     // [ntiles][3]: s, first entry, entry count (<= 128)
   const uint32_t* entries;   // (element index << 6) | alpha shift r (mod 2m)
@@ -68,12 +75,31 @@ __device__ __forceinline__ uint32_t* tc_dst(const TcArgs& A, uint32_t el, int ew
 template <int MM>
 struct TcSmem {
   static constexpr int K = MM * 16;                    // bytes per element (A row)
+  static constexpr int KBLOCKS = K / 128;              // 128-byte K blocks of [128 rows][128 B], swizzled
+  static constexpr int KBBYTES = kTcRows * 128;
   static constexpr int ABYTES = kTcRows * K;           // A tile
   static constexpr int VBYTES = (2 * MM - 1) * 16 * 16;
   static constexpr int VPAD = (VBYTES + 1023) / 1024 * 1024;
-  static constexpr int STAGE = ABYTES + VPAD + kTcRows * 4;  // + entries
-  static constexpr int BYTES = 2 * STAGE + 1024;             // two stages + alignment slack
+  // three A stages (a gather is issued two tiles ahead of its MMAs: its latency is longer than one
+  // tile's MMAs), two V stages (a table is 1/4 of an A tile and arrives by one bulk copy)
+  static constexpr int ASTAGES = 3, VSTAGES = 2;
+  static constexpr int VOFF = ASTAGES * ABYTES;
+  static constexpr int BYTES = ASTAGES * ABYTES + VSTAGES * VPAD + 1024;  // + alignment slack
 };
+
+#ifdef DKSS_TC_TRACE  // experiment builds only: SM-clock stamps of CTA 0's roles (tools/tc_trace.py)
+// [launch % 8][role: 0 producer, 1 MMA, 2 epilogue warp 0][event]
+static __device__ unsigned long long g_tc_trace[8][3][512];
+static __device__ unsigned int g_tc_launch;
+#define TC_STAMP(role, idx)                                                            \
+  do {                                                                                 \
+    if (blockIdx.x == 0 && (idx) < 512) g_tc_trace[trace_slot][role][idx] = clock64(); \
+  } while (0)
+#else
+#define TC_STAMP(role, idx) \
+  do {                      \
+  } while (0)
+#endif
 
 namespace tc {
 
@@ -89,6 +115,28 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;  // descriptor version 1
   return d;
+}
+
+// K-major operand in the 128-byte-swizzle layout (rows of 128 B, 8-row atoms of 1024 B)
+__device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                  // leading byte offset: unused with a swizzled K-major operand
+  d |= (uint64_t)(1024 >> 4) << 32;        // stride between 8-row atoms
+  d |= (uint64_t)1 << 46;                  // descriptor version 1
+  d |= (uint64_t)2 << 61;                  // SWIZZLE_128B
+  return d;
+}
+
+// TMA row gather: rows r0..r3 of the 2-D tensor, 128 bytes each starting at byte column c0, into
+// four consecutive 128-byte rows of a swizzled K block
+__device__ __forceinline__ void tma_gather4(void* sdst, const void* tmap, int c0, int r0, int r1, int r2, int r3,
+                                            uint64_t* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];\n" ::"r"(smem_u32(sdst)),
+      "l"(tmap), "r"(smem_u32(mbar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
 }
 
 // kind::i8 instruction descriptor: D s32 (bits 4-5 = 2), A u8 (7-9 = 0), B s8 (10-12 = 1),
@@ -146,7 +194,11 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t 
 }
 
 __device__ __forceinline__ void cp16(void* sdst, const void* gsrc, bool valid) {
+#ifdef DKSS_TC_CA
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(sdst)), "l"(gsrc),
+#else
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(sdst)), "l"(gsrc),
+#endif
                "r"(valid ? 16 : 0)
                : "memory");
 }
@@ -175,6 +227,18 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, int32_t (&v)[32
       : "r"(taddr)
       : "memory");
 }
+
+// 16 columns (one coefficient's byte-position sums) of this lane's row, no wait
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, int32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 // z = (sum_{d<16} Z[d] 256^d) 2^-32 mod p, canonical, for p = 1 + p3 2^96 (L = 4) with
 // 2^31 <= p3 < 2^32 - 2^17 (p in (2^127, 2^128 - 2^113)).  |Z[d]| <= 16 m 255 128, so
@@ -242,26 +306,27 @@ __device__ __forceinline__ void reduce_coeff16(const Arr& Z, int z0, uint32_t p3
 //   epilogue warps (kTcEpiWarps): per chunk, tcgen05.ld of their coefficient columns, release the
 //     TMEM buffer, then reduce (tc::reduce_coeff16) and store.
 template <int MM>
-__global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
+__global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(const __grid_constant__ TcArgs A) {
   // PDL: the set-up, the first tile's schedule entries and V table (constants of the plan) overlap
   // the tail of the column pass; only the element gather waits for it (griddep_wait below)
   griddep_launch();
   using S = TcSmem<MM>;
   constexpr int K = S::K, NCH = MM * 16 / kTcNChunk, KSTEPS = K / 32;
-  constexpr int SBO_A = MM * 128;      // bytes between 8-row groups of A
   constexpr int CPC = kTcNChunk / 16;  // coefficients per N chunk (16 byte positions each)
   constexpr int EW = MM * 4;           // words per element
   constexpr int CPE = CPC / 4;         // coefficients per epilogue warp per chunk (4 lane quadrants)
-  static_assert(kTcEpiWarps == 16 && CPC == 16 && CPE == 4, "two coefficient pairs per epilogue warp per chunk");
+  static_assert(kTcEpiWarps == 16 && CPC == 16 && CPE == 4, "four coefficients per epilogue warp per chunk");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  // full[2], empty[2] (smem stages), tfull[2], tempty[2] (TMEM buffers)
-  __shared__ __align__(8) uint64_t bars[8];
+  // full[AS], empty[AS] (A stages; a tile's V table arrives on the same "full"), tfull[2],
+  // tempty[2] (TMEM buffers)
+  constexpr int AS = S::ASTAGES;
+  __shared__ __align__(8) uint64_t bars[2 * AS + 4];
   __shared__ uint32_t tmem_sh;
   uint64_t* full = bars;
-  uint64_t* empty = bars + 2;
-  uint64_t* tfull = bars + 4;
-  uint64_t* tempty = bars + 6;
+  uint64_t* empty = bars + AS;
+  uint64_t* tfull = bars + 2 * AS;
+  uint64_t* tempty = bars + 2 * AS + 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tc::smem_u32(&tmem_sh)),
@@ -269,9 +334,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (threadIdx.x == 32) {
-    for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&full[i], kTcProdWarps * 32 + 1);  // every producer lane + the V expect-tx
+    for (int i = 0; i < AS; ++i) {
+      tc::mbar_init(&full[i], 1);  // one arrival carrying the expected bytes (elements + V table)
       tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&tfull[i], 1);
       tc::mbar_init(&tempty[i], kTcEpiWarps);
     }
@@ -282,129 +349,187 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
   tc::fence_after();
   const uint32_t tmem = tmem_sh;
   const int G = gridDim.x;
+#ifdef DKSS_TC_TRACE
+  const unsigned int trace_slot = g_tc_launch & 7u;
+  int ev = 0;
+  TC_STAMP(warp < kTcEpiWarps ? 2 : warp - kTcEpiWarps == 0 ? 0 : 1, ev++);
+#endif
 
   if (warp >= kTcEpiWarps && warp < kTcEpiWarps + kTcProdWarps) {
     // ===== producers =====
-    // Each lane gathers rows g8 * 8 + (lane & 7) of the tile (g8 = pw, pw + kTcProdWarps, ...),
-    // 16-byte chunks c = 4 i + (lane >> 3).  The tile header and row entries of tile k + 1 are
-    // loaded while tile k's copies are in flight; a tile's "full" barrier is signalled as soon as
-    // its own copies have landed (wait_group 0, proxy fence, arrive).
-    constexpr int GPW = kTcRows / 8 / kTcProdWarps;  // row groups per producer warp
+    // One TMA row-gather instruction moves 4 rows x 128 B (one K block) into the swizzled tile at
+    // full shared-memory width (16-byte cp.async copies cost one shared-memory wavefront each and
+    // starved the MMAs' operand reads).  A tile needs 32 row groups x KBLOCKS of them and a warp
+    // issues one about every 60 clocks, so they are spread over all producer lanes: lane idx =
+    // 32 pw + lane takes row group idx / KBLOCKS, K block idx % KBLOCKS (m = 16: half the lanes).
+    // Rows past the tile's count repeat its first row (their products are never stored); row
+    // groups past the count are skipped.  The tile header and row entries of tile k + 1 are
+    // loaded while tile k's copies fly.
     const int pw = warp - kTcEpiWarps;
-    const int rr = lane & 7, cc = lane >> 3;
-    uint32_t hs = 0, hcnt = 0, ent[GPW];
+    const int pidx = pw * 32 + lane;
+    const uint32_t pgroup = pidx / S::KBLOCKS;
+    const int pkb = pidx % S::KBLOCKS;
+    uint32_t hs = 0, hcnt = 0;
+    int r[4] = {0, 0, 0, 0};
     auto load_tile = [&](int t) {
       const uint32_t first = __ldg(A.tiles + 3 * t + 1);
       hs = __ldg(A.tiles + 3 * t);
       hcnt = __ldg(A.tiles + 3 * t + 2);
 #pragma unroll
-      for (int i = 0; i < GPW; ++i) ent[i] = __ldg(A.entries + first + (pw + i * kTcProdWarps) * 8 + rr) >> 6;
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t row = 4 * pgroup + i;
+        r[i] = (int)(__ldg(A.entries + first + (row < hcnt ? row : 0u)) >> 6);
+      }
     };
-    int k = 0;
+    int k = 0, sa = 0, ua = 0;  // tile count, its A stage k % AS and that stage's use count k / AS
+    int sp = AS - 2, up = -1;   // stage and use count of tile k - 2
     if ((int)blockIdx.x < A.ntiles) load_tile(blockIdx.x);
     for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
-      const int st = k & 1;
-      if (k >= 2) tc::mbar_wait_parity(&empty[st], ((k >> 1) - 1) & 1);
-      uint8_t* sA = smem + st * S::STAGE;
-      uint8_t* sV = sA + S::ABYTES;
-      if (pw == 0 && lane == 0) {
-        tc::mbar_arrive_tx(&full[st], S::VBYTES);
-        tc::bulk_g2s(sV, A.vtab + (size_t)hs * S::VBYTES, S::VBYTES, &full[st]);
-      }
+#ifdef DKSS_TC_TRACE
+      if (pidx == 0) TC_STAMP(0, ev++);  // before the stage wait
+#endif
+      if (k >= AS) tc::mbar_wait_parity(&empty[sa], (ua - 1) & 1);
+#ifdef DKSS_TC_TRACE
+      if (pidx == 0) TC_STAMP(0, ev++);  // stage free
+#endif
+      uint8_t* sA = smem + sa * S::ABYTES;
+      const uint32_t groups = (hcnt + 3) >> 2;
       if (k == 0) griddep_wait();  // the column pass that produced the elements has completed
 #ifndef DKSS_TC_EXP_NOLOAD  // experiment builds only: time the pipeline without the element gather
-#pragma unroll
-      for (int i = 0; i < GPW; ++i) {
-        const int g8 = pw + i * kTcProdWarps;
-        const bool live = (uint32_t)(g8 * 8 + rr) < hcnt;  // rows past the count: zero-filled
-        const uint32_t* src = A.poly + (size_t)(live ? ent[i] : 0u) * EW;
-        uint8_t* dst = sA + g8 * SBO_A + rr * 16;
-#pragma unroll
-        for (int c0 = 0; c0 < MM; c0 += 4) {
-          const int c = c0 + cc;
-          tc::cp16(dst + (MM - 1 - c) * 128, src + c * 4, live);
-        }
-      }
+      if (pgroup < groups)
+        tc::tma_gather4(sA + pkb * S::KBBYTES + pgroup * 512, &A.tmap, pkb * 128, r[0], r[1], r[2], r[3], &full[sa]);
 #endif
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      if (pidx == 0) {
+        // V stage k & 1 was read by tile k - 2: its MMAs have completed when that tile's A stage
+        // is released (the same event the next tile's gather waits for); the expected byte count
+        // may be posted after some of the gathers have completed (tx-count is signed)
+        if (k >= 2) tc::mbar_wait_parity(&empty[sp], up & 1);
+#ifdef DKSS_TC_EXP_NOLOAD
+        tc::mbar_arrive_tx(&full[sa], S::VBYTES);
+#else
+        tc::mbar_arrive_tx(&full[sa], S::VBYTES + groups * 4 * S::K);
+#endif
+        tc::bulk_g2s(smem + S::VOFF + (k & 1) * S::VPAD, A.vtab + (size_t)hs * S::VBYTES, S::VBYTES, &full[sa]);
+      }
       if (t + G < A.ntiles) load_tile(t + G);  // next tile's header and rows, under this tile's copies
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic-proxy writes -> tensor core
-      tc::mbar_arrive(&full[st]);
+#ifdef DKSS_TC_TRACE
+      if (pidx == 0) TC_STAMP(0, ev++);  // copies issued
+#endif
+      if (++sa == AS) sa = 0, ++ua;
+      if (++sp == AS) sp = 0, ++up;
     }
   } else if (warp == kTcEpiWarps + kTcProdWarps) {
     // ===== MMA issuer =====
     if (lane == 0) {
       const uint32_t idesc = tc::make_idesc(kTcRows, kTcNChunk);
-      int k = 0, g = 0;
+      int k = 0, g = 0, sa = 0, ua = 0;
       for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
-        const int st = k & 1;
-        tc::mbar_wait_parity(&full[st], (k >> 1) & 1);
+        TC_STAMP(1, ev++);  // before the "full" wait
+        tc::mbar_wait_parity(&full[sa], ua & 1);
         tc::fence_after();
-        const uint32_t a_base = tc::smem_u32(smem + st * S::STAGE);
-        const uint32_t v_base = a_base + S::ABYTES;
+        TC_STAMP(1, ev++);  // tile in shared memory
+        const uint32_t a_base = tc::smem_u32(smem + sa * S::ABYTES);
+        const uint32_t v_base = tc::smem_u32(smem + S::VOFF + (k & 1) * S::VPAD);
         for (int ch = 0; ch < NCH; ++ch, ++g) {
           const int b = g & 1;
           if (g >= 2) {
             tc::mbar_wait_parity(&tempty[b], ((g >> 1) - 1) & 1);
             tc::fence_after();
           }
+          TC_STAMP(1, ev++);  // TMEM buffer free
           const uint32_t tbuf = tmem + (uint32_t)(b * kTcNChunk);
 #pragma unroll
           for (int ks = 0; ks < KSTEPS; ++ks) {
-            const uint64_t da = tc::make_desc(a_base + ks * 256, 128, SBO_A);
+            const uint64_t da = tc::make_desc_sw128(a_base + (ks >> 2) * S::KBBYTES + (ks & 3) * 32);
             const uint64_t db = tc::make_desc(v_base + (ch * kTcNChunk / 8) * 128 + ks * 512, 256, 128);
             tc::mma_i8(tbuf, da, db, idesc, ks > 0 ? 1u : 0u);
           }
           tc::mma_commit(&tfull[b]);
+          TC_STAMP(1, ev++);  // chunk issued
         }
-        tc::mma_commit(&empty[st]);
+        tc::mma_commit(&empty[sa]);
+        if (++sa == AS) sa = 0, ++ua;
       }
     }
   } else if (warp < kTcEpiWarps) {
     // ===== epilogue =====
+    // Warp (quad, q) owns the four coefficients 4q .. 4q+3 of every chunk (64 TMEM columns) for
+    // the 32 rows of lane quadrant `quad`.
     griddep_wait();  // its stores overwrite elements the previous kernel wrote
-    const int quad = warp & 3;
+    const int quad = warp & 3, q = warp >> 2;
     const int row = 32 * quad + lane;
     int g = 0;
+    // the next tile's header and row entry are loaded a tile ahead
+    uint32_t nfirst = 0, ncnt = 0, nent = 0;
+    if ((int)blockIdx.x < A.ntiles) {
+      nfirst = __ldg(A.tiles + 3 * blockIdx.x + 1);
+      ncnt = __ldg(A.tiles + 3 * blockIdx.x + 2);
+      nent = (uint32_t)row < ncnt ? __ldg(A.entries + nfirst + row) : 0u;
+    }
     for (int t = blockIdx.x; t < A.ntiles; t += G) {
-      const uint32_t first = __ldg(A.tiles + 3 * t + 1), cnt = __ldg(A.tiles + 3 * t + 2);
+      const uint32_t cnt = ncnt, ent = nent;
+      if (t + G < A.ntiles) {
+        nfirst = __ldg(A.tiles + 3 * (t + G) + 1);
+        ncnt = __ldg(A.tiles + 3 * (t + G) + 2);
+        nent = (uint32_t)row < ncnt ? __ldg(A.entries + nfirst + row) : 0u;
+      }
       const bool live = (uint32_t)row < cnt;
       const bool warp_live = (uint32_t)(32 * quad) < cnt;  // warp-uniform
-      const uint32_t ent = live ? __ldg(A.entries + first + row) : 0u;
-      uint32_t* dst = tc_dst(A, ent >> 6, EW);
       const int rot = (int)(ent & 63u);
+      uint32_t* dst = tc_dst(A, ent >> 6, EW);
       for (int ch = 0; ch < NCH; ++ch, ++g) {
         const int b = g & 1;
+#ifdef DKSS_TC_TRACE
+        if (warp == 0 && lane == 0) TC_STAMP(2, ev++);  // before the accumulator wait
+#endif
         tc::mbar_wait_parity(&tfull[b], (g >> 1) & 1);
         tc::fence_after();
-        int32_t Z0[32], Z1[32];
-        const uint32_t lane_addr = tmem + (uint32_t)(b * kTcNChunk) + ((uint32_t)(32 * quad) << 16);
-        const int pp0 = warp >> 2, pp1 = pp0 + 4;  // coefficient pairs (2 x 16 columns) of this warp
+#ifdef DKSS_TC_TRACE
+        if (warp == 0 && lane == 0) TC_STAMP(2, ev++);  // accumulators ready
+#endif
+        // the four coefficients are loaded one ahead: coefficient h + 1's tcgen05.ld is in flight
+        // while coefficient h is reduced and stored (the TMEM read of a chunk takes about as long
+        // as its MMAs, so it must overlap the reduction, not precede it)
+        int32_t Za[16], Zb[16];
+        const uint32_t caddr = tmem + (uint32_t)(b * kTcNChunk) + ((uint32_t)(32 * quad) << 16) + q * 64;
+        const int c0 = ch * CPC + 4 * q;  // first column block of this warp's four
+        auto finish = [&](const int32_t(&Z)[16], int h) {
+#ifdef DKSS_TC_EXP_NOEPI  // experiment builds only: time the pipeline without the reduction
+          if (live && Z[0] == 0x7fffffff) dst[0] = 0u;
+#else
+          const int pos = (MM - 1 - (c0 + h) + rot) & (2 * MM - 1);  // column block cb: coefficient m - 1 - cb
+          uint32_t o[4];
+          tc::reduce_coeff16(Z, 0, A.p3, pos >= MM, o);
+#ifdef DKSS_TC_EXP_NOSTORE  // experiment builds only: the reduction without its stores
+          if (live && (o[0] ^ o[1] ^ o[2] ^ o[3]) == 0x9e3779b9u)
+#else
+          if (live)
+#endif
+            *reinterpret_cast<uint4*>(dst + (pos & (MM - 1)) * 4) = make_uint4(o[0], o[1], o[2], o[3]);
+#endif
+        };
         if (warp_live) {
-          tc::tmem_ld32_nowait(lane_addr + pp0 * 32, Z0);
-          tc::tmem_ld32_nowait(lane_addr + pp1 * 32, Z1);
-          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          tc::tmem_ld16_nowait(caddr, Za);
+          tc::tmem_ld_wait();
+          tc::tmem_ld16_nowait(caddr + 16, Zb);
+          finish(Za, 0);
+          tc::tmem_ld_wait();
+          tc::tmem_ld16_nowait(caddr + 32, Za);
+          finish(Zb, 1);
+          tc::tmem_ld_wait();
+          tc::tmem_ld16_nowait(caddr + 48, Zb);
+          finish(Za, 2);
+          tc::tmem_ld_wait();
         }
         tc::fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&tempty[b]);  // this warp's columns of buffer b are read
-#ifdef DKSS_TC_EXP_NOEPI  // experiment builds only: time the pipeline without the reduction
-        if (live && Z0[0] == 0x7fffffff && Z1[0] == 0x7fffffff) dst[0] = 0u;
-#else
-        if (live) {
-#pragma unroll
-          for (int h = 0; h < CPE; ++h) {
-            const int cj = 2 * (h < 2 ? pp0 : pp1) + (h & 1);
-            const int pos = (ch * CPC + cj + rot) & (2 * MM - 1);
-            uint32_t o[4];
-            if (h < 2)
-              tc::reduce_coeff16(Z0, 16 * (h & 1), A.p3, pos >= MM, o);
-            else
-              tc::reduce_coeff16(Z1, 16 * (h & 1), A.p3, pos >= MM, o);
-            *reinterpret_cast<uint4*>(dst + (pos & (MM - 1)) * 4) = make_uint4(o[0], o[1], o[2], o[3]);
-          }
-        }
+#ifdef DKSS_TC_TRACE
+        if (warp == 0 && lane == 0) TC_STAMP(2, ev++);  // buffer released
+#endif
+        if (warp_live) finish(Zb, 3);
+#ifdef DKSS_TC_TRACE
+        if (warp == 0 && lane == 0) TC_STAMP(2, ev++);  // chunk stored
 #endif
       }
     }
@@ -412,6 +537,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(TcArgs A) {
   if (A.peer) __threadfence_system();  // fused exchange: stores to other GPUs performed
   tc::fence_before();
   __syncthreads();
+#ifdef DKSS_TC_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    g_tc_trace[trace_slot][0][511] = clock64();
+    g_tc_launch = g_tc_launch + 1;
+  }
+#endif
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * kTcNChunk));
 }
 
@@ -473,7 +604,7 @@ __global__ void k_tc_build_v(const uint32_t* __restrict__ twr, long long nrows, 
         unit[d][k >> 2] |= byte << (8 * (k & 3));
       }
     }
-    uint4* out = reinterpret_cast<uint4*>(vtab + (size_t)it * 16 * 16);
+    uint4* out = reinterpret_cast<uint4*>(vtab + (size_t)(s * LP + (LP - 1 - lp)) * 16 * 16);
 #pragma unroll
     for (int d = 0; d < 16; ++d) out[d] = make_uint4(unit[d][0], unit[d][1], unit[d][2], unit[d][3]);
   }
