@@ -238,6 +238,13 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, int32_t (&v)[16
       : "memory");
 }
 
+// 32-byte store (one full sector; a 16-byte store of a 32-byte sector is a partial write)
+__device__ __forceinline__ void st256(uint32_t* p, const uint32_t (&lo)[4], const uint32_t (&hi)[4]) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"l"(p), "r"(lo[0]), "r"(lo[1]), "r"(lo[2]),
+               "r"(lo[3]), "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3])
+               : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 // z = (sum_{d<16} Z[d] 256^d) 2^-32 mod p, canonical, for p = 1 + p3 2^96 (L = 4) with
@@ -459,24 +466,37 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(const __grid_const
     const int quad = warp & 3, q = warp >> 2;
     const int row = 32 * quad + lane;
     int g = 0;
-    // the next tile's header and row entry are loaded a tile ahead
-    uint32_t nfirst = 0, ncnt = 0, nent = 0;
-    if ((int)blockIdx.x < A.ntiles) {
-      nfirst = __ldg(A.tiles + 3 * blockIdx.x + 1);
-      ncnt = __ldg(A.tiles + 3 * blockIdx.x + 2);
-      nent = (uint32_t)row < ncnt ? __ldg(A.entries + nfirst + row) : 0u;
+    // tile headers are loaded two tiles ahead and row entries one tile ahead, so neither of the
+    // dependent loads is waited for
+    uint32_t cnt1 = 0, ent1 = 0, first2 = 0, cnt2 = 0;
+    {
+      const int t0 = blockIdx.x;
+      if (t0 < A.ntiles) {
+        const uint32_t first1 = __ldg(A.tiles + 3 * t0 + 1);
+        cnt1 = __ldg(A.tiles + 3 * t0 + 2);
+        ent1 = (uint32_t)row < cnt1 ? __ldg(A.entries + first1 + row) : 0u;
+      }
+      if (t0 + G < A.ntiles) {
+        first2 = __ldg(A.tiles + 3 * (t0 + G) + 1);
+        cnt2 = __ldg(A.tiles + 3 * (t0 + G) + 2);
+      }
     }
     for (int t = blockIdx.x; t < A.ntiles; t += G) {
-      const uint32_t cnt = ncnt, ent = nent;
-      if (t + G < A.ntiles) {
-        nfirst = __ldg(A.tiles + 3 * (t + G) + 1);
-        ncnt = __ldg(A.tiles + 3 * (t + G) + 2);
-        nent = (uint32_t)row < ncnt ? __ldg(A.entries + nfirst + row) : 0u;
+      const uint32_t cnt = cnt1, ent = ent1;
+      ent1 = (t + G < A.ntiles && (uint32_t)row < cnt2) ? __ldg(A.entries + first2 + row) : 0u;
+      cnt1 = cnt2;
+      if (t + 2 * G < A.ntiles) {
+        first2 = __ldg(A.tiles + 3 * (t + 2 * G) + 1);
+        cnt2 = __ldg(A.tiles + 3 * (t + 2 * G) + 2);
       }
       const bool live = (uint32_t)row < cnt;
       const bool warp_live = (uint32_t)(32 * quad) < cnt;  // warp-uniform
       const int rot = (int)(ent & 63u);
       uint32_t* dst = tc_dst(A, ent >> 6, EW);
+      // column blocks c0 .. c0 + 3 of a chunk hold coefficients m-1-c0 .. m-4-c0: positions P, P-1,
+      // P-2, P-3 (mod 2m) of the rotated element, c0 a multiple of 4.  P odd: (P-1, P) and (P-3, P-2)
+      // are 32-byte sectors; P even: (P-2, P-1) is one, P and P-3 are stored alone.
+      const bool podd = ((MM - 1 + rot) & 1) != 0;
       for (int ch = 0; ch < NCH; ++ch, ++g) {
         const int b = g & 1;
 #ifdef DKSS_TC_TRACE
@@ -488,37 +508,40 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(const __grid_const
         if (warp == 0 && lane == 0) TC_STAMP(2, ev++);  // accumulators ready
 #endif
         // the four coefficients are loaded one ahead: coefficient h + 1's tcgen05.ld is in flight
-        // while coefficient h is reduced and stored (the TMEM read of a chunk takes about as long
-        // as its MMAs, so it must overlap the reduction, not precede it)
+        // while coefficient h is reduced (the TMEM read of a chunk takes about as long as its MMAs,
+        // so it must overlap the reduction, not precede it)
         int32_t Za[16], Zb[16];
         const uint32_t caddr = tmem + (uint32_t)(b * kTcNChunk) + ((uint32_t)(32 * quad) << 16) + q * 64;
         const int c0 = ch * CPC + 4 * q;  // first column block of this warp's four
-        auto finish = [&](const int32_t(&Z)[16], int h) {
-#ifdef DKSS_TC_EXP_NOEPI  // experiment builds only: time the pipeline without the reduction
-          if (live && Z[0] == 0x7fffffff) dst[0] = 0u;
-#else
-          const int pos = (MM - 1 - (c0 + h) + rot) & (2 * MM - 1);  // column block cb: coefficient m - 1 - cb
-          uint32_t o[4];
-          tc::reduce_coeff16(Z, 0, A.p3, pos >= MM, o);
-#ifdef DKSS_TC_EXP_NOSTORE  // experiment builds only: the reduction without its stores
-          if (live && (o[0] ^ o[1] ^ o[2] ^ o[3]) == 0x9e3779b9u)
-#else
-          if (live)
-#endif
-            *reinterpret_cast<uint4*>(dst + (pos & (MM - 1)) * 4) = make_uint4(o[0], o[1], o[2], o[3]);
-#endif
+        const int P = (MM - 1 - c0 + rot) & (2 * MM - 1);
+        uint32_t o0[4], o1[4], o2[4], o3[4];
+        auto reduce = [&](const int32_t(&Z)[16], int h, uint32_t(&o)[4]) {
+          tc::reduce_coeff16(Z, 0, A.p3, ((P - h) & (2 * MM - 1)) >= MM, o);
         };
+        auto at = [&](int h) { return dst + ((P - h) & (MM - 1)) * 4; };
+#if defined(DKSS_TC_EXP_NOEPI) || defined(DKSS_TC_EXP_NOSTORE)  // experiment builds only
+        const bool st = live && P == 0x7fffffff;
+#else
+        const bool st = live;
+#endif
         if (warp_live) {
           tc::tmem_ld16_nowait(caddr, Za);
           tc::tmem_ld_wait();
           tc::tmem_ld16_nowait(caddr + 16, Zb);
-          finish(Za, 0);
+          reduce(Za, 0, o0);
           tc::tmem_ld_wait();
           tc::tmem_ld16_nowait(caddr + 32, Za);
-          finish(Zb, 1);
+          reduce(Zb, 1, o1);
+          if (st) {
+            if (podd)
+              tc::st256(at(1), o1, o0);
+            else
+              *reinterpret_cast<uint4*>(at(0)) = make_uint4(o0[0], o0[1], o0[2], o0[3]);
+          }
           tc::tmem_ld_wait();
           tc::tmem_ld16_nowait(caddr + 48, Zb);
-          finish(Za, 2);
+          reduce(Za, 2, o2);
+          if (st && !podd) tc::st256(at(2), o2, o1);
           tc::tmem_ld_wait();
         }
         tc::fence_before();
@@ -527,7 +550,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(const __grid_const
 #ifdef DKSS_TC_TRACE
         if (warp == 0 && lane == 0) TC_STAMP(2, ev++);  // buffer released
 #endif
-        if (warp_live) finish(Zb, 3);
+        if (warp_live) {
+          reduce(Zb, 3, o3);
+          if (st) {
+            if (podd)
+              tc::st256(at(3), o3, o2);
+            else
+              *reinterpret_cast<uint4*>(at(3)) = make_uint4(o3[0], o3[1], o3[2], o3[3]);
+          }
+        }
 #ifdef DKSS_TC_TRACE
         if (warp == 0 && lane == 0) TC_STAMP(2, ev++);  // chunk stored
 #endif
