@@ -255,23 +255,23 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 // conditional subtraction makes r canonical.  `Z` points at 16 consecutive sums.
 template <class Arr>
 __device__ __forceinline__ void reduce_coeff16(const Arr& Z, int z0, uint32_t p3, bool neg, uint32_t (&out)[4]) {
-  uint32_t t0, t1, t2, t3, t4;
-  {
-    long long c = 0;
-    uint32_t t[4];
+  // signed fold with the negation of the alpha^m = -1 wrap in the multipliers (+-256^k): one
+  // IMAD.WIDE per byte position (register multipliers, so ptxas cannot split them into shift +
+  // high-product + two adds), 64-bit sums of four positions carried into 32-bit limbs
+  const int m0 = neg ? -1 : 1, m1 = m0 * 256, m2 = m0 * 65536, m3 = m0 * 16777216;
+  long long a[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {  // 64-bit sums of four byte positions, carried into 32-bit limbs
-      long long a = (long long)Z[z0 + 4 * k];
-      asm("mad.wide.s32 %0, %1, 256, %0;" : "+l"(a) : "r"(Z[z0 + 4 * k + 1]));
-      asm("mad.wide.s32 %0, %1, 65536, %0;" : "+l"(a) : "r"(Z[z0 + 4 * k + 2]));
-      asm("mad.wide.s32 %0, %1, 16777216, %0;" : "+l"(a) : "r"(Z[z0 + 4 * k + 3]));
-      a += c;
-      t[k] = (uint32_t)a;
-      c = a >> 32;
-    }
-    t0 = t[0], t1 = t[1], t2 = t[2], t3 = t[3];
-    t4 = (uint32_t)c;  // two's complement top limb (|c| < 2^16)
+  for (int k = 0; k < 4; ++k) {
+    asm("mul.wide.s32 %0, %1, %2;" : "=l"(a[k]) : "r"(Z[z0 + 4 * k]), "r"(m0));
+    asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(a[k]) : "r"(Z[z0 + 4 * k + 1]), "r"(m1));
+    asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(a[k]) : "r"(Z[z0 + 4 * k + 2]), "r"(m2));
+    asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(a[k]) : "r"(Z[z0 + 4 * k + 3]), "r"(m3));
   }
+  a[1] += a[0] >> 32;
+  a[2] += a[1] >> 32;
+  a[3] += a[2] >> 32;
+  uint32_t t0 = (uint32_t)a[0], t1 = (uint32_t)a[1], t2 = (uint32_t)a[2], t3 = (uint32_t)a[3];
+  uint32_t t4 = (uint32_t)(a[3] >> 32);  // two's complement top limb (|.| < 2^16)
   // + p 2^17 = 2^17 + p3 2^113: limbs (2^17, 0, 0, p3 << 17, p3 >> 15); then the REDC step
   const uint32_t q = 0u - (t0 + 0x20000u);
   asm("add.cc.u32 %0, %0, 0x20000;\n\taddc.cc.u32 %1, %1, 0;\n\taddc.cc.u32 %2, %2, 0;\n\t"
@@ -280,23 +280,17 @@ __device__ __forceinline__ void reduce_coeff16(const Arr& Z, int z0, uint32_t p3
       "madc.lo.cc.u32 %3, %7, %8, %3;\n\tmadc.hi.u32 %4, %7, %8, %4;\n"
       : "+r"(t0), "+r"(t1), "+r"(t2), "+r"(t3), "+r"(t4)
       : "r"(p3 << 17), "r"(p3 >> 15), "r"(q), "r"(p3));
-  // r = t1..t4 < 2^113 + p: subtract p once if r >= p; then p - r when `neg` (alpha^m = -1 wrap)
+  // r = t1..t4 < 2^113 + p: subtract p once if r >= p (a zero sum gives r = p -> 0)
   uint32_t r0, r1, r2, r3, bo;
   asm("sub.cc.u32 %0, %5, 1;\n\tsubc.cc.u32 %1, %6, 0;\n\tsubc.cc.u32 %2, %7, 0;\n\t"
       "subc.cc.u32 %3, %8, %9;\n\tsubc.u32 %4, 0, 0;\n"
       : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3), "=r"(bo)
       : "r"(t1), "r"(t2), "r"(t3), "r"(t4), "r"(p3));
   const bool keep = bo != 0u;  // borrow: r < p
-  const uint32_t c0 = keep ? t1 : r0, c1 = keep ? t2 : r1, c2 = keep ? t3 : r2, c3 = keep ? t4 : r3;
-  uint32_t e0, e1, e2, e3;
-  asm("sub.cc.u32 %0, 1, %4;\n\tsubc.cc.u32 %1, 0, %5;\n\tsubc.cc.u32 %2, 0, %6;\n\tsubc.u32 %3, %8, %7;\n"
-      : "=r"(e0), "=r"(e1), "=r"(e2), "=r"(e3)
-      : "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(p3));
-  const bool flip = neg && ((c0 | c1 | c2 | c3) != 0u);
-  out[0] = flip ? e0 : c0;
-  out[1] = flip ? e1 : c1;
-  out[2] = flip ? e2 : c2;
-  out[3] = flip ? e3 : c3;
+  out[0] = keep ? t1 : r0;
+  out[1] = keep ? t2 : r1;
+  out[2] = keep ? t3 : r2;
+  out[3] = keep ? t4 : r3;
 }
 
 }  // namespace tc
