@@ -504,13 +504,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(const __grid_const
         // the four coefficients are loaded one ahead: coefficient h + 1's tcgen05.ld is in flight
         // while coefficient h is reduced (the TMEM read of a chunk takes about as long as its MMAs,
         // so it must overlap the reduction, not precede it)
-        int32_t Za[16], Zb[16];
+        int32_t Za[32], Zb[32];
         const uint32_t caddr = tmem + (uint32_t)(b * kTcNChunk) + ((uint32_t)(32 * quad) << 16) + q * 64;
         const int c0 = ch * CPC + 4 * q;  // first column block of this warp's four
         const int P = (MM - 1 - c0 + rot) & (2 * MM - 1);
         uint32_t o0[4], o1[4], o2[4], o3[4];
-        auto reduce = [&](const int32_t(&Z)[16], int h, uint32_t(&o)[4]) {
-          tc::reduce_coeff16(Z, 0, A.p3, ((P - h) & (2 * MM - 1)) >= MM, o);
+        auto reduce = [&](const int32_t(&Z)[32], int z0, int h, uint32_t(&o)[4]) {
+          tc::reduce_coeff16(Z, z0, A.p3, ((P - h) & (2 * MM - 1)) >= MM, o);
         };
         auto at = [&](int h) { return dst + ((P - h) & (MM - 1)) * 4; };
 #if defined(DKSS_TC_EXP_NOEPI) || defined(DKSS_TC_EXP_NOSTORE)  // experiment builds only
@@ -519,23 +519,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(const __grid_const
         const bool st = live;
 #endif
         if (warp_live) {
-          tc::tmem_ld16_nowait(caddr, Za);
+          tc::tmem_ld32_nowait(caddr, Za);
           tc::tmem_ld_wait();
-          tc::tmem_ld16_nowait(caddr + 16, Zb);
-          reduce(Za, 0, o0);
-          tc::tmem_ld_wait();
-          tc::tmem_ld16_nowait(caddr + 32, Za);
-          reduce(Zb, 1, o1);
+          tc::tmem_ld32_nowait(caddr + 32, Zb);  // in flight while the first two are reduced
+          reduce(Za, 0, 0, o0);
+          reduce(Za, 16, 1, o1);
           if (st) {
             if (podd)
               tc::st256(at(1), o1, o0);
             else
               *reinterpret_cast<uint4*>(at(0)) = make_uint4(o0[0], o0[1], o0[2], o0[3]);
           }
-          tc::tmem_ld_wait();
-          tc::tmem_ld16_nowait(caddr + 48, Zb);
-          reduce(Za, 2, o2);
-          if (st && !podd) tc::st256(at(2), o2, o1);
           tc::tmem_ld_wait();
         }
         tc::fence_before();
@@ -545,7 +539,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(const __grid_const
         if (warp == 0 && lane == 0) TC_STAMP(2, ev++);  // buffer released
 #endif
         if (warp_live) {
-          reduce(Zb, 3, o3);
+          reduce(Zb, 0, 2, o2);
+          if (st && !podd) tc::st256(at(2), o2, o1);
+          reduce(Zb, 16, 3, o3);
           if (st) {
             if (podd)
               tc::st256(at(3), o3, o2);
