@@ -481,6 +481,79 @@ __device__ __forceinline__ void dft64_regs(uint32_t* buf, const ModCtx& mc) {
   __syncthreads();
 }
 
+// The first level's column DFT of a freshly encoded operand (m = 32): its inputs are u-bit slices
+// (u <= 56), so every intermediate value is an integer of magnitude < 2^(u + 6) and the whole DFT
+// runs on signed 64-bit integers -- a butterfly is two 64-bit adds instead of an add and a
+// subtract mod p on four limbs -- converted to canonical residues (v or p + v) at the end.
+// Values travel in the low two words of a residue slot.
+template <bool R0>
+__device__ __forceinline__ void bfly_s64(long long& u, long long& v, int r, int k) {
+  long long x = v;
+  if constexpr (!R0) x = __shfl_sync(0xFFFFFFFFu, v, (k - r) & 31);
+  const long long sm = u + x, df = u - x;
+  const bool neg = !R0 && k < r;
+  u = neg ? df : sm;
+  v = neg ? sm : df;
+}
+
+template <int L>
+__device__ __forceinline__ void dft64_regs_enc(uint32_t* buf, const ModCtx& mc) {
+  constexpr int ES = Smem<32, L>::ES;
+  const int w = threadIdx.x >> 5, k = threadIdx.x & 31;
+  long long x[8];
+  auto ld64 = [&](int slot) {
+    const uint2 v = *reinterpret_cast<const uint2*>(buf + slot * ES + k * L);
+    return (long long)(((unsigned long long)v.y << 32) | v.x);
+  };
+  auto st64 = [&](int slot, long long v) {
+    *reinterpret_cast<uint2*>(buf + slot * ES + k * L) = make_uint2((uint32_t)v, (uint32_t)((unsigned long long)v >> 32));
+  };
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = ld64(8 * w + i);
+#pragma unroll
+  for (int a = 0; a < 8; a += 2) bfly_s64<true>(x[a], x[a + 1], 0, k);
+#pragma unroll
+  for (int a = 0; a < 8; a += 4) {
+    bfly_s64<true>(x[a], x[a + 2], 0, k);
+    bfly_s64<false>(x[a + 1], x[a + 3], 16, k);
+  }
+  bfly_s64<true>(x[0], x[4], 0, k);
+  bfly_s64<false>(x[1], x[5], 8, k);
+  bfly_s64<false>(x[2], x[6], 16, k);
+  bfly_s64<false>(x[3], x[7], 24, k);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) st64(8 * w + i, x[i]);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = ld64(w + 8 * i);
+#pragma unroll
+  for (int i = 0; i < 8; i += 2) bfly_s64<false>(x[i], x[i + 1], 4 * w, k);
+#pragma unroll
+  for (int i = 0; i < 8; i += 4) {
+    bfly_s64<false>(x[i], x[i + 2], 2 * w, k);
+    bfly_s64<false>(x[i + 1], x[i + 3], 2 * (w + 8), k);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) bfly_s64<false>(x[i], x[i + 4], w + 8 * i, k);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    // canonical residue of the integer x[i]: x[i] or p + x[i] (|x[i]| < 2^62 << p)
+    const bool ng = x[i] < 0;
+    const uint32_t ext = ng ? 0xFFFFFFFFu : 0u;
+    uint32_t res[L];
+    unsigned long long c = 0;
+#pragma unroll
+    for (int q = 0; q < L; ++q) {
+      const uint32_t xv = q == 0 ? (uint32_t)x[i] : q == 1 ? (uint32_t)((unsigned long long)x[i] >> 32) : ext;
+      c += (unsigned long long)xv + (ng ? mc.p[q] : 0u);
+      res[q] = (uint32_t)c;
+      c >>= 32;
+    }
+    st_res<L>(buf + (w + 8 * i) * ES + k * L, res);
+  }
+  __syncthreads();
+}
+
 // the base-case DFT of the bottom kernel for m = 32, b = 16 (2^24: four groups of 16 elements per
 // 64-element tile, root alpha^4): stages 1-3 exactly as dft64_regs's (same roots), then stage 4
 // (pairs (16g + i, 16g + 8 + i), root alpha^(4i)) after one exchange through shared memory
@@ -899,7 +972,17 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, DO ? 3 : Cfg<MM>::MINB) k_fwd_pas
     TRACE_MARK
     mbar_wait(&bar[st], (k >> 1) & 1);
     TRACE_MARK
-    const uint32_t* xv = kExpNoDft ? buf : column_dft<MM, L, NE>(buf, smem + 2 * STAGE, LOGE, mc);
+    const uint32_t* xv;
+    if constexpr (MM == 32 && NE == 64 && C::NT == 256) {
+      if (enc && A.u <= 56 && !kExpNoDft) {
+        dft64_regs_enc<L>(buf, mc);
+        xv = buf;
+      } else {
+        xv = kExpNoDft ? buf : column_dft<MM, L, NE>(buf, smem + 2 * STAGE, LOGE, mc);
+      }
+    } else {
+      xv = kExpNoDft ? buf : column_dft<MM, L, NE>(buf, smem + 2 * STAGE, LOGE, mc);
+    }
     TRACE_MARK
     for (int it = threadIdx.x; it < NE * TPE; it += NT) {
       const int el = it / TPE, k0 = (it % TPE) * kT;

@@ -18,18 +18,23 @@
 // formulation with T = t 2^160 needs 32m output positions, half of them zero bands).
 //
 // One CTA tile = up to 128 elements sharing s: D[128][16m] (s32, TMEM) += A[128][16m] (u8)
-// x B[16m][16m] (s8).  B is never materialised: with A's 16-byte K chunks in reversed
-// coefficient order (chunk i' holds x_{m-1-i'}), B row (j, d), K chunk i' is the 16-byte unit
-// V[j + i'][d] = (D_{j+i'-m+1,k}[d])_{k<16} of a per-s table V[2m-1][16][16], so the UMMA
-// descriptor of B is just V read with strides (SBO 128 B between 8-row groups, LBO 256 B between
-// K chunks): 16 KB of shared memory for the whole 16m x 16m operand (m = 32).
+// x B[16m][16m] (s8).
+//   A: the elements' own bytes, K = (coefficient c, byte k) in memory order, fetched by TMA row
+//      gathers (tile::gather4: 4 rows x 128 B per instruction) into the 128-byte-swizzle K-major
+//      layout (K blocks of [128 rows][128 B]).
+//   B is never materialised: B row (jj, d), K chunk c is the 16-byte unit W[jj + c][d] of a per-s
+//      table W[2m-1][16][16], W[t] = (D_{m-1-t,k}[d])_{k<16} (negated for the wrapped part), so
+//      the UMMA descriptor of B is just W read with strides (SBO 128 B between 8-row groups, LBO
+//      256 B between K chunks): 16 KB of shared memory for the whole 16m x 16m operand (m = 32).
+//      TMEM column block jj holds coefficient m - 1 - jj.
 //
 // Epilogue (CUDA cores, one thread per element row and coefficient): tcgen05.ld of the 16
-// byte-position sums of a coefficient, folded into a signed five-limb integer with three
-// IMAD.WIDE per limb, + p 2^17 (non-negative), one Montgomery REDC step with R = 2^32 using
-// p = 1 + P3 2^96 (Proth: -p^-1 = -1 mod 2^32, q p touches limbs 0, 3, 4), one conditional
-// subtraction, then stored at (j + r) mod 2m with the negation of alpha^m = -1 -- the same
-// element the CUDA-core kernels' ring_mul + store_rot produce (tests/test_gpu_parity.py).
+// byte-position sums of a coefficient, folded into a signed five-limb integer with one IMAD.WIDE
+// per position (the multipliers +-256^k carry the negation of the rotation's alpha^m = -1 wrap),
+// + p 2^17 (non-negative), one Montgomery REDC step with R = 2^32 using p = 1 + P3 2^96 (Proth:
+// -p^-1 = -1 mod 2^32, q p touches limbs 0, 3, 4), one conditional subtraction, then stored at
+// (j + r) mod 2m -- the same element the CUDA-core kernels' ring_mul + store_rot produce
+// (tests/test_gpu_parity.py).
 #pragma once
 #include <cstdint>
 #include "dkss_kernels.cuh"
@@ -298,14 +303,14 @@ __device__ __forceinline__ void reduce_coeff16(const Arr& Z, int z0, uint32_t p3
 // Grouped twiddle products of one level, in place (see the file comment).  Persistent CTAs walk
 // the tile list with warp-specialised roles and mbarrier pipelines (no CTA-wide barriers in the
 // loop):
-//   producer warps (kTcProdWarps): gather tile k's elements into smem stage k & 1 with 16-byte
-//     cp.async (8 rows x 64 contiguous bytes per instruction: coalesced reads, conflict-free
-//     writes), the tile's V table with one bulk copy; stage reuse waits on the MMA's commit;
+//   producer warps (kTcProdWarps): TMA row gathers of tile k's elements into A stage k % 3, the
+//     tile's W table with one bulk copy into V stage k % 2; stage reuse waits on the MMA's commit;
 //   MMA warp (one thread): per N chunk, waits for a free TMEM buffer, issues the K steps,
 //     commits to the buffer's "full" barrier, and after the tile's last chunk to the stage's
 //     "empty" barrier;
-//   epilogue warps (kTcEpiWarps): per chunk, tcgen05.ld of their coefficient columns, release the
-//     TMEM buffer, then reduce (tc::reduce_coeff16) and store.
+//   epilogue warps (kTcEpiWarps): per chunk, tcgen05.ld of their coefficient columns (two
+//     coefficients ahead of the reduction), release the TMEM buffer, reduce (tc::reduce_coeff16)
+//     and store adjacent coefficients as 32-byte sectors.
 template <int MM>
 __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(const __grid_constant__ TcArgs A) {
   // PDL: the set-up, the first tile's schedule entries and V table (constants of the plan) overlap
@@ -567,11 +572,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_twiddle(const __grid_const
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * kTcNChunk));
 }
 
-// V tables of the tensor-core twiddle products: for every table row s, the effective twiddle
+// W tables of the tensor-core twiddle products: for every table row s, the effective twiddle
 // t = w R^-1 of the stored (Montgomery-form) row w (ring_mul computes REDC(x w)); with
-// ck[k] = 2^(32 + 8k) mod p, C_l,k = t_l 256^k 2^32 = mont_mul(w_l, ck[k]).  V[s][l'][d] = the
-// 16 bytes k = 0..15 of digit d of (l' >= m-1 ? C_{l'-m+1,k} : p - C_{l'+1,k}) written in
-// (-p/2, p/2) with balanced base-256 digits (16 suffice: p/2 < 127 (256^16 - 1) / 255).
+// ck[k] = 2^(32 + 8k) mod p, C_l,k = t_l 256^k 2^32 = mont_mul(w_l, ck[k]).  With l' = 2m-2-t:
+// W[s][t][d] = the 16 bytes k = 0..15 of digit d of (l' >= m-1 ? C_{l'-m+1,k} : p - C_{l'+1,k})
+// written in (-p/2, p/2) with balanced base-256 digits (16 suffice: p/2 < 127 (256^16 - 1) / 255).
 template <int MM>
 __global__ void k_tc_build_v(const uint32_t* __restrict__ twr, long long nrows, uint8_t* __restrict__ vtab, ModCtx mc,
                              const uint32_t* __restrict__ ck) {
