@@ -683,6 +683,81 @@ __device__ __forceinline__ void dft32x4_regs(uint32_t* buf, const ModCtx& mc) {
   __syncthreads();
 }
 
+// dft32x4_regs for the first level of a freshly encoded operand, on signed 64-bit integers (see
+// dft64_regs_enc)
+template <bool R0>
+__device__ __forceinline__ void bfly_s64_16(long long& u, long long& v, int r, int k, int h) {
+  long long x = v;
+  if constexpr (!R0) x = __shfl_sync(0xFFFFFFFFu, v, (h << 4) | ((k - r) & 15));
+  const long long sm = u + x, df = u - x;
+  const bool neg = !R0 && k < r;
+  u = neg ? df : sm;
+  v = neg ? sm : df;
+}
+
+template <int L>
+__device__ __forceinline__ void dft32x4_regs_enc(uint32_t* buf, const ModCtx& mc) {
+  constexpr int ES = Smem<16, L>::ES;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, h = lane >> 4, k = lane & 15;
+  uint32_t* col = buf + (2 * (w >> 2) + h) * 32 * ES;
+  const int b = w & 3;
+  long long x[8];
+  auto ld64 = [&](int slot) {
+    const uint2 v = *reinterpret_cast<const uint2*>(col + slot * ES + k * L);
+    return (long long)(((unsigned long long)v.y << 32) | v.x);
+  };
+  auto st64 = [&](int slot, long long v) {
+    *reinterpret_cast<uint2*>(col + slot * ES + k * L) = make_uint2((uint32_t)v, (uint32_t)((unsigned long long)v >> 32));
+  };
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = ld64(8 * b + i);
+#pragma unroll
+  for (int a = 0; a < 8; a += 2) bfly_s64_16<true>(x[a], x[a + 1], 0, k, h);
+#pragma unroll
+  for (int a = 0; a < 8; a += 4) {
+    bfly_s64_16<true>(x[a], x[a + 2], 0, k, h);
+    bfly_s64_16<false>(x[a + 1], x[a + 3], 8, k, h);
+  }
+  bfly_s64_16<true>(x[0], x[4], 0, k, h);
+  bfly_s64_16<false>(x[1], x[5], 4, k, h);
+  bfly_s64_16<false>(x[2], x[6], 8, k, h);
+  bfly_s64_16<false>(x[3], x[7], 12, k, h);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) st64(8 * b + i, x[i]);
+  __syncthreads();
+#pragma unroll
+  for (int g = 0; g < 2; ++g)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[4 * g + i] = ld64(2 * b + g + 8 * i);
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    const int bp = 2 * b + g;
+    bfly_s64_16<false>(x[4 * g + 0], x[4 * g + 1], 2 * bp, k, h);
+    bfly_s64_16<false>(x[4 * g + 2], x[4 * g + 3], 2 * bp, k, h);
+    bfly_s64_16<false>(x[4 * g + 0], x[4 * g + 2], bp, k, h);
+    bfly_s64_16<false>(x[4 * g + 1], x[4 * g + 3], bp + 8, k, h);
+  }
+#pragma unroll
+  for (int g = 0; g < 2; ++g)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const long long v = x[4 * g + i];
+      const bool ng = v < 0;
+      const uint32_t ext = ng ? 0xFFFFFFFFu : 0u;
+      uint32_t res[L];
+      unsigned long long c = 0;
+#pragma unroll
+      for (int q = 0; q < L; ++q) {
+        const uint32_t xv = q == 0 ? (uint32_t)v : q == 1 ? (uint32_t)((unsigned long long)v >> 32) : ext;
+        c += (unsigned long long)xv + (ng ? mc.p[q] : 0u);
+        res[q] = (uint32_t)c;
+        c >>= 32;
+      }
+      st_res<L>(col + (2 * b + g + 8 * i) * ES + k * L, res);
+    }
+  __syncthreads();
+}
+
 // the column DFT of a pass tile: registers for m = 32 (one 64-element column, 8 warps), the
 // shared-memory ping-pong otherwise; returns the buffer holding the result
 template <int MM, int L, int NE>
@@ -976,6 +1051,13 @@ __global__ void __launch_bounds__(Cfg<MM>::NT, DO ? 3 : Cfg<MM>::MINB) k_fwd_pas
     if constexpr (MM == 32 && NE == 64 && C::NT == 256) {
       if (enc && A.u <= 56 && !kExpNoDft) {
         dft64_regs_enc<L>(buf, mc);
+        xv = buf;
+      } else {
+        xv = kExpNoDft ? buf : column_dft<MM, L, NE>(buf, smem + 2 * STAGE, LOGE, mc);
+      }
+    } else if constexpr (MM == 16 && NE == 128) {
+      if (enc && A.u <= 56 && !kExpNoDft) {
+        dft32x4_regs_enc<L>(buf, mc);
         xv = buf;
       } else {
         xv = kExpNoDft ? buf : column_dft<MM, L, NE>(buf, smem + 2 * STAGE, LOGE, mc);
