@@ -967,14 +967,21 @@ template <int MM, int L, class C = Cfg<MM>>
 __device__ __forceinline__ void cta_encode_tile(const PassArgs& A, long long tile, uint32_t* buf) {
   constexpr int ES = Smem<MM, L>::ES, NT = C::NT, NE = C::NE, COLS = C::COLS;
   constexpr int E = 2 * MM, LOGE = Geo<MM>::LOGE, HALF = MM / 2;
-  for (int it = threadIdx.x; it < NE * MM; it += NT) {
-    const int el = it / MM, k = it % MM;
+  // only the lower m/2 coefficients of an element carry operand bits: those items are spread over
+  // all threads and unrolled, so a thread's operand loads are in flight together; the upper
+  // halves are zero-filled
+  constexpr int ITEMS = NE * HALF;
+#pragma unroll
+  for (int it0 = 0; it0 < ITEMS; it0 += NT) {
+    const int it = it0 + threadIdx.x;
+    if (ITEMS % NT != 0 && it >= ITEMS) break;
+    const int el = it / HALF, k = it % HALF;
     const int c = el / E, j = el % E;
     const long long cg = tile * COLS + c;
     uint32_t out[L];
 #pragma unroll
     for (int q = 0; q < L; ++q) out[q] = 0;
-    if (cg < A.total_cols && k < HALF) {
+    if (cg < A.total_cols) {
       const long long q = cg >> A.log_cpp, cc = cg & ((1LL << A.log_cpp) - 1);
       const long long inst = cc >> A.log_mu, l = cc & ((1LL << A.log_mu) - 1);
       const long long pos = (inst << (A.log_mu_enc + LOGE)) + ((long long)j << A.log_mu_enc) + l + A.l_off;
@@ -985,7 +992,7 @@ __device__ __forceinline__ void cta_encode_tile(const PassArgs& A, long long til
         const int sh = (int)(bit & 31);
         uint32_t src[4];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) src[w] = (w0 + w < A.na) ? __ldg(op + w0 + w) : 0u;
+        for (int w = 0; w < 4; ++w) src[w] = (w0 + w < A.na && 32 * w < sh + A.u) ? __ldg(op + w0 + w) : 0u;
         int rem = A.u;
 #pragma unroll
         for (int w = 0; w < 3 && w < L; ++w) {
@@ -995,7 +1002,12 @@ __device__ __forceinline__ void cta_encode_tile(const PassArgs& A, long long til
         }
       }
     }
-    st_res<L>(buf + (c * E + bitrev_n(j, LOGE)) * ES + k * L, out);
+    uint32_t* slot = buf + (c * E + bitrev_n(j, LOGE)) * ES;
+    st_res<L>(slot + k * L, out);
+    uint32_t zero[L];
+#pragma unroll
+    for (int q = 0; q < L; ++q) zero[q] = 0;
+    st_res<L>(slot + (HALF + k) * L, zero);
   }
 }
 
