@@ -1021,7 +1021,8 @@ int run_mul(dkss_plan* P, int batch, const uint32_t* a, const uint32_t* b, long 
 
 // One product in two parts (the host digits path, run_digits_split): part 0 is operand a's first
 // transform level (fused encode + column DFT; its table twiddles wait for b), part 1 the same for
-// b, then level 0's table twiddles of both polynomials in one launch and the rest of run_mul.
+// b, then level 0's table twiddles of both polynomials in one launch and the rest of run_mul --
+// or, for large operands, each operand's whole forward transform in its own part (below).
 // Same kernels and products as run_mul.
 bool split_ok(const dkss_plan* P) { return P->levels > 0 && !P->rows_cs && !P->dyn_grid; }
 
@@ -1029,6 +1030,19 @@ int run_mul_part(dkss_plan* P, int part, const uint32_t* op, long long nl, uint3
   uint32_t* pa = P->d_poly;
   uint32_t* pb = P->d_poly + P->poly_words;
   int rc;
+  // From 2^23-bit operands on, each part runs its operand's WHOLE forward transform (single-
+  // polynomial tensor-core launches): b's transfer (138 us at 2^24) is much longer than a's first
+  // level (25 us), and the extra device time of the unbatched launches (~40 us at 2^24) is less
+  // than the transfer it hides: dmul(int, int) 880 -> 845 us at 2^24, 3090 -> 2897 us at 2^26;
+  // below that the batched forward wins (2^21: 227 vs 242 us, 2^22: 282 vs 285 us).
+  const bool full_a = P->N >= (1LL << 23) && use_tc(P, 1);
+  if (full_a) {
+    if ((rc = launch_fwd_levels(P, part ? pb : pa, 1, s, op, nullptr, nl, 1))) return rc;
+    if (part == 0) return 0;
+    if ((rc = launch_bottom(P, pa, pb, 1, 1, false, s))) return rc;
+    if ((rc = launch_inv_levels(P, pa, 1, true, s))) return rc;
+    return launch_decode(P, pa, prod, 1, s);
+  }
   if ((rc = launch_fwd_levels(P, part ? pb : pa, 1, s, op, nullptr, nl, 1, 0, 1, nullptr, 2, false))) return rc;
   if (part == 0) return 0;
   if (use_tc(P, 2) && (rc = launch_tc(P, pa, 2, 0, false, s))) return rc;
