@@ -294,33 +294,39 @@ def dmul(a, b, thresholds=None, arena: ScratchArena | None = None) -> Natural:
 
 
 _PIPE_MIN_PAIRS = 64   # batches at least this large run as chunks on two device lanes
-_PIPE_CHUNKS = 2  # measured at 1024 x 2^18: 1 chunk 23.2 ms, 2: 20.1, 4: 20.5, 8: 20.8, 16: 22.0
+# chunks (at least 64 pairs each) dealt round-robin to device lanes; measured at 1024 x 2^18
+# (tools/batch_lanes_probe.py, e2e ms): 2 lanes x 2 chunks 9.8, 2 x 4 9.4, 3 x 6 8.4, 4 x 4 8.7,
+# 4 x 8 8.1, 4 x 16 8.2, 8 x 16 8.3
+_PIPE_CHUNKS = 8
+_PIPE_LANES = 4
 _pipe_pool = None
 
 
 def _pipelined_batch(plan, da, db, digit_bits: int, nc: int) -> np.ndarray:
-    """The batch as _PIPE_CHUNKS chunks on two device plans (own stream and workspace each),
-    driven by two host threads: one chunk's host staging, H2D and D2H overlap the other
-    lane's device work (the C call releases the GIL).  Same products as one batch call."""
+    """The batch as up to _PIPE_CHUNKS chunks on up to _PIPE_LANES device plans (own stream and
+    workspace each), one host thread per lane: a chunk's host staging, H2D and D2H overlap the
+    other lanes' device work (the C call releases the GIL).  Same products as one batch call."""
     global _pipe_pool
     from concurrent.futures import ThreadPoolExecutor
 
-    if _pipe_pool is None:
-        _pipe_pool = ThreadPoolExecutor(max_workers=2, thread_name_prefix="dkss-lane")
     n = len(da)
-    step = -(-n // _PIPE_CHUNKS)
+    nchunks = max(2, min(_PIPE_CHUNKS, n // _PIPE_MIN_PAIRS))
+    lanes = max(1, min(_PIPE_LANES, nchunks))
+    if _pipe_pool is None or _pipe_pool._max_workers < lanes:
+        _pipe_pool = ThreadPoolExecutor(max_workers=lanes, thread_name_prefix="dkss-lane")
+    step = -(-n // nchunks)
     chunks = [(i, min(n, i + step)) for i in range(0, n, step)]
     out = pinned_empty((n, nc))  # the lanes' products land here straight from the device
     device = _device()
 
     def lane_work(lane):
         dpl = device_plan(plan, device, lane)
-        for k in range(lane, len(chunks), 2):
+        for k in range(lane, len(chunks), lanes):
             lo, hi = chunks[k]
             dpl.mul_batch_digits([d[1] for d in da[lo:hi]], [d[2] for d in da[lo:hi]], [d[1] for d in db[lo:hi]],
                                  [d[2] for d in db[lo:hi]], digit_bits, nc, out=out[lo:hi])
 
-    futs = [_pipe_pool.submit(lane_work, lane) for lane in (0, 1)]
+    futs = [_pipe_pool.submit(lane_work, lane) for lane in range(lanes)]
     for f in futs:
         f.result()
     return out
