@@ -55,6 +55,27 @@ int fail(int code, const char* fmt, ...) {
 
 bool knob_on(const char* v) { return v && *v && *v != '0'; }
 
+// Every stream of this library is non-blocking, so nothing orders it after work on the legacy
+// default stream -- and a synchronous cudaMemcpy from pageable host memory may return once the
+// source is staged, before the DMA has landed (CUDA "API synchronization behavior"), as may a
+// cudaMemset.  Plan tables, schedules and counters are therefore uploaded on a private stream that
+// is synchronized before returning (legal while another stream of the thread is being captured,
+// unlike a device-wide synchronize).  Without it a plan's twiddle table was occasionally read
+// half-uploaded: about one fresh large plan in a few hundred gave products that were wrong in
+// every bit until the plan was rebuilt -- found by tools/soak.py.  src == nullptr: zero fill.
+cudaError_t upload_sync(void* dst, const void* src, size_t bytes) {
+  constexpr int kMaxDev = 64;
+  static thread_local cudaStream_t up[kMaxDev] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+  if (!up[dev] && (e = cudaStreamCreateWithFlags(&up[dev], cudaStreamNonBlocking)) != cudaSuccess) return e;
+  e = src ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, up[dev]) : cudaMemsetAsync(dst, 0, bytes, up[dev]);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(up[dev]);
+  return e;
+}
+
 // kernels this library launched (graph replays add their kernel nodes), for dkss_kernel_launches()
 std::atomic<long long> g_launches{0};
 // set while a stream of this thread is being captured into a graph: launches then become graph
@@ -331,7 +352,7 @@ int ensure_ws(dkss_plan* P, int batch) {
   CUCHK(cudaMalloc(&P->d_pmask, (size_t)batch * nwarps * 4));
   CUCHK(cudaMalloc(&P->d_bstat, (size_t)batch * dec_blocks(P) * 4));
   CUCHK(cudaMalloc(&P->d_dyn, (4 + 2 * (size_t)batch * 2 * P->m) * 4));
-  CUCHK(cudaMemset(P->d_dyn, 0, (4 + 2 * (size_t)batch * 2 * P->m) * 4));
+  CUCHK(upload_sync(P->d_dyn, nullptr, (4 + 2 * (size_t)batch * 2 * P->m) * 4));
   P->cap_batch = batch;
   P->ws_bytes = 2 * (size_t)batch * poly_b + 2 * (size_t)batch * P->op_limbs * 4 + (size_t)batch * P->prod_limbs * 4 +
                 (size_t)batch * nwarps * 8 + (size_t)batch * dec_blocks(P) * 4;
@@ -570,8 +591,8 @@ int tc_sched(dkss_plan* P, const TcLayout& lay, const TcSched** out) {
   if (sc.ntiles) {
     CUCHK(cudaMalloc(&sc.d_tiles, tiles.size() * 4));
     CUCHK(cudaMalloc(&sc.d_entries, entries.size() * 4));
-    CUCHK(cudaMemcpy(sc.d_tiles, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice));
-    CUCHK(cudaMemcpy(sc.d_entries, entries.data(), entries.size() * 4, cudaMemcpyHostToDevice));
+    CUCHK(upload_sync(sc.d_tiles, tiles.data(), tiles.size() * 4));
+    CUCHK(upload_sync(sc.d_entries, entries.data(), entries.size() * 4));
   }
   *out = &(P->tc_sched[key] = sc);
   return 0;
@@ -1328,12 +1349,12 @@ int plan_init(dkss_plan* P, const dkss_plan_desc* d, const dkss_plan_opts& opts,
   {
     P->dyn_tiles = !knob_on(DKSS_KNOB("DKSS_NO_DYNTILES"));
     CUCHK(cudaMalloc(&P->d_tick, 2 * kTickSlots * sizeof(unsigned)));
-    CUCHK(cudaMemset(P->d_tick, 0, 2 * kTickSlots * sizeof(unsigned)));
+    CUCHK(upload_sync(P->d_tick, nullptr, 2 * kTickSlots * sizeof(unsigned)));
   }
   // twiddle table -> Montgomery form
   const size_t tw_words = (size_t)(M / m) * m * L;
   cudaError_t e = cudaMalloc(&P->d_tw, tw_words * 4);
-  if (e == cudaSuccess) e = cudaMemcpy(P->d_tw, d->rho_powers, tw_words * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = upload_sync(P->d_tw, d->rho_powers, tw_words * 4);
   if (e == cudaSuccess) {
     count_launch();
     kt.mscale<<<(int)std::min<size_t>((tw_words / L + 255) / 256, 4096), 256, 0, P->stream>>>(P->d_tw, tw_words / L, 0,
@@ -1380,7 +1401,7 @@ int plan_init(dkss_plan* P, const dkss_plan_desc* d, const dkss_plan_opts& opts,
     uint32_t* d_c = nullptr;
     const size_t vbytes = (size_t)(M / m) * kt.tc_vbytes;
     e = cudaMalloc(&d_c, 4 * ck.size());
-    if (e == cudaSuccess) e = cudaMemcpy(d_c, ck.data(), 4 * ck.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = upload_sync(d_c, ck.data(), 4 * ck.size());
     if (e == cudaSuccess) e = cudaMalloc(&P->d_vtab, vbytes);
     if (e == cudaSuccess) e = cudaMalloc(&P->d_vtab_s, vbytes);
     const int gb = (int)std::min<long long>(((long long)(M / m) * (2 * m - 1) + 127) / 128, 4096);
